@@ -1,0 +1,131 @@
+/*
+ * polar_b200.h -- C ABI of the B200 Fast-SSC list-CRC polar decoder.
+ *
+ * Drop-in boundary for the reference's list-decode call
+ *   polaris.listdec.ListDecoder(schedule, list_size)      listdec.py:171-185
+ *   ListDecoder.decode(llr) -> DecodeResult                listdec.py:289-308
+ *   ListDecoder.decode_paths(llr) -> list[PathOutcome]     listdec.py:275-287
+ *   polaris.decode(llr, schedule, list_size)               listdec.py:462-468
+ * (reference root: /root/reference/pkg/src/polaris/).  The reference has no
+ * FFI of its own (pure Python); these entry points are what a ctypes / cffi
+ * binding of that call would bind -- see INTEGRATION.md.
+ *
+ * Plain C types only: no torch or CUDA types cross the boundary (the stream is
+ * an opaque cudaStream_t passed as void*).  All pointers may be host or
+ * device memory; the library detects which.
+ */
+#ifndef POLAR_B200_H
+#define POLAR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PB_API_VERSION 1
+
+/* return codes (0 = success).  The Python layer maps PB_EINVAL to
+ * ValueError (same messages as the reference) and the rest to RuntimeError. */
+#define PB_OK 0
+#define PB_EINVAL -1     /* bad argument: list size, LLR width, schedule ... */
+#define PB_ECUDA -2      /* CUDA runtime error (message via pb_last_error) */
+#define PB_EINTERNAL -3  /* internal invariant violated */
+#define PB_ENOMEM -4     /* device / host allocation failed */
+
+/* schedule op kinds; numbering of schedule.KIND_CODE in the Python package.
+ * Mirrors polaris.schedule.NodeKind (schedule.py:29-41). */
+#define PB_OP_F 0
+#define PB_OP_G 1
+#define PB_OP_COMBINE 2
+#define PB_OP_RATE0 3
+#define PB_OP_RATE1 4
+#define PB_OP_REP 5
+#define PB_OP_SPC 6
+
+/* arithmetic modes */
+#define PB_MODE_F32 0   /* float32 LLRs, float64 path metrics (reference numerics) */
+#define PB_MODE_INT8 1  /* int8 saturating LLRs, integer path metrics */
+
+/* input LLR element types for pb_decode / pb_decode_paths */
+#define PB_IN_F32 0     /* float32 [batch][N]; int8 mode quantises clip(rint(4x),+-127) */
+#define PB_IN_I8 1      /* int8 [batch][N] (int8 mode only) */
+
+/* A polar code: reference polaris.codes.CodeSpec (codes.py:201-265) with its
+ * CrcConfig (codes.py:29-61) flattened. crc_width 0 = no CRC. */
+typedef struct pb_code {
+    int32_t N;               /* block length, power of two, 2..65536 */
+    int32_t k;               /* payload bits (CRC excluded), >= 1 */
+    const uint8_t *frozen_mask; /* [N] host pointer, 1 = frozen */
+    int32_t crc_width;       /* 0, 8, 16 or 32 */
+    uint32_t crc_poly;       /* normal form, implicit leading term */
+    uint32_t crc_init;
+    int32_t crc_reflect;     /* 1 = LSB-first register (IEEE CRC-32 style) */
+    uint32_t crc_xor_out;
+} pb_code;
+
+/* One schedule step: reference polaris.schedule.NodeOp (schedule.py:44-58). */
+typedef struct pb_op {
+    int32_t kind;            /* PB_OP_* */
+    int32_t size;
+    int32_t stage;           /* log2(size) */
+    int32_t side;            /* 0 left / 1 right child of the parent */
+    int32_t spc_truncated;
+} pb_op;
+
+typedef struct pb_handle pb_handle;
+
+/* Build a decoder for (code, schedule, list size) on a CUDA device.
+ * Replaces ListDecoder.__init__ (listdec.py:171-185): validates the list size
+ * (ValueError "list size X must be >= 1"), re-validates the op list against
+ * the schedule grammar (schedule.py:159-201), and uploads the lowered device
+ * program, CRC syndrome tables and payload positions.
+ * list_size: 1..32 (PB_EINVAL above 32 in this version). */
+int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
+              int device, pb_handle **out);
+
+/* Decode `batch` frames.  Replaces ListDecoder.decode (listdec.py:289-308),
+ * batched.  llr: [batch][N] of in_type.  Outputs (each may be NULL):
+ *   info_out   uint8 [batch][k]  payload bits of the chosen path (0/1 bytes)
+ *   crc_ok     uint8 [batch]     DecodeResult.crc_ok
+ *   pm_out     double[batch]     DecodeResult.chosen_pm
+ *   paths_used int32 [batch]     DecodeResult.paths_used
+ * Host buffers: synchronous (staged through device memory on `stream`).
+ * All-device buffers: asynchronous on `stream` (a cudaStream_t; NULL = default).
+ */
+int pb_decode(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *info_out,
+              uint8_t *crc_ok, double *pm_out, int32_t *paths_used, void *stream);
+
+/* Every surviving path of every frame: ListDecoder.decode_paths
+ * (listdec.py:275-287).  codewords: uint8 [batch][list_size][N] (root bit
+ * estimates x, one byte per bit), path_pm double [batch][list_size],
+ * path_crc uint8 [batch][list_size], paths_used int32 [batch]; rows beyond
+ * paths_used[b] are zero.  Host buffers only; synchronous. */
+int pb_decode_paths(pb_handle *h, const void *llr, int in_type, int64_t batch,
+                    uint8_t *codewords, double *path_pm, uint8_t *path_crc,
+                    int32_t *paths_used, void *stream);
+
+/* Release the handle and its device memory. */
+int pb_destroy(pb_handle *h);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char *pb_last_error(void);
+
+/* Launch configuration / storage plan the handle chose, as a JSON string
+ * owned by the handle (valid until pb_destroy). */
+const char *pb_plan_json(pb_handle *h);
+
+/* Kernel launches issued by this handle so far (for launch accounting). */
+int64_t pb_launch_count(pb_handle *h);
+
+/* Device time of the most recent pb_decode's decode kernel, in milliseconds,
+ * measured with CUDA events on the launch stream (0 if unavailable). */
+double pb_last_kernel_ms(pb_handle *h);
+
+/* API version (PB_API_VERSION). */
+int pb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLAR_B200_H */

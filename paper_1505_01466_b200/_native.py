@@ -1,0 +1,102 @@
+"""Loader and in-tree builder for the native decoder library.
+
+``libpolar_b200.so`` (built from ``csrc/`` for sm_100a) exports the C ABI of
+``include/polar_b200.h``.  There is no fallback: if the library is missing or
+fails to load, every decode call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_REPO = os.path.dirname(_PKG)
+CSRC = os.path.join(_PKG, "csrc")
+LIB_DIR = os.path.join(_PKG, "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libpolar_b200.so")
+INCLUDE = os.path.join(_REPO, "include")
+
+NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
+              "-Xcompiler", "-fPIC", "-shared"]
+SOURCES = ["decode_kernel.cu", "runtime.cu"]
+
+# C ABI constants (include/polar_b200.h)
+PB_OK, PB_EINVAL, PB_ECUDA, PB_EINTERNAL, PB_ENOMEM = 0, -1, -2, -3, -4
+PB_MODE_F32, PB_MODE_INT8 = 0, 1
+PB_IN_F32, PB_IN_I8 = 0, 1
+
+EXPORTS = ("pb_create", "pb_decode", "pb_decode_paths", "pb_destroy", "pb_last_error",
+           "pb_plan_json", "pb_launch_count", "pb_last_kernel_ms", "pb_version")
+
+
+class PbCode(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("k", ctypes.c_int32),
+                ("frozen_mask", ctypes.POINTER(ctypes.c_uint8)),
+                ("crc_width", ctypes.c_int32), ("crc_poly", ctypes.c_uint32),
+                ("crc_init", ctypes.c_uint32), ("crc_reflect", ctypes.c_int32),
+                ("crc_xor_out", ctypes.c_uint32)]
+
+
+class PbOp(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("size", ctypes.c_int32), ("stage", ctypes.c_int32),
+                ("side", ctypes.c_int32), ("spc_truncated", ctypes.c_int32)]
+
+
+def build(verbose: bool = False) -> str:
+    """Compile the CUDA sources in-tree for sm_100a (nvcc cross-compiles
+    without a GPU)."""
+    os.makedirs(LIB_DIR, exist_ok=True)
+    cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, *[os.path.join(CSRC, s) for s in SOURCES],
+           "-o", LIB_PATH]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    """The loaded native library (raises if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"native decoder library missing: {LIB_PATH} (run __graft_entry__.build())")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    L.pb_create.restype = i32
+    L.pb_create.argtypes = [ctypes.POINTER(PbCode), ctypes.POINTER(PbOp), i32, i32, i32, i32,
+                            ctypes.POINTER(vp)]
+    L.pb_decode.restype = i32
+    L.pb_decode.argtypes = [vp, vp, i32, i64, vp, vp, vp, vp, vp]
+    L.pb_decode_paths.restype = i32
+    L.pb_decode_paths.argtypes = [vp, vp, i32, i64, vp, vp, vp, vp, vp]
+    L.pb_destroy.restype = i32
+    L.pb_destroy.argtypes = [vp]
+    L.pb_last_error.restype = ctypes.c_char_p
+    L.pb_last_error.argtypes = []
+    L.pb_plan_json.restype = ctypes.c_char_p
+    L.pb_plan_json.argtypes = [vp]
+    L.pb_launch_count.restype = i64
+    L.pb_launch_count.argtypes = [vp]
+    L.pb_last_kernel_ms.restype = ctypes.c_double
+    L.pb_last_kernel_ms.argtypes = [vp]
+    L.pb_version.restype = i32
+    L.pb_version.argtypes = []
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    """Map a C ABI return code to the reference's exception types."""
+    if rc == PB_OK:
+        return
+    msg = (lib().pb_last_error() or b"").decode("utf-8", "replace") or what
+    if rc == PB_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(f"{what}: {msg} (code {rc})")

@@ -1,0 +1,609 @@
+// runtime.cu -- native host runtime behind include/polar_b200.h.
+//
+//   * validates the reference schedule (grammar of schedule.py:159-201) and
+//     lowers it to the device program: root F/G become mode switches for the
+//     never-stored stage n-1, every leaf absorbs the Combines that follow it
+//     (its "chain"), and the active-path count before/after every op is
+//     resolved statically (it does not depend on the data)
+//   * builds the CRC tables: per-u-position syndrome rows (codes.py:127-156 as
+//     an affine GF(2) map) transformed into each leaf's local codeword
+//     coordinates, so a path's CRC state is one uint32 updated per leaf
+//   * plans the per-frame storage (shared memory vs global scratch per alpha
+//     stage), sizes the persistent grid, stages host buffers, times launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/polar_b200.h"
+#include "decoder.cuh"
+
+extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int grid, size_t smem,
+                                        cudaStream_t stream);
+extern "C" cudaError_t pb_occupancy(int mode, size_t smem, int *blocks_per_sm);
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    return fail(PB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define PB_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t _e = (call);                        \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+uint32_t rev_bits(uint32_t v, int w) {
+    uint32_t r = 0;
+    for (int i = 0; i < w; ++i) {
+        r = (r << 1) | (v & 1u);
+        v >>= 1;
+    }
+    return r;
+}
+
+struct Crc {
+    int w;
+    uint32_t poly, init, xor_out;
+    bool reflect;
+    uint32_t mask() const { return w == 32 ? 0xffffffffu : ((1u << w) - 1u); }
+    uint32_t step(uint32_t reg, int b) const {  // codes.py:79-118
+        if (reflect) {
+            uint32_t rp = rev_bits(poly, w);
+            return ((reg ^ (uint32_t)b) & 1u) ? (reg >> 1) ^ rp : reg >> 1;
+        }
+        uint32_t fb = ((reg >> (w - 1)) ^ (uint32_t)b) & 1u;
+        return ((reg << 1) & mask()) ^ (fb ? poly : 0u);
+    }
+    uint32_t start() const { return reflect ? rev_bits(init, w) : init; }
+    // checksum value -> append-order bit vector (bit j = j-th appended bit)
+    uint32_t append_word(uint32_t value) const {  // codes.py:121-124
+        if (reflect) return value & mask();
+        return rev_bits(value & mask(), w);
+    }
+};
+
+struct Handle;
+
+}  // namespace
+
+struct pb_handle {
+    int device = 0, mode = 0, L = 0, N = 0, n = 0, k = 0;
+    pb::Params base{};
+    std::vector<pb::DOp> prog;
+    pb::DOp *d_prog = nullptr;
+    uint32_t *d_msyn = nullptr, *d_info = nullptr;
+    int grid = 0, blocks_per_sm = 0, sms = 0;
+    size_t smem_frame = 0;
+    unsigned char *d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+    // staging (host-buffer calls)
+    void *d_in = nullptr;
+    size_t d_in_cap = 0;
+    unsigned char *d_out = nullptr;
+    size_t d_out_cap = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool timed = false;
+    long long launches = 0;
+    std::string plan_json;
+};
+
+namespace {
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+// grammar walk: node(lo, hi, side) := leaf | F node(lo,mid,0) G node(mid,hi,1) Combine
+bool walk(const pb_op *ops, int n_ops, int &pos, int lo, int hi, int side, std::string &err) {
+    int size = hi - lo, stage = 0;
+    while ((1 << stage) < size) ++stage;
+    if (pos >= n_ops) {
+        err = "schedule ends early";
+        return false;
+    }
+    const pb_op &op = ops[pos];
+    if (op.size != size || op.stage != stage || op.side != side) {
+        err = "op " + std::to_string(pos) + " does not match the schedule grammar";
+        return false;
+    }
+    if (op.kind == PB_OP_RATE0 || op.kind == PB_OP_RATE1 || op.kind == PB_OP_REP || op.kind == PB_OP_SPC) {
+        if (op.kind == PB_OP_SPC && size < 4) {
+            err = "SPC leaf of size " + std::to_string(size) + " (needs >= 4)";
+            return false;
+        }
+        ++pos;
+        return true;
+    }
+    if (op.kind != PB_OP_F || size < 2) {
+        err = "op " + std::to_string(pos) + ": expected F or a leaf";
+        return false;
+    }
+    ++pos;
+    int mid = lo + size / 2;
+    if (!walk(ops, n_ops, pos, lo, mid, 0, err)) return false;
+    if (pos >= n_ops || ops[pos].kind != PB_OP_G || ops[pos].size != size || ops[pos].side != side) {
+        err = "op " + std::to_string(pos) + ": expected G " + std::to_string(size);
+        return false;
+    }
+    ++pos;
+    if (!walk(ops, n_ops, pos, mid, hi, 1, err)) return false;
+    if (pos >= n_ops || ops[pos].kind != PB_OP_COMBINE || ops[pos].size != size || ops[pos].side != side) {
+        err = "op " + std::to_string(pos) + ": expected Combine " + std::to_string(size);
+        return false;
+    }
+    ++pos;
+    return true;
+}
+
+int n_cands(int kind, int size, int L) {
+    if (kind == PB_OP_RATE0) return 1;
+    if (kind == PB_OP_REP || (kind == PB_OP_RATE1 && size == 1)) return 2;
+    if (kind == PB_OP_RATE1) return 4;
+    return L != 2 ? 8 : 2;  // SPC, listdec.py:387
+}
+
+int align_up(int x, int a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" {
+
+const char *pb_last_error(void) { return g_err.c_str(); }
+int pb_version(void) { return PB_API_VERSION; }
+
+int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode, int device,
+              pb_handle **out) {
+    g_err.clear();
+    if (!out || !code || !ops) return fail(PB_EINVAL, "null argument");
+    *out = nullptr;
+    if (list_size < 1) return fail(PB_EINVAL, "list size " + std::to_string(list_size) + " must be >= 1");
+    if (list_size > pb::kMaxL)
+        return fail(PB_EINVAL, "list size " + std::to_string(list_size) + " exceeds the supported maximum 32");
+    if (mode != PB_MODE_F32 && mode != PB_MODE_INT8) return fail(PB_EINVAL, "unknown mode");
+    const int N = code->N;
+    if (N < 2 || (N & (N - 1)) || N > (1 << pb::kMaxLog))
+        return fail(PB_EINVAL, "block length " + std::to_string(N) + " is not a power of two in [2, 65536]");
+    int n = 0;
+    while ((1 << n) < N) ++n;
+    if (!code->frozen_mask) return fail(PB_EINVAL, "frozen mask missing");
+    const int w = code->crc_width;
+    if (w != 0 && w != 8 && w != 16 && w != 32) return fail(PB_EINVAL, "unsupported CRC width");
+    std::vector<int> info;
+    for (int i = 0; i < N; ++i)
+        if (!code->frozen_mask[i]) info.push_back(i);
+    if (code->k < 1 || code->k + w != (int)info.size())
+        return fail(PB_EINVAL, "payload + CRC does not match the unfrozen positions");
+    {
+        int pos = 0;
+        std::string err;
+        if (!walk(ops, n_ops, pos, 0, N, 0, err)) return fail(PB_EINVAL, "invalid schedule: " + err);
+        if (pos != n_ops) return fail(PB_EINVAL, "invalid schedule: trailing ops");
+    }
+
+    pb_handle *h = new pb_handle();
+    h->device = device;
+    h->mode = mode;
+    h->L = list_size;
+    h->N = N;
+    h->n = n;
+    h->k = code->k;
+    const int L = list_size;
+
+    // ---- CRC syndrome rows per u position (affine map of codes.py:127-156)
+    std::vector<uint32_t> Hu(N, 0u);
+    uint32_t crc_const = 0;
+    if (w) {
+        Crc crc{w, code->crc_poly, code->crc_init, code->crc_xor_out, code->crc_reflect != 0};
+        const int k = code->k;
+        uint32_t v = crc.step(0u, 1);  // injection of one input bit
+        for (int j = k - 1; j >= 0; --j) {
+            Hu[info[j]] = crc.append_word(v);
+            v = crc.step(v, 0);
+        }
+        uint32_t reg = crc.start();
+        for (int j = 0; j < k; ++j) reg = crc.step(reg, 0);
+        crc_const = crc.append_word(reg ^ crc.xor_out);
+        for (int j = 0; j < w; ++j) Hu[info[k + j]] = 1u << j;
+    }
+
+    // ---- lower the schedule
+    std::vector<uint32_t> M = Hu;
+    int P = 1, vstate = pb::VM_F, leaf_off = 0, final_op = -1, max_hard = 1;
+    for (int i = 0; i < n_ops; ++i) {
+        const pb_op &op = ops[i];
+        pb::DOp d{};
+        if (op.kind == PB_OP_F || op.kind == PB_OP_G) {
+            if (op.stage == n) {
+                vstate = op.kind == PB_OP_F ? pb::VM_F : pb::VM_G;
+                d.kind = pb::DK_NOP;
+            } else {
+                d.kind = op.kind == PB_OP_F ? pb::DK_F : pb::DK_G;
+                d.vmode = op.stage == n - 1 ? (int8_t)vstate : (int8_t)pb::VM_NONE;
+            }
+            d.stage = (int8_t)op.stage;
+            d.pin = (int8_t)P;
+            d.pout = (int8_t)P;
+            h->prog.push_back(d);
+            continue;
+        }
+        if (op.kind == PB_OP_COMBINE) {
+            delete h;
+            return fail(PB_EINVAL, "invalid schedule: Combine not preceded by a right-child leaf");
+        }
+        const int t = op.stage, m = op.size;
+        const int C = n_cands(op.kind, m, L);
+        d.kind = op.kind == PB_OP_RATE0 ? pb::DK_R0
+                 : op.kind == PB_OP_REP ? pb::DK_REP
+                 : op.kind == PB_OP_RATE1 ? pb::DK_R1
+                                          : pb::DK_SPC;
+        d.stage = (int8_t)t;
+        d.pin = (int8_t)P;
+        d.ncand = (int8_t)C;
+        const int pout = op.kind == PB_OP_RATE0 ? P : std::min(L, P * C);
+        d.pout = (int8_t)pout;
+        d.select = (int8_t)(op.kind != PB_OP_RATE0 && P * C > L);
+        d.vmode = t == n - 1 ? (int8_t)vstate : (int8_t)pb::VM_NONE;
+        d.off = leaf_off;
+        if ((op.kind == PB_OP_RATE1 && m > 1) || op.kind == PB_OP_SPC) max_hard = std::max(max_hard, m);
+        // chain of Combines absorbed by this leaf
+        int target = t;
+        if (op.side == 1) {
+            int j = i + 1;
+            for (;;) {
+                if (j >= n_ops || ops[j].kind != PB_OP_COMBINE || ops[j].stage != target + 1) {
+                    delete h;
+                    return fail(PB_EINVAL, "invalid schedule: broken Combine chain");
+                }
+                target = ops[j].stage;
+                int sd = ops[j].side;
+                ++j;
+                if (sd == 0 || target == n) break;
+            }
+            i = j - 1;
+        }
+        d.target = (int8_t)target;
+        leaf_off += m;
+        P = pout;
+        final_op = (int)h->prog.size();
+        h->prog.push_back(d);
+    }
+    // leaf-local subset transform of the syndrome rows:
+    // M[o + j] = XOR_{i subset of j} Hu[o + i]  (u = beta G_m, G_m involution)
+    for (auto &d : h->prog) {
+        if (d.kind < pb::DK_R0 || d.kind > pb::DK_SPC) continue;
+        const int m = 1 << d.stage, o = d.off;
+        for (int hb = 1; hb < m; hb <<= 1)
+            for (int j = 0; j < m; ++j)
+                if (j & hb) M[o + j] ^= M[o + (j ^ hb)];
+    }
+    for (auto &d : h->prog) {
+        if (d.kind != pb::DK_REP && !(d.kind == pb::DK_R1 && d.stage == 0)) continue;
+        uint32_t s = 0;
+        for (int j = 0; j < (1 << d.stage); ++j) s ^= M[d.off + j];
+        d.rep_syn = s;
+    }
+
+    // ---- storage plan
+    const int es = mode == PB_MODE_F32 ? 4 : 1;
+    pb::FrameLayout &lay = h->base.lay;
+    int off = 0;
+    lay.ch_off = off;
+    off = align_up(off + N * es, 16);
+    for (int s = 0; s < n; ++s) {
+        int words = std::max(1, (1 << s) / 32);
+        lay.b_stride[s] = words > 1 ? words + 1 : 1;
+        lay.b_off[s] = off;
+        off = align_up(off + L * lay.b_stride[s] * 4, 16);
+    }
+    lay.pm_off = off;
+    off = align_up(off + 2 * L * 8, 16);
+    lay.syn_off = off;
+    off = align_up(off + 2 * L * 4, 16);
+    lay.idx_stride = n <= 16 ? 16 : 32;
+    lay.ia_off = off;
+    off = align_up(off + 2 * L * lay.idx_stride, 16);
+    lay.ib_off = off;
+    off = align_up(off + 2 * L * lay.idx_stride, 16);
+    lay.cd_off = off;
+    off = align_up(off + L * pb::kMaxCand * 8, 16);
+    lay.clrb_off = off;
+    off = align_up(off + L * 4 * 2, 16);
+    lay.chs_off = off;
+    off = align_up(off + L * 4, 16);
+    lay.cflag_off = off;
+    off = align_up(off + L, 16);
+    lay.asg_off = off;
+    off = align_up(off + 2 * L, 16);
+    lay.hard_words = std::max(1, max_hard / 32);
+    lay.hard_off = off;
+    off = align_up(off + L * lay.hard_words * 4, 16);
+    lay.root_words = std::max(1, N / 32);
+    lay.root_off = off;
+    off = align_up(off + lay.root_words * 4, 16);
+
+    const int smem_cap = 227 * 1024;
+    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", mode == PB_MODE_F32 ? 3 : 6));
+    const int budget = std::max(off, env_int("PB_SMEM_BUDGET", smem_cap / target_fps - 1024));
+    // alpha stages s = 0 .. n-2, lowest stages first into shared memory
+    int s_global = n - 1;  // stages >= s_global go to global scratch
+    for (int s = 0; s <= n - 2; ++s) {
+        int stride = es == 4 ? (1 << s) + 1 : (1 << s) + 4;
+        int bytes = align_up(L * stride * es, 16);
+        if (off + bytes > budget) {
+            s_global = s;
+            break;
+        }
+        lay.a_off[s] = off;
+        lay.a_stride[s] = stride;
+        off += bytes;
+    }
+    lay.a_gfrom = s_global;
+    int goff = 0;
+    for (int s = s_global; s <= n - 2; ++s) {
+        lay.a_off[s] = goff;
+        lay.a_stride[s] = std::max(1 << s, 32 / es);
+        goff = align_up(goff + L * lay.a_stride[s] * es, 256);
+    }
+    lay.gbytes = goff;
+    lay.smem_bytes = align_up(off, 16);
+    if (lay.smem_bytes > smem_cap) {
+        delete h;
+        return fail(PB_EINVAL, "code too large for the per-frame shared-memory plan (" +
+                                   std::to_string(lay.smem_bytes) + " bytes)");
+    }
+    h->smem_frame = lay.smem_bytes;
+
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_fail(e, "cudaSetDevice");
+    }
+    cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+    e = pb_occupancy(mode, h->smem_frame, &h->blocks_per_sm);
+    if (e != cudaSuccess || h->blocks_per_sm < 1) {
+        delete h;
+        return cuda_fail(e == cudaSuccess ? cudaErrorInvalidConfiguration : e, "occupancy");
+    }
+    h->grid = h->sms * h->blocks_per_sm;
+
+    // ---- device tables
+    if ((e = cudaMalloc(&h->d_prog, sizeof(pb::DOp) * h->prog.size())) != cudaSuccess ||
+        (e = cudaMalloc(&h->d_msyn, sizeof(uint32_t) * N)) != cudaSuccess ||
+        (e = cudaMalloc(&h->d_info, sizeof(uint32_t) * std::max(1, code->k))) != cudaSuccess) {
+        pb_destroy(h);
+        return cuda_fail(e, "cudaMalloc tables");
+    }
+    std::vector<uint32_t> info_k(info.begin(), info.begin() + code->k);
+    cudaMemcpy(h->d_prog, h->prog.data(), sizeof(pb::DOp) * h->prog.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(h->d_msyn, M.data(), sizeof(uint32_t) * N, cudaMemcpyHostToDevice);
+    cudaMemcpy(h->d_info, info_k.data(), sizeof(uint32_t) * code->k, cudaMemcpyHostToDevice);
+    if (lay.gbytes) {
+        h->scratch_bytes = (size_t)h->grid * lay.gbytes;
+        if ((e = cudaMalloc(&h->d_scratch, h->scratch_bytes)) != cudaSuccess) {
+            pb_destroy(h);
+            return cuda_fail(e, "cudaMalloc scratch");
+        }
+    }
+    cudaEventCreate(&h->ev0);
+    cudaEventCreate(&h->ev1);
+
+    pb::Params &pr = h->base;
+    pr.prog = h->d_prog;
+    pr.n_ops = (int)h->prog.size();
+    pr.msyn = h->d_msyn;
+    pr.info_pos = h->d_info;
+    pr.N = N;
+    pr.n = n;
+    pr.k = code->k;
+    pr.L = L;
+    pr.has_crc = w != 0;
+    pr.crc_const = crc_const;
+    pr.final_op = final_op;
+    pr.gscratch = h->d_scratch;
+
+    char buf[1024];
+    snprintf(buf, sizeof buf,
+             "{\"N\": %d, \"k\": %d, \"L\": %d, \"mode\": \"%s\", \"ops\": %d, \"device_ops\": %d, "
+             "\"smem_per_frame\": %d, \"alpha_global_from_stage\": %d, \"global_scratch_per_frame\": %d, "
+             "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": 32}",
+             N, code->k, L, mode == PB_MODE_F32 ? "f32" : "int8", n_ops, (int)h->prog.size(),
+             lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm, h->sms, h->grid);
+    h->plan_json = buf;
+    *out = h;
+    return PB_OK;
+}
+
+int pb_destroy(pb_handle *h) {
+    if (!h) return PB_OK;
+    cudaFree(h->d_prog);
+    cudaFree(h->d_msyn);
+    cudaFree(h->d_info);
+    cudaFree(h->d_scratch);
+    cudaFree(h->d_in);
+    cudaFree(h->d_out);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    delete h;
+    return PB_OK;
+}
+
+const char *pb_plan_json(pb_handle *h) { return h ? h->plan_json.c_str() : ""; }
+long long pb_launch_count_impl(pb_handle *h) { return h ? h->launches : 0; }
+int64_t pb_launch_count(pb_handle *h) { return h ? h->launches : 0; }
+
+double pb_last_kernel_ms(pb_handle *h) {
+    if (!h || !h->timed) return 0.0;
+    float ms = 0.f;
+    if (cudaEventSynchronize(h->ev1) != cudaSuccess) return 0.0;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    return ms;
+}
+
+}  // extern "C"
+
+namespace {
+
+int ensure(void **p, size_t *cap, size_t need) {
+    if (*cap >= need) return PB_OK;
+    cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    size_t sz = std::max(need, (size_t)1 << 20);
+    cudaError_t e = cudaMalloc(p, sz);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc staging");
+    *cap = sz;
+    return PB_OK;
+}
+
+int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
+    int grid = (int)std::min<long long>(h->grid, pr.batch);
+    if (grid < 1) return PB_OK;
+    PB_CUDA(cudaEventRecord(h->ev0, st));
+    cudaError_t e = pb_launch_decode(&pr, h->mode, grid, h->smem_frame, st);
+    if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
+    PB_CUDA(cudaEventRecord(h->ev1, st));
+    h->timed = true;
+    h->launches += 1;
+    return PB_OK;
+}
+
+}  // namespace
+
+extern "C" int pb_decode(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *info_out,
+                         uint8_t *crc_ok, double *pm_out, int32_t *paths_used, void *stream) {
+    g_err.clear();
+    if (!h) return fail(PB_EINVAL, "null handle");
+    if (batch < 0) return fail(PB_EINVAL, "negative batch");
+    if (in_type != PB_IN_F32 && in_type != PB_IN_I8) return fail(PB_EINVAL, "unknown input type");
+    if (in_type == PB_IN_I8 && h->mode != PB_MODE_INT8)
+        return fail(PB_EINVAL, "int8 LLR input needs an int8-mode decoder");
+    if (batch == 0) return PB_OK;
+    if (!llr) return fail(PB_EINVAL, "null LLR pointer");
+    PB_CUDA(cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t in_es = in_type == PB_IN_F32 ? 4 : 1;
+    const size_t in_bytes = (size_t)batch * h->N * in_es;
+    pb::Params pr = h->base;
+    pr.in_type = in_type;
+    pr.batch = batch;
+    pr.path_cw = nullptr;
+    pr.path_pm = nullptr;
+    pr.path_crc = nullptr;
+
+    const bool dev_in = is_device_ptr(llr);
+    const bool all_dev = dev_in && (!info_out || is_device_ptr(info_out)) && (!crc_ok || is_device_ptr(crc_ok)) &&
+                         (!pm_out || is_device_ptr(pm_out)) && (!paths_used || is_device_ptr(paths_used));
+    if (all_dev) {
+        pr.llr = llr;
+        pr.info_out = info_out;
+        pr.crc_ok = crc_ok;
+        pr.pm_out = pm_out;
+        pr.paths_used = paths_used;
+        return launch(h, pr, st);
+    }
+    // staged path: host buffers in and/or out
+    if (!dev_in) {
+        int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
+        if (rc) return rc;
+        PB_CUDA(cudaMemcpyAsync(h->d_in, llr, in_bytes, cudaMemcpyHostToDevice, st));
+        pr.llr = h->d_in;
+    } else {
+        pr.llr = llr;
+    }
+    const size_t big_info = (size_t)batch * h->k;
+    const size_t o_info = 0;
+    const size_t o_ok = (big_info + 255) / 256 * 256;
+    const size_t o_pm = o_ok + ((size_t)batch + 255) / 256 * 256;
+    const size_t o_pu = o_pm + (size_t)batch * 8;
+    const size_t total = o_pu + (size_t)batch * 4;
+    int rc = ensure((void **)&h->d_out, &h->d_out_cap, total);
+    if (rc) return rc;
+    pr.info_out = info_out ? h->d_out + o_info : nullptr;
+    pr.crc_ok = crc_ok ? h->d_out + o_ok : nullptr;
+    pr.pm_out = pm_out ? reinterpret_cast<double *>(h->d_out + o_pm) : nullptr;
+    pr.paths_used = paths_used ? reinterpret_cast<int32_t *>(h->d_out + o_pu) : nullptr;
+    rc = launch(h, pr, st);
+    if (rc) return rc;
+    if (info_out) PB_CUDA(cudaMemcpyAsync(info_out, pr.info_out, big_info, cudaMemcpyDeviceToHost, st));
+    if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok, pr.crc_ok, (size_t)batch, cudaMemcpyDeviceToHost, st));
+    if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out, pr.pm_out, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
+    if (paths_used)
+        PB_CUDA(cudaMemcpyAsync(paths_used, pr.paths_used, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+    PB_CUDA(cudaStreamSynchronize(st));
+    PB_CUDA(cudaGetLastError());
+    return PB_OK;
+}
+
+extern "C" int pb_decode_paths(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *codewords,
+                               double *path_pm, uint8_t *path_crc, int32_t *paths_used, void *stream) {
+    g_err.clear();
+    if (!h) return fail(PB_EINVAL, "null handle");
+    if (batch < 0) return fail(PB_EINVAL, "negative batch");
+    if (in_type != PB_IN_F32 && in_type != PB_IN_I8) return fail(PB_EINVAL, "unknown input type");
+    if (in_type == PB_IN_I8 && h->mode != PB_MODE_INT8)
+        return fail(PB_EINVAL, "int8 LLR input needs an int8-mode decoder");
+    if (batch == 0) return PB_OK;
+    if (!llr || !codewords || !path_pm || !path_crc || !paths_used) return fail(PB_EINVAL, "null pointer");
+    PB_CUDA(cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int L = h->L, rw = h->base.lay.root_words;
+    const size_t in_bytes = (size_t)batch * h->N * (in_type == PB_IN_F32 ? 4 : 1);
+    int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
+    if (rc) return rc;
+    PB_CUDA(cudaMemcpyAsync(h->d_in, llr, in_bytes, cudaMemcpyHostToDevice, st));
+    const size_t o_cw = 0, n_cw = (size_t)batch * L * rw * 4;
+    const size_t o_pm = (n_cw + 255) / 256 * 256;
+    const size_t o_crc = o_pm + (size_t)batch * L * 8;
+    const size_t o_pu = (o_crc + (size_t)batch * L + 255) / 256 * 256;
+    const size_t total = o_pu + (size_t)batch * 4;
+    rc = ensure((void **)&h->d_out, &h->d_out_cap, total);
+    if (rc) return rc;
+    PB_CUDA(cudaMemsetAsync(h->d_out, 0, total, st));
+    pb::Params pr = h->base;
+    pr.llr = h->d_in;
+    pr.in_type = in_type;
+    pr.batch = batch;
+    pr.info_out = nullptr;
+    pr.crc_ok = nullptr;
+    pr.pm_out = nullptr;
+    pr.paths_used = reinterpret_cast<int32_t *>(h->d_out + o_pu);
+    pr.path_cw = reinterpret_cast<uint32_t *>(h->d_out + o_cw);
+    pr.path_pm = reinterpret_cast<double *>(h->d_out + o_pm);
+    pr.path_crc = h->d_out + o_crc;
+    rc = launch(h, pr, st);
+    if (rc) return rc;
+    std::vector<uint32_t> cw((size_t)batch * L * rw);
+    PB_CUDA(cudaMemcpyAsync(cw.data(), pr.path_cw, n_cw, cudaMemcpyDeviceToHost, st));
+    PB_CUDA(cudaMemcpyAsync(path_pm, pr.path_pm, (size_t)batch * L * 8, cudaMemcpyDeviceToHost, st));
+    PB_CUDA(cudaMemcpyAsync(path_crc, pr.path_crc, (size_t)batch * L, cudaMemcpyDeviceToHost, st));
+    PB_CUDA(cudaMemcpyAsync(paths_used, pr.paths_used, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+    PB_CUDA(cudaStreamSynchronize(st));
+    const int N = h->N;
+    for (size_t r = 0; r < (size_t)batch * L; ++r)
+        for (int i = 0; i < N; ++i) codewords[r * N + i] = (uint8_t)((cw[r * rw + (i >> 5)] >> (i & 31)) & 1u);
+    return PB_OK;
+}
