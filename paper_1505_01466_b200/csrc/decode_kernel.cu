@@ -1,23 +1,26 @@
 // decode_kernel.cu -- Fast-SSC list-CRC decode kernel for sm_100a.
 //
-// One warp decodes one frame at a time (persistent loop over frames); the
-// L path slots of the list live on the warp's lanes.  Per op:
-//   F / G      element-parallel over (path, element): P active paths split the
-//              32 lanes into groups of G = 32/pow2(P) lanes per path
+// One CTA of W warps decodes one frame at a time (persistent loop over
+// frames).  The L path slots are split across the warps (PPW = L/W per warp);
+// a warp only synchronises with the others at leaves.  Per op:
+//   F / G      element-parallel over the warp's (path, element) pairs: its A
+//              active paths split 32 lanes into groups of G = 32/pow2(A)
 //              (kernels.py:39-56, listdec.py:319-326)
 //   leaves     group scans of the node LLRs: pairwise-exact float sums
-//              (Rate-0 / Rep, listdec.py:340-359), stable two/four least
+//              (Rate-0 / Rep, listdec.py:340-359), stable two / four least
 //              reliable positions + hard decisions + parity (Rate-1 / SPC,
 //              listdec.py:360-394)
-//   selection  lane = source path; each lane's candidates are a sorted
-//              column, the L best are found by warp-shuffle bitonic sorts of
-//              the columns with early exit (listdec.py:63-100)
-//   materialise survivors copy the source's row-index vectors (lazy copy,
-//              listdec.py:103-143,397-434), write their leaf word and run the
+//   selection  warp 0, lane = source path: each lane's candidates form a
+//              sorted column; the L-th best metric comes from warp-shuffle
+//              bitonic sorts of the columns (early exit once no column entry
+//              can enter), exact ties resolved by (source, cand) prefix
+//              counts -- listdec.py:63-100
+//   materialise survivors copy their source's row-index vectors (lazy copy,
+//              listdec.py:103-143,397-434), write the leaf word and run the
 //              leaf's chain of Combines in place (listdec.py:327-332)
 //   finalise   CRC by per-path GF(2) syndrome == constant, strict-max pick
 //              among CRC-passing paths (listdec.py:289-308), polar transform
-//              of the winner and payload gather (encode.py:29-53,76-87).
+//              of the winner and payload gather (encode.py:29-53,76-87)
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -26,6 +29,9 @@
 
 #define PB_IN_F32 0
 #define PB_IN_I8 1
+
+// one frame per CTA: the frame's shared block is the whole dynamic smem
+extern __shared__ __align__(16) unsigned char g_smem[];
 
 namespace pb {
 
@@ -46,14 +52,14 @@ struct Elem<int8_t> {
     static __device__ __forceinline__ void st(int8_t *p, float v) { *p = (int8_t)__float2int_rn(v); }
 };
 
-// min-sum F: sign(a) sign(b) min(|a|,|b|); zero products give a signed zero,
-// numerically equal to the reference's 0 (kernels.py:39-48)
+// min-sum F: sign(a) sign(b) min(|a|,|b|); a zero product comes out as a
+// signed zero, numerically equal to the reference's 0 (kernels.py:39-48)
 __device__ __forceinline__ float f_op(float a, float b) {
     unsigned s = (__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u;
     return __uint_as_float(__float_as_uint(fminf(fabsf(a), fabsf(b))) | s);
 }
 
-// G: b + (1 - 2 beta) a, one correctly rounded add (kernels.py:51-56);
+// G: b + (1 - 2 beta) a -- one correctly rounded add (kernels.py:51-56);
 // int8 mode saturates to [-127, 127]
 template <typename T>
 __device__ __forceinline__ float g_op(float a, float b, unsigned bit) {
@@ -63,128 +69,185 @@ __device__ __forceinline__ float g_op(float a, float b, unsigned bit) {
 }
 
 __device__ __forceinline__ int pow2ceil(int x) { return x <= 1 ? 1 : 1 << (32 - __clz(x - 1)); }
+__device__ __forceinline__ int log2ceil(int x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
-// Reads the LLRs of one node for one path: a stored alpha row, the channel
-// (root leaf) or the never-stored stage n-1, recomputed from the channel.
+// ------------------------------------------------------------- sources
+// A stored alpha row (block-interleaved, stride ppw between elements)
 template <typename T>
-struct Src {
+struct RowSrc {
     const T *p;
+    int ppw;
+    __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(p + i * ppw); }
+};
+template <typename T>
+struct RowDst {
+    T *p;
+    int ppw;
+    __device__ __forceinline__ void put(int i, float v) const { Elem<T>::st(p + i * ppw, v); }
+};
+// stage n-1 in the left half of the tree: f(channel halves)
+template <typename T>
+struct VirtF {
+    const T *ch;
+    int half;
+    __device__ __forceinline__ float get(int i) const {
+        return f_op(Elem<T>::ld(ch + i), Elem<T>::ld(ch + i + half));
+    }
+};
+// stage n-1 in the right half: g(channel halves, the path's left-half bits)
+template <typename T>
+struct VirtG {
     const T *ch;
     const uint32_t *bw;
     int half;
-    int mode;
     __device__ __forceinline__ float get(int i) const {
-        if (mode == VM_NONE) return Elem<T>::ld(p + i);
-        float a = Elem<T>::ld(ch + i), b = Elem<T>::ld(ch + i + half);
-        if (mode == VM_F) return f_op(a, b);
-        unsigned bit = (bw[i >> 5] >> (i & 31)) & 1u;
-        return g_op<T>(a, b, bit);
+        return g_op<T>(Elem<T>::ld(ch + i), Elem<T>::ld(ch + i + half), (bw[i >> 5] >> (i & 31)) & 1u);
     }
 };
-
+// the channel itself (a root leaf)
 template <typename T>
-struct Frame {
+struct ChanSrc {
+    const T *ch;
+    __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(ch + i); }
+};
+
+// ------------------------------------------------------- frame state
+
+template <typename T, int W>
+struct Dec {
     const Params &P;
-    unsigned char *fs;  // this frame's shared memory block
     unsigned char *gs;  // this frame's global scratch block
-    int cur;            // which half of the double-buffered path state is live
+    int lane, warp;
+    int cur;            // live half of the double-buffered path state
+    int par;            // candidate-buffer parity (toggles at forking leaves)
+    int lpar;           // parity used by the last forking leaf
 
-    __device__ Frame(const Params &p, unsigned char *f, unsigned char *g) : P(p), fs(f), gs(g), cur(0) {}
+    __device__ Dec(const Params &p, unsigned char *g)
+        : P(p), gs(g), lane(threadIdx.x & 31), warp(threadIdx.x >> 5), cur(0), par(0), lpar(0) {}
 
-    __device__ __forceinline__ T *alpha_row(int s, int row) const {
-        unsigned char *base = s >= P.lay.a_gfrom ? gs : fs;
-        return reinterpret_cast<T *>(base + P.lay.a_off[s]) + row * P.lay.a_stride[s];
+    // row r, element 0 of a block-interleaved stage s (ppw is a power of two)
+    __device__ __forceinline__ int rowoff(int s, int r) const {
+        return ((r >> P.lppw) << (P.lppw + s)) + (r & (P.ppw - 1));
     }
+    __device__ __forceinline__ T *a_sm(int s) const { return reinterpret_cast<T *>(g_smem + P.lay.a_off[s]); }
+    __device__ __forceinline__ T *a_gl(int s) const { return reinterpret_cast<T *>(gs + P.lay.a_off[s]); }
     __device__ __forceinline__ uint32_t *beta_row(int s, int row) const {
-        return reinterpret_cast<uint32_t *>(fs + P.lay.b_off[s]) + row * P.lay.b_stride[s];
+        return reinterpret_cast<uint32_t *>(g_smem + P.lay.b_off[s]) + row * P.lay.b_stride[s];
     }
-    __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(fs + P.lay.ch_off); }
-    __device__ __forceinline__ double *pm(int buf) const {
-        return reinterpret_cast<double *>(fs + P.lay.pm_off) + buf * P.L;
+    __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(g_smem + P.lay.ch_off); }
+    __device__ __forceinline__ double *pm(int b) const {
+        return reinterpret_cast<double *>(g_smem + P.lay.pm_off) + b * P.L;
     }
-    __device__ __forceinline__ uint32_t *syn(int buf) const {
-        return reinterpret_cast<uint32_t *>(fs + P.lay.syn_off) + buf * P.L;
+    __device__ __forceinline__ uint32_t *syn(int b) const {
+        return reinterpret_cast<uint32_t *>(g_smem + P.lay.syn_off) + b * P.L;
     }
-    __device__ __forceinline__ uint8_t *ia(int buf, int q) const {
-        return fs + P.lay.ia_off + (buf * P.L + q) * P.lay.idx_stride;
+    __device__ __forceinline__ uint8_t *ia(int b, int q) const {
+        return g_smem + P.lay.ia_off + (b * P.L + q) * P.lay.idx_stride;
     }
-    __device__ __forceinline__ uint8_t *ib(int buf, int q) const {
-        return fs + P.lay.ib_off + (buf * P.L + q) * P.lay.idx_stride;
+    __device__ __forceinline__ uint8_t *ib(int b, int q) const {
+        return g_smem + P.lay.ib_off + (b * P.L + q) * P.lay.idx_stride;
     }
-    __device__ __forceinline__ double *cd(int q) const {
-        return reinterpret_cast<double *>(fs + P.lay.cd_off) + q * kMaxCand;
+    __device__ __forceinline__ double *cd(int b, int q) const {
+        return reinterpret_cast<double *>(g_smem + P.lay.cd_off) + (b * P.L + q) * kMaxCand;
     }
-    __device__ __forceinline__ uint16_t *clrb(int q) const {
-        return reinterpret_cast<uint16_t *>(fs + P.lay.clrb_off) + q * 4;
+    __device__ __forceinline__ uint16_t *clrb(int b, int q) const {
+        return reinterpret_cast<uint16_t *>(g_smem + P.lay.clrb_off) + (b * P.L + q) * 4;
     }
-    __device__ __forceinline__ uint32_t *chs() const { return reinterpret_cast<uint32_t *>(fs + P.lay.chs_off); }
-    __device__ __forceinline__ uint8_t *cflag() const { return fs + P.lay.cflag_off; }
-    __device__ __forceinline__ uint8_t *asg() const { return fs + P.lay.asg_off; }
-    __device__ __forceinline__ uint32_t *hard(int q) const {
-        return reinterpret_cast<uint32_t *>(fs + P.lay.hard_off) + q * P.lay.hard_words;
+    __device__ __forceinline__ uint32_t *chs(int b) const {
+        return reinterpret_cast<uint32_t *>(g_smem + P.lay.chs_off) + b * P.L;
     }
-    __device__ __forceinline__ uint32_t *root() const { return reinterpret_cast<uint32_t *>(fs + P.lay.root_off); }
+    __device__ __forceinline__ uint8_t *cflag(int b) const { return g_smem + P.lay.cflag_off + b * P.L; }
+    __device__ __forceinline__ uint8_t *asg(int b) const { return g_smem + P.lay.asg_off + b * 2 * P.L; }
+    __device__ __forceinline__ uint32_t *hard(int b, int q) const {
+        return reinterpret_cast<uint32_t *>(g_smem + P.lay.hard_off) + (b * P.L + q) * P.lay.hard_words;
+    }
+    __device__ __forceinline__ uint32_t *root() const { return reinterpret_cast<uint32_t *>(g_smem + P.lay.root_off); }
 
-    // LLRs of path q at stage s
-    __device__ __forceinline__ Src<T> src(int s, int q, int vmode) const {
-        Src<T> r;
-        r.ch = channel();
-        r.half = P.N >> 1;
-        r.bw = nullptr;
-        if (s == P.n) {
-            r.mode = VM_NONE;
-            r.p = channel();
-        } else if (s == P.n - 1) {
-            r.mode = vmode;
-            r.p = nullptr;
-            if (vmode == VM_G) r.bw = beta_row(P.n - 1, ib(cur, q)[P.n - 1]);
-        } else {
-            r.mode = VM_NONE;
-            r.p = alpha_row(s, ia(cur, q)[s]);
-        }
-        return r;
+    __device__ __forceinline__ void sync() const {
+        if (W > 1)
+            __syncthreads();
+        else
+            __syncwarp();
+    }
+
+    // lane -> (path, sub-lane) for this warp when np paths are active
+    struct Map {
+        int q, sub, G;
+        bool active;
+    };
+    __device__ __forceinline__ Map map(int np) const {
+        Map m;
+        int act = np - warp * P.ppw;
+        act = act < 0 ? 0 : (act > P.ppw ? P.ppw : act);
+        const int lg = 5 - log2ceil(act > 0 ? act : 1);
+        m.G = 1 << lg;
+        const int ql = lane >> lg;
+        m.sub = lane & (m.G - 1);
+        m.active = ql < act;
+        m.q = warp * P.ppw + ql;
+        return m;
     }
 };
 
 // ---------------------------------------------------------------- F / G
 
-template <typename T, bool IS_G>
-__device__ void fg_op(Frame<T> &F, const DOp &o, int lane) {
-    const int s = o.stage, h = 1 << (s - 1), np = o.pin;
-    const int G = 32 / pow2ceil(np);
-    const int q = lane / G, sub = lane & (G - 1);
-    if (q < np) {
-        Src<T> src = F.src(s, q, o.vmode);
-        T *dst = F.alpha_row(s - 1, q);
-        if (IS_G) {
-            const uint32_t *bw = F.beta_row(s - 1, F.ib(F.cur, q)[s - 1]);
-            for (int i = sub; i < h; i += G) {
-                unsigned bit = (bw[i >> 5] >> (i & 31)) & 1u;
-                Elem<T>::st(dst + i, g_op<T>(src.get(i), src.get(i + h), bit));
-            }
-        } else {
-            for (int i = sub; i < h; i += G) Elem<T>::st(dst + i, f_op(src.get(i), src.get(i + h)));
+template <typename T, bool IS_G, class S, class D>
+__device__ __forceinline__ void fg_loop(const S &src, const D &dst, const uint32_t *bw, int h, int G, int sub) {
+    if (!IS_G) {
+#pragma unroll 4
+        for (int i = sub; i < h; i += G) dst.put(i, f_op(src.get(i), src.get(i + h)));
+    } else {
+        const int lim = h < 32 ? h : 32;
+        for (int c0 = 0; c0 < h; c0 += 32) {
+            const uint32_t word = bw[c0 >> 5];
+#pragma unroll 4
+            for (int j = sub; j < lim; j += G) dst.put(c0 + j, g_op<T>(src.get(c0 + j), src.get(c0 + j + h), (word >> j) & 1u));
         }
-        if (sub == 0) F.ia(F.cur, q)[s - 1] = (uint8_t)q;
     }
+}
+
+template <typename T, int W, bool IS_G, class S>
+__device__ __forceinline__ void fg_to_dst(const Dec<T, W> &F, const S &src, int s, int q, const uint32_t *bw, int h,
+                                          int G, int sub) {
+    const int off = F.rowoff(s - 1, q);
+    if (s - 1 < F.P.lay.a_gfrom)
+        fg_loop<T, IS_G>(src, RowDst<T>{F.a_sm(s - 1) + off, F.P.ppw}, bw, h, G, sub);
+    else
+        fg_loop<T, IS_G>(src, RowDst<T>{F.a_gl(s - 1) + off, F.P.ppw}, bw, h, G, sub);
+}
+
+template <typename T, int W, bool IS_G>
+__device__ __forceinline__ void fg_op(Dec<T, W> &F, const DOp &o) {
+    const auto mp = F.map(o.pin);
+    if (!mp.active) return;
+    const Params &P = F.P;
+    const int s = o.stage, h = 1 << (s - 1), q = mp.q;
+    const uint32_t *bw = IS_G ? F.beta_row(s - 1, F.ib(F.cur, q)[s - 1]) : nullptr;
+    if (s == P.n - 1) {
+        if (o.vmode == VM_F)
+            fg_to_dst<T, W, IS_G>(F, VirtF<T>{F.channel(), P.N >> 1}, s, q, bw, h, mp.G, mp.sub);
+        else
+            fg_to_dst<T, W, IS_G>(F, VirtG<T>{F.channel(), F.beta_row(P.n - 1, F.ib(F.cur, q)[P.n - 1]), P.N >> 1},
+                                  s, q, bw, h, mp.G, mp.sub);
+    } else {
+        const int off = F.rowoff(s, F.ia(F.cur, q)[s]);
+        if (s < P.lay.a_gfrom)
+            fg_to_dst<T, W, IS_G>(F, RowSrc<T>{F.a_sm(s) + off, P.ppw}, s, q, bw, h, mp.G, mp.sub);
+        else
+            fg_to_dst<T, W, IS_G>(F, RowSrc<T>{F.a_gl(s) + off, P.ppw}, s, q, bw, h, mp.G, mp.sub);
+    }
+    if (mp.sub == 0) F.ia(F.cur, q)[s - 1] = (uint8_t)q;
 }
 
 // ------------------------------------------------- pairwise-exact sums
 // numpy float32 pairwise summation (what the reference's sum(axis=1) runs):
 // n < 8 sequential from 0; 8 <= n <= 128 eight strided accumulators combined
-// ((0+1)+(2+3))+((4+5)+(6+7)); larger n halves recursively.  For the power-
-// of-two node sizes that is a perfect binary tree over 8*nb accumulators
-// (nb = max(1, n/128)), each a sequential sum of 16 (or n/8) elements.
+// ((0+1)+(2+3))+((4+5)+(6+7)); larger n halves recursively.  For power-of-
+// two node sizes that is a perfect binary tree over 8*nb accumulators
+// (nb = max(1, n/128)), each a sequential sum of min(n,128)/8 elements.
 // Lane j of an 8-lane group owns accumulator column j of every 128-block.
 
-template <typename T, int NS>
-struct SumOut {
-    float v[NS];
-};
-
-// NS sums of functions of a: NS=1 -> sum(min(a,0)); NS=3 -> (sum min(a,0),
-// sum max(a,0), sum a)
-template <typename T, int NS>
+template <int NS>
 __device__ __forceinline__ void acc_add(float (&acc)[NS], float a) {
     acc[0] = __fadd_rn(acc[0], fminf(a, 0.f));
     if (NS == 3) {
@@ -201,17 +264,16 @@ __device__ __forceinline__ void acc_init(float (&acc)[NS], float a) {
     }
 }
 
-// returns the sums in every lane of the 8-lane group (valid when the group's
-// path is active)
-template <typename T, int NS>
-__device__ void group8_pairwise(const Src<T> &src, int m, bool active, int j, float (&out)[NS]) {
+// NS = 1: sum min(a,0); NS = 3: (sum min(a,0), sum max(a,0), sum a).
+// Result valid in every lane of the 8-lane group.
+template <int NS, class S>
+__device__ __forceinline__ void group8_pairwise(const S &src, int m, bool active, int j, float (&out)[NS]) {
     if (m < 8) {
         float r[NS];
 #pragma unroll
         for (int t = 0; t < NS; ++t) r[t] = 0.f;
         if (active && j == 0)
-            for (int i = 0; i < m; ++i) acc_add<T, NS>(r, src.get(i));
-        // broadcast from lane j==0 of the group
+            for (int i = 0; i < m; ++i) acc_add<NS>(r, src.get(i));
 #pragma unroll
         for (int t = 0; t < NS; ++t) out[t] = __shfl_sync(FULL_MASK, r[t], (threadIdx.x & 31) & ~7);
         return;
@@ -219,24 +281,22 @@ __device__ void group8_pairwise(const Src<T> &src, int m, bool active, int j, fl
     const int blk = m < 128 ? m : 128;
     const int nb = m / blk;
     const int per = blk / 8;
-    float stk[NS][8];  // binary-counter stack over blocks (nb <= 128 -> depth <= 7)
+    float stk[NS][8];
     float carry[NS];
     for (int b = 0; b < nb; ++b) {
         float acc[NS];
         const int base = b * blk + j;
         if (active) {
             acc_init<NS>(acc, src.get(base));
-            for (int r = 1; r < per; ++r) acc_add<T, NS>(acc, src.get(base + 8 * r));
+            for (int r = 1; r < per; ++r) acc_add<NS>(acc, src.get(base + 8 * r));
         } else {
 #pragma unroll
             for (int t = 0; t < NS; ++t) acc[t] = 0.f;
         }
-        // ((0+1)+(2+3))+((4+5)+(6+7)) within the block: xor 1, 2, 4
 #pragma unroll
         for (int d = 1; d < 8; d <<= 1)
 #pragma unroll
             for (int t = 0; t < NS; ++t) acc[t] = __fadd_rn(acc[t], __shfl_xor_sync(FULL_MASK, acc[t], d));
-        // combine block sums as a binary tree in block order
 #pragma unroll
         for (int t = 0; t < NS; ++t) carry[t] = acc[t];
         int lvl = 0;
@@ -265,13 +325,12 @@ struct TopK {
             i[k] = 0x7fffffff;
         }
     }
-    // insert keeping ascending (magnitude, index): stable argsort order
-    __device__ __forceinline__ void push(float v, int idx) {
+    __device__ __forceinline__ void insert(float v, int idx) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            bool lt = v < m[k] || (v == m[k] && idx < i[k]);
-            float tm = m[k];
-            int ti = i[k];
+            const bool lt = v < m[k] || (v == m[k] && idx < i[k]);
+            const float tm = m[k];
+            const int ti = i[k];
             if (lt) {
                 m[k] = v;
                 i[k] = idx;
@@ -280,38 +339,37 @@ struct TopK {
             }
         }
     }
+    // ascending index scan: a value equal to the current K-th keeps the
+    // earlier index, so only strictly smaller values enter (stable argsort)
+    __device__ __forceinline__ void push_scan(float v, int idx) {
+        if (v < m[K - 1]) insert(v, idx);
+    }
 };
 
 // ------------------------------------------------------------ selection
 
-__device__ __forceinline__ bool better(double am, int as, double bm, int bs) {
-    return am > bm || (am == bm && as < bs);
-}
-
-// bitonic network over the first W lanes; desc = best first
-__device__ __forceinline__ void bitonic_sort(double &m, int &s, int W, bool desc, int lane) {
-    for (int k = 2; k <= W; k <<= 1)
+__device__ __forceinline__ void bitonic_sort(double &v, int Wd, bool desc, int lane) {
+    for (int k = 2; k <= Wd; k <<= 1)
         for (int j = k >> 1; j > 0; j >>= 1) {
-            double om = __shfl_xor_sync(FULL_MASK, m, j);
-            int os = __shfl_xor_sync(FULL_MASK, s, j);
-            bool seg_desc = ((lane & k) == 0) == desc;
-            bool want_better = ((lane & j) == 0) == seg_desc;
-            if (want_better == better(om, os, m, s)) {
-                m = om;
-                s = os;
-            }
+            const double o = __shfl_xor_sync(FULL_MASK, v, j);
+            const bool seg_desc = ((lane & k) == 0) == desc;
+            v = (((lane & j) == 0) == seg_desc) ? fmax(v, o) : fmin(v, o);
         }
 }
-__device__ __forceinline__ void bitonic_merge_desc(double &m, int &s, int W, int lane) {
-    for (int j = W >> 1; j > 0; j >>= 1) {
-        double om = __shfl_xor_sync(FULL_MASK, m, j);
-        int os = __shfl_xor_sync(FULL_MASK, s, j);
-        bool want_better = (lane & j) == 0;
-        if (want_better == better(om, os, m, s)) {
-            m = om;
-            s = os;
-        }
+__device__ __forceinline__ void bitonic_merge_desc(double &v, int Wd, int lane) {
+    for (int j = Wd >> 1; j > 0; j >>= 1) {
+        const double o = __shfl_xor_sync(FULL_MASK, v, j);
+        v = ((lane & j) == 0) ? fmax(v, o) : fmin(v, o);
     }
+}
+__device__ __forceinline__ int excl_scan(int v, int lane) {
+    int incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(FULL_MASK, incl, d);
+        if (lane >= d) incl += t;
+    }
+    return incl - v;
 }
 
 // SPC flip sets relative to the ML word over the four LRB slots, emission
@@ -320,89 +378,81 @@ __device__ __constant__ uint8_t kSpcPairs[7] = {0x3, 0x5, 0x9, 0x6, 0xA, 0xC, 0x
 
 __device__ __forceinline__ int flip_mask(int kind, int c, int odd) {
     if (kind == DK_R1) return c;  // (), (b1), (b2), (b1, b2)
-    int ml = odd ? 1 : 0;
+    const int ml = odd ? 1 : 0;
     return c == 0 ? ml : (kSpcPairs[c - 1] ^ ml);
 }
 
-// Phase B: choose survivors; writes asg[k] = (source, cand) for k < pout.
-template <typename T>
-__device__ void select_survivors(Frame<T> &F, const DOp &o, int lane) {
-    const int np = o.pin, C = o.ncand, L = F.P.L;
-    const bool valid_lane = lane < np;
+// Phase B (warp 0, lane = source): survivors -> asg[par][k] = (source, cand)
+// in (source, cand) order.  The L best by (metric desc, source asc, cand asc)
+// == listdec.py:63-100 (bounded heap == full sort, tests/oracles.py:74-89).
+template <typename T, int W>
+__device__ __forceinline__ void select_phase(const Dec<T, W> &F, const DOp &o) {
+    const int lane = F.lane, np = o.pin, C = o.ncand, L = F.P.L;
+    const bool vl = lane < np;
+    const double pm = vl ? F.pm(F.cur)[lane] : 0.0;
+    const double *cd = F.cd(F.par, vl ? lane : 0);
     double met[kMaxCand];
-    int seq[kMaxCand];
-    const double pm = valid_lane ? F.pm(F.cur)[lane] : 0.0;
-    const double *cd = F.cd(valid_lane ? lane : 0);
 #pragma unroll
-    for (int c = 0; c < kMaxCand; ++c) {
-        bool v = valid_lane && c < C;
-        met[c] = v ? pm + cd[c] : -INFINITY;
-        seq[c] = v ? lane * kMaxCand + c : 0x7fff0000 + lane * kMaxCand + c;
-    }
+    for (int c = 0; c < kMaxCand; ++c) met[c] = (vl && c < C) ? pm + cd[c] : -INFINITY;
     unsigned mask;
     if (!o.select) {
-        mask = valid_lane ? (1u << C) - 1 : 0u;
+        mask = vl ? (1u << C) - 1u : 0u;
     } else {
-        // sort this lane's column best-first (stable by cand index)
-        if (C == 2 || C == 8) {
-            // odd-even transposition sort, C passes (C <= 8)
+        double srt[kMaxCand];
+#pragma unroll
+        for (int c = 0; c < kMaxCand; ++c) srt[c] = met[c];
+        // best-first column per lane (Rate-1 columns already are:
+        // 0 >= -m1 >= -m2 >= -(m1+m2), monotone under rounding)
+        if (C != 4) {
 #pragma unroll
             for (int pass = 0; pass < kMaxCand; ++pass) {
                 if (pass >= C) break;
 #pragma unroll
                 for (int c = pass & 1; c + 1 < kMaxCand; c += 2) {
-                    if (c + 1 < C && better(met[c + 1], seq[c + 1], met[c], seq[c])) {
-                        double tm = met[c];
-                        met[c] = met[c + 1];
-                        met[c + 1] = tm;
-                        int ts = seq[c];
-                        seq[c] = seq[c + 1];
-                        seq[c + 1] = ts;
-                    }
+                    const double a = srt[c], b = srt[c + 1];
+                    srt[c] = fmax(a, b);
+                    srt[c + 1] = fmin(a, b);
                 }
             }
         }
-        // Rate-1 columns are already best-first: 0 >= -m1 >= -m2 >= -(m1+m2)
-        const int W = pow2ceil(L);
-        double Rm = met[0];
-        int Rs = seq[0];
-        bitonic_sort(Rm, Rs, W, true, lane);
-        double Tm = __shfl_sync(FULL_MASK, Rm, L - 1);
-        int Ts = __shfl_sync(FULL_MASK, Rs, L - 1);
+        const int Wd = pow2ceil(L);
+        double R = srt[0];
+        bitonic_sort(R, Wd, true, lane);
+        double Tm = __shfl_sync(FULL_MASK, R, L - 1);
 #pragma unroll
         for (int j = 1; j < kMaxCand; ++j) {
             if (j >= C) break;
-            double xm = met[j];
-            int xs = seq[j];
-            if (!__any_sync(FULL_MASK, better(xm, xs, Tm, Ts))) break;
-            bitonic_sort(xm, xs, W, false, lane);
-            if (better(xm, xs, Rm, Rs)) {
-                Rm = xm;
-                Rs = xs;
-            }
-            bitonic_merge_desc(Rm, Rs, W, lane);
-            Tm = __shfl_sync(FULL_MASK, Rm, L - 1);
-            Ts = __shfl_sync(FULL_MASK, Rs, L - 1);
+            double x = srt[j];
+            if (!__any_sync(FULL_MASK, x > Tm)) break;
+            bitonic_sort(x, Wd, false, lane);
+            R = fmax(R, x);
+            bitonic_merge_desc(R, Wd, lane);
+            Tm = __shfl_sync(FULL_MASK, R, L - 1);
         }
+        // Tm = the L-th best metric; keep all better, then the earliest ties
+        int gt = 0, eq = 0;
+#pragma unroll
+        for (int c = 0; c < kMaxCand; ++c) {
+            gt += met[c] > Tm;
+            eq += met[c] == Tm;
+        }
+        const int need = L - (int)__reduce_add_sync(FULL_MASK, (unsigned)gt);
+        int r = excl_scan(eq, lane);
         mask = 0u;
 #pragma unroll
         for (int c = 0; c < kMaxCand; ++c) {
-            bool keep = valid_lane && c < C && (better(met[c], seq[c], Tm, Ts) || seq[c] == Ts);
-            if (keep) mask |= 1u << (seq[c] & (kMaxCand - 1));
+            if (met[c] > Tm) {
+                mask |= 1u << c;
+            } else if (met[c] == Tm) {
+                if (r < need) mask |= 1u << c;
+                ++r;
+            }
         }
     }
-    // survivors in (source, cand) order
-    int cnt = __popc(mask);
-    int incl = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        int v = __shfl_up_sync(FULL_MASK, incl, d);
-        if (lane >= d) incl += v;
-    }
-    int k = incl - cnt;
-    uint8_t *asg = F.asg();
+    int k = excl_scan(__popc(mask), lane);
+    uint8_t *asg = F.asg(F.par);
     while (mask) {
-        int c = __ffs(mask) - 1;
+        const int c = __ffs(mask) - 1;
         mask &= mask - 1;
         asg[2 * k] = (uint8_t)lane;
         asg[2 * k + 1] = (uint8_t)c;
@@ -412,52 +462,51 @@ __device__ void select_survivors(Frame<T> &F, const DOp &o, int lane) {
 
 // ----------------------------------------------------- leaf word + chain
 
-// Word bits of the leaf decision for (source p, cand c): value of the 32-bit
-// word w of an m-bit leaf word (m < 32: the m-bit value).
-template <typename T>
-__device__ __forceinline__ uint32_t leaf_word(const Frame<T> &F, int kind, int m, int p, int c, int w) {
+// 32-bit word w of the leaf word of decision (p, c) (m < 32: the m-bit value)
+template <typename T, int W>
+__device__ __forceinline__ uint32_t leaf_word(const Dec<T, W> &F, int b, int kind, int m, int p, int c, int w) {
     const uint32_t fullw = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
     if (kind == DK_R0) return 0u;
     if (kind == DK_REP) {
-        bool ones = F.cflag()[p] ? (c == 0) : (c == 1);
+        const bool ones = F.cflag(b)[p] ? (c == 0) : (c == 1);
         return ones ? fullw : 0u;
     }
-    uint32_t v = F.hard(p)[w];
-    int fm = flip_mask(kind, c, F.cflag()[p]);
-    const uint16_t *lrb = F.clrb(p);
+    uint32_t v = F.hard(b, p)[w];
+    const int fm = flip_mask(kind, c, F.cflag(b)[p]);
+    const uint16_t *lrb = F.clrb(b, p);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
         if ((fm >> j) & 1) {
-            int pos = lrb[j];
+            const int pos = lrb[j];
             if ((pos >> 5) == w) v ^= 1u << (pos & 31);
         }
     return v;
 }
 
 __device__ __forceinline__ uint32_t bits_get(const uint32_t *row, int off, int len) {
-    uint32_t msk = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
+    const uint32_t msk = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
     return (row[off >> 5] >> (off & 31)) & msk;
 }
 __device__ __forceinline__ void bits_put(uint32_t *row, int off, int len, uint32_t v) {
-    uint32_t msk = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
+    const uint32_t msk = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
     uint32_t &w = row[off >> 5];
     w = (w & ~(msk << (off & 31))) | ((v & msk) << (off & 31));
 }
 
-// Writes the leaf word of path k (decision (p, c) of leaf o) into dst at
-// [E - m, E), then runs the leaf's combine chain t .. E's stage - 1:
-//   dst[E - 2^(s+1), E - 2^s) = slot_s[row] ^ dst[E - 2^s, E)
-// (listdec.py:327-332 with the right child's bits kept in place).
-// All 32 lanes must call it (it synchronises the warp between steps).
-template <typename T>
-__device__ void word_and_chain(const Frame<T> &F, const DOp &o, int kind, bool active, int G, int sub,
+// Leaf word of path k (decision (p, c)) into dst[E - m, E), then the leaf's
+// chain of Combines t .. sE-1 in place:
+//   dst[E - 2^(s+1), E - 2^s) = slot_s[row_s] ^ dst[E - 2^s, E)
+// (listdec.py:327-332 with the right child's bits kept where they are).
+// Called by all lanes of a warp (synchronises the warp between steps).
+template <typename T, int W>
+__device__ __forceinline__ void word_and_chain(const Dec<T, W> &F, int b, const DOp &o, int kind, bool active, int G, int sub,
                                int p, int c, const uint8_t *ibsrc, uint32_t *dst, int sE) {
     const int t = o.stage, m = 1 << t, E = 1 << sE;
     if (active) {
         if (m >= 32) {
-            for (int w = sub; w < (m >> 5); w += G) dst[((E - m) >> 5) + w] = leaf_word(F, kind, m, p, c, w);
+            for (int w = sub; w < (m >> 5); w += G) dst[((E - m) >> 5) + w] = leaf_word(F, b, kind, m, p, c, w);
         } else if (sub == 0) {
-            bits_put(dst, E - m, m, leaf_word(F, kind, m, p, c, 0));
+            bits_put(dst, E - m, m, leaf_word(F, b, kind, m, p, c, 0));
         }
     }
     __syncwarp();
@@ -466,10 +515,10 @@ __device__ void word_and_chain(const Frame<T> &F, const DOp &o, int kind, bool a
         if (active) {
             const uint32_t *sl = F.beta_row(s, ibsrc[s]);
             if (seg >= 32) {
-                const int a = (E - 2 * seg) >> 5, b = (E - seg) >> 5;
-                for (int w = sub; w < (seg >> 5); w += G) dst[a + w] = sl[w] ^ dst[b + w];
+                const int a = (E - 2 * seg) >> 5, bb = (E - seg) >> 5;
+                for (int w = sub; w < (seg >> 5); w += G) dst[a + w] = sl[w] ^ dst[bb + w];
             } else if (sub == 0) {
-                uint32_t v = (sl[0] & ((1u << seg) - 1u)) ^ bits_get(dst, E - seg, seg);
+                const uint32_t v = (sl[0] & ((1u << seg) - 1u)) ^ bits_get(dst, E - seg, seg);
                 bits_put(dst, E - 2 * seg, seg, v);
             }
         }
@@ -479,161 +528,203 @@ __device__ void word_and_chain(const Frame<T> &F, const DOp &o, int kind, bool a
 
 // ------------------------------------------------------------- leaves
 
-template <typename T>
-__device__ void leaf_op(Frame<T> &F, const DOp &o, int lane) {
-    const Params &P = F.P;
-    const int t = o.stage, m = 1 << t, np = o.pin;
-    int kind = o.kind;
-    if (kind == DK_R1 && m == 1) kind = DK_REP;  // listdec.py:347
-
-    if (kind == DK_R0 || kind == DK_REP) {
-        // 8 lanes per path, 4 paths per pass
-        const int g8 = lane >> 3, j = lane & 7;
-        for (int base = 0; base < np; base += 4) {
-            const int q = base + g8;
-            const bool active = q < np;
-            Src<T> src = F.src(t, active ? q : 0, o.vmode);
-            if (kind == DK_R0) {
-                float r[1];
-                group8_pairwise<T, 1>(src, m, active, j, r);
-                if (active && j == 0) F.pm(F.cur)[q] += (double)r[0];  // listdec.py:341-343
-            } else {
-                float r[3];
-                group8_pairwise<T, 3>(src, m, active, j, r);
-                if (active && j == 0) {  // listdec.py:348-358
-                    const bool ones_first = r[2] < 0.f;
-                    double *cd = F.cd(q);
-                    const double neg = (double)r[0], pos = (double)r[1];
-                    cd[0] = ones_first ? -pos : neg;
-                    cd[1] = ones_first ? neg : -pos;
-                    F.cflag()[q] = ones_first;
-                }
-            }
-        }
+template <typename T, int W, class S>
+__device__ __forceinline__ void leaf_sums(Dec<T, W> &F, const DOp &o, int kind, const S &src, int q, bool active, int j) {
+    const int m = 1 << o.stage;
+    if (kind == DK_R0) {
+        float r[1];
+        group8_pairwise<1>(src, m, active, j, r);
+        if (active && j == 0) F.pm(F.cur)[q] += (double)r[0];  // listdec.py:341-343
     } else {
-        // Rate-1 / SPC scan: G lanes per path
-        const int G = 32 / pow2ceil(np);
-        const int q = lane / G, sub = lane & (G - 1);
-        const bool active = q < np;
-        Src<T> src = F.src(t, active ? q : 0, o.vmode);
-        TopK<4> tk;
-        tk.init();
-        uint32_t hs = 0u, hword = 0u;
-        int par = 0;
-        const int iters = (m + G - 1) / G;
-        uint32_t *hard = F.hard(active ? q : 0);
-        for (int it = 0; it < iters; ++it) {
-            const int i = it * G + sub;
-            const bool valid = active && i < m;
-            const float a = valid ? src.get(i) : 0.f;
-            const bool neg = valid && a < 0.f;
-            if (valid) {
-                tk.push(fabsf(a), i);
-                if (neg) hs ^= __ldg(P.msyn + o.off + i);
-            }
-            const uint32_t bal = __ballot_sync(FULL_MASK, neg);
-            const uint32_t gb = G == 32 ? bal : (bal >> (q * G)) & ((1u << G) - 1u);
-            const int base = it * G;
-            hword |= gb << (base & 31);
-            if (((base + G) & 31) == 0 || it == iters - 1) {
-                if (active && sub == 0) hard[base >> 5] = hword;
-                par ^= __popc(hword);
-                hword = 0u;
-            }
-        }
-        // merge across the group's lanes
-        for (int d = 1; d < G; d <<= 1) {
-            hs ^= __shfl_xor_sync(FULL_MASK, hs, d);
-            float om[4];
-            int oi[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                om[k] = __shfl_xor_sync(FULL_MASK, tk.m[k], d);
-                oi[k] = __shfl_xor_sync(FULL_MASK, tk.i[k], d);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) tk.push(om[k], oi[k]);
-        }
-        if (active && sub == 0) {
-            double *cd = F.cd(q);
-            uint16_t *lrb = F.clrb(q);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) lrb[k] = (uint16_t)(tk.i[k] < m ? tk.i[k] : 0);
-            F.chs()[q] = hs;
-            if (kind == DK_R1) {  // listdec.py:360-372
-                const double w1 = (double)tk.m[0], w2 = (double)tk.m[1];
-                cd[0] = 0.0;
-                cd[1] = -w1;
-                cd[2] = -w2;
-                cd[3] = -(w1 + w2);
-                F.cflag()[q] = 0;
-            } else {  // SPC, listdec.py:373-394
-                const int odd = par & 1;
-                F.cflag()[q] = (uint8_t)odd;
-                // slots in ascending position order (the order the reference sums in)
-                int ord[4] = {0, 1, 2, 3};
-#pragma unroll
-                for (int x = 1; x < 4; ++x)
-#pragma unroll
-                    for (int y = x; y > 0; --y)
-                        if (tk.i[ord[y]] < tk.i[ord[y - 1]]) {
-                            int tt = ord[y];
-                            ord[y] = ord[y - 1];
-                            ord[y - 1] = tt;
-                        }
-                double w[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) w[k] = (double)tk.m[k];
-                for (int c = 0; c < o.ncand; ++c) {
-                    const int fm = flip_mask(DK_SPC, c, odd);
-                    double accd = 0.0;
-                    bool any = false;
-#pragma unroll
-                    for (int x = 0; x < 4; ++x)
-                        if ((fm >> ord[x]) & 1) {
-                            accd = any ? accd + w[ord[x]] : w[ord[x]];
-                            any = true;
-                        }
-                    cd[c] = any ? -accd : 0.0;
-                }
-            }
+        float r[3];
+        group8_pairwise<3>(src, m, active, j, r);
+        if (active && j == 0) {  // listdec.py:348-358
+            const bool ones_first = r[2] < 0.f;
+            double *cd = F.cd(F.par, q);
+            const double neg = (double)r[0], pos = (double)r[1];
+            cd[0] = ones_first ? -pos : neg;
+            cd[1] = ones_first ? neg : -pos;
+            F.cflag(F.par)[q] = ones_first;
         }
     }
-    __syncwarp();
+}
+
+template <typename T, int W, int K, class S>
+__device__ __forceinline__ void leaf_scan(Dec<T, W> &F, const DOp &o, int kind, const S &src, int q, bool active, int G, int sub) {
+    const Params &P = F.P;
+    const int m = 1 << o.stage;
+    TopK<K> tk;
+    tk.init();
+    uint32_t hs = 0u, hword = 0u;
+    int par = 0;
+    const int lgG = 31 - __clz(G);
+    const int iters = (m + G - 1) >> lgG;
+    uint32_t *hard = F.hard(F.par, active ? q : 0);
+    const uint32_t *msyn = P.msyn + o.off;
+    const int gshift = (q - F.warp * P.ppw) * G;
+    const uint32_t gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+    for (int it = 0; it < iters; ++it) {
+        const int i = it * G + sub;
+        const bool valid = active && i < m;
+        const float a = valid ? src.get(i) : 0.f;
+        const bool neg = valid && a < 0.f;
+        if (valid) tk.push_scan(fabsf(a), i);
+        if (neg) hs ^= __ldg(msyn + i);
+        const uint32_t gb = (__ballot_sync(FULL_MASK, neg) >> (G == 32 ? 0 : gshift)) & gmask;
+        const int base = it * G;
+        hword |= gb << (base & 31);
+        if (((base + G) & 31) == 0 || it == iters - 1) {
+            if (active && sub == 0) hard[base >> 5] = hword;
+            par ^= __popc(hword);
+            hword = 0u;
+        }
+    }
+    for (int d = 1; d < G; d <<= 1) {
+        hs ^= __shfl_xor_sync(FULL_MASK, hs, d);
+        float om[K];
+        int oi[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            om[k] = __shfl_xor_sync(FULL_MASK, tk.m[k], d);
+            oi[k] = __shfl_xor_sync(FULL_MASK, tk.i[k], d);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) tk.insert(om[k], oi[k]);
+    }
+    if (!(active && sub == 0)) return;
+    double *cd = F.cd(F.par, q);
+    uint16_t *lrb = F.clrb(F.par, q);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) lrb[k] = (uint16_t)(k < K && tk.i[k < K ? k : 0] < m ? tk.i[k < K ? k : 0] : 0);
+    F.chs(F.par)[q] = hs;
+    if (kind == DK_R1) {  // listdec.py:360-372
+        const double w1 = (double)tk.m[0], w2 = (double)tk.m[1];
+        cd[0] = 0.0;
+        cd[1] = -w1;
+        cd[2] = -w2;
+        cd[3] = -(w1 + w2);
+        F.cflag(F.par)[q] = 0;
+        return;
+    }
+    // SPC, listdec.py:373-394: deltas sum the net flips in ascending position
+    const int odd = par & 1;
+    F.cflag(F.par)[q] = (uint8_t)odd;
+    int ord[4] = {0, 1, 2, 3};
+#pragma unroll
+    for (int x = 1; x < 4; ++x)
+#pragma unroll
+        for (int y = x; y > 0; --y)
+            if (tk.i[ord[y] & (K - 1)] < tk.i[ord[y - 1] & (K - 1)]) {
+                const int tt = ord[y];
+                ord[y] = ord[y - 1];
+                ord[y - 1] = tt;
+            }
+    double w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = (double)tk.m[k & (K - 1)];
+    for (int c = 0; c < o.ncand; ++c) {
+        const int fm = flip_mask(DK_SPC, c, odd);
+        double accd = 0.0;
+        bool any = false;
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+            if ((fm >> ord[x]) & 1) {
+                accd = any ? accd + w[ord[x]] : w[ord[x]];
+                any = true;
+            }
+        cd[c] = any ? -accd : 0.0;
+    }
+}
+
+template <typename T, int W, class S>
+__device__ __forceinline__ void leaf_phase_a(Dec<T, W> &F, const DOp &o, int kind, const S &src, int q, bool active, int G, int sub,
+                             int j8) {
+    if (kind == DK_R0 || kind == DK_REP)
+        leaf_sums(F, o, kind, src, q, active, j8);
+    else if (kind == DK_R1)
+        leaf_scan<T, W, 2>(F, o, kind, src, q, active, G, sub);
+    else
+        leaf_scan<T, W, 4>(F, o, kind, src, q, active, G, sub);
+}
+
+// dispatch on where the node's LLRs live
+template <typename T, int W>
+__device__ __forceinline__ void leaf_read(Dec<T, W> &F, const DOp &o, int kind, int q, bool active, int G, int sub, int j8) {
+    const Params &P = F.P;
+    const int t = o.stage;
+    const int qq = active ? q : F.warp * P.ppw;
+    if (t == P.n) {
+        leaf_phase_a(F, o, kind, ChanSrc<T>{F.channel()}, q, active, G, sub, j8);
+    } else if (t == P.n - 1) {
+        if (o.vmode == VM_F)
+            leaf_phase_a(F, o, kind, VirtF<T>{F.channel(), P.N >> 1}, q, active, G, sub, j8);
+        else
+            leaf_phase_a(F, o, kind, VirtG<T>{F.channel(), F.beta_row(P.n - 1, F.ib(F.cur, qq)[P.n - 1]), P.N >> 1}, q,
+                         active, G, sub, j8);
+    } else {
+        const int off = F.rowoff(t, F.ia(F.cur, qq)[t]);
+        if (t < P.lay.a_gfrom)
+            leaf_phase_a(F, o, kind, RowSrc<T>{F.a_sm(t) + off, P.ppw}, q, active, G, sub, j8);
+        else
+            leaf_phase_a(F, o, kind, RowSrc<T>{F.a_gl(t) + off, P.ppw}, q, active, G, sub, j8);
+    }
+}
+
+template <typename T, int W>
+__device__ __forceinline__ void leaf_op(Dec<T, W> &F, const DOp &o) {
+    const Params &P = F.P;
+    const int np = o.pin;
+    int kind = o.kind;
+    if (kind == DK_R1 && o.stage == 0) kind = DK_REP;  // listdec.py:347
+
+    // Phase A: per-source sums / scans, this warp's sources
+    if (kind == DK_R0 || kind == DK_REP) {
+        // 8 lanes per path, 4 paths per pass
+        int act = np - F.warp * P.ppw;
+        act = act < 0 ? 0 : (act > P.ppw ? P.ppw : act);
+        const int g8 = F.lane >> 3, j8 = F.lane & 7;
+        for (int base = 0; base < act; base += 4) {
+            const int ql = base + g8;
+            leaf_read(F, o, kind, F.warp * P.ppw + ql, ql < act, 32, 0, j8);
+        }
+    } else {
+        const auto mp = F.map(np);
+        leaf_read(F, o, kind, mp.q, mp.active, mp.G, mp.sub, 0);
+    }
+    F.sync();
 
     const bool fork = kind != DK_R0;
     if (fork) {
-        select_survivors(F, o, lane);
-        __syncwarp();
+        if (F.warp == 0) select_phase(F, o);
+        F.sync();
     }
 
-    // Phase C: materialise survivors k < pout
-    const int npo = o.pout;
-    const int G = 32 / pow2ceil(npo);
-    const int k = lane / G, sub = lane & (G - 1);
-    const bool active = k < npo;
+    // Phase C: materialise survivors k < pout (this warp's)
+    const auto mp = F.map(o.pout);
+    const int k = mp.q;
     const int nxt = fork ? F.cur ^ 1 : F.cur;
+    const int b = F.par;
     int p = k, c = 0;
-    if (fork && active) {
-        p = F.asg()[2 * k];
-        c = F.asg()[2 * k + 1];
+    if (fork && mp.active) {
+        p = F.asg(b)[2 * k];
+        c = F.asg(b)[2 * k + 1];
     }
-    const uint8_t *ibsrc = F.ib(F.cur, active ? p : 0);
-    if (active && sub == 0 && fork) {
+    const uint8_t *ibsrc = F.ib(F.cur, mp.active ? p : 0);
+    if (fork && mp.active && mp.sub == 0) {
         uint32_t sy = F.syn(F.cur)[p];
         if (kind == DK_REP) {
-            bool ones = F.cflag()[p] ? (c == 0) : (c == 1);
+            const bool ones = F.cflag(b)[p] ? (c == 0) : (c == 1);
             if (ones) sy ^= o.rep_syn;
         } else {
-            sy ^= F.chs()[p];
-            const int fm = flip_mask(kind, c, F.cflag()[p]);
-            const uint16_t *lrb = F.clrb(p);
+            sy ^= F.chs(b)[p];
+            const int fm = flip_mask(kind, c, F.cflag(b)[p]);
+            const uint16_t *lrb = F.clrb(b, p);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if ((fm >> j) & 1) sy ^= __ldg(P.msyn + o.off + lrb[j]);
+            for (int jj = 0; jj < 4; ++jj)
+                if ((fm >> jj) & 1) sy ^= __ldg(P.msyn + o.off + lrb[jj]);
         }
         F.syn(nxt)[k] = sy;
-        F.pm(nxt)[k] = F.pm(F.cur)[p] + F.cd(p)[c];  // listdec.py:415
+        F.pm(nxt)[k] = F.pm(F.cur)[p] + F.cd(b, p)[c];  // listdec.py:415
         const uint4 *sa = reinterpret_cast<const uint4 *>(F.ia(F.cur, p));
         const uint4 *sb = reinterpret_cast<const uint4 *>(F.ib(F.cur, p));
         uint4 *da = reinterpret_cast<uint4 *>(F.ia(nxt, k));
@@ -645,11 +736,15 @@ __device__ void leaf_op(Frame<T> &F, const DOp &o, int lane) {
     }
     const int sE = o.target;
     if (sE < P.n) {
-        word_and_chain(F, o, kind, active, G, sub, p, c, ibsrc, F.beta_row(sE, k), sE);
-        if (active && sub == 0) F.ib(nxt, k)[sE] = (uint8_t)k;
+        word_and_chain(F, b, o, kind, mp.active, mp.G, mp.sub, p, c, ibsrc, F.beta_row(sE, k), sE);
+        if (mp.active && mp.sub == 0) F.ib(nxt, k)[sE] = (uint8_t)k;
     }
     __syncwarp();
     F.cur = nxt;
+    if (fork) {
+        F.lpar = F.par;
+        F.par ^= 1;
+    }
 }
 
 // ------------------------------------------------------------ finalise
@@ -673,24 +768,25 @@ __device__ __forceinline__ void polar_transform_words(uint32_t *x, int N, int la
     }
 }
 
-template <typename T>
-__device__ void build_root(const Frame<T> &F, const DOp &fo, int k, uint32_t *dst, int lane) {
+template <typename T, int W>
+__device__ __forceinline__ void build_root(const Dec<T, W> &F, const DOp &fo, int k, uint32_t *dst) {
     int kind = fo.kind;
     if (kind == DK_R1 && fo.stage == 0) kind = DK_REP;
     int p = k, c = 0;
+    const int b = F.lpar;
     if (kind != DK_R0) {
-        p = F.asg()[2 * k];
-        c = F.asg()[2 * k + 1];
+        p = F.asg(b)[2 * k];
+        c = F.asg(b)[2 * k + 1];
     }
-    // zero the word if it is partial (N < 32)
-    if (F.P.N < 32 && lane == 0) dst[0] = 0u;
+    if (F.P.N < 32 && F.lane == 0) dst[0] = 0u;
     __syncwarp();
-    word_and_chain(F, fo, kind, true, 32, lane, p, c, F.ib(F.cur, k), dst, F.P.n);
+    word_and_chain(F, b, fo, kind, true, 32, F.lane, p, c, F.ib(F.cur, k), dst, F.P.n);
 }
 
-template <typename T>
-__device__ void finalize(Frame<T> &F, long long f, int np, int lane) {
+template <typename T, int W>
+__device__ __forceinline__ void finalize(Dec<T, W> &F, long long f, int np) {
     const Params &P = F.P;
+    const int lane = F.lane;
     const DOp fo = P.prog[P.final_op];
     const bool live = lane < np;
     const double pmk = live ? F.pm(F.cur)[lane] : -INFINITY;
@@ -702,8 +798,8 @@ __device__ void finalize(Frame<T> &F, long long f, int np, int lane) {
     int bk = elig ? lane : 64;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
-        double om = __shfl_xor_sync(FULL_MASK, bm, d);
-        int ok2 = __shfl_xor_sync(FULL_MASK, bk, d);
+        const double om = __shfl_xor_sync(FULL_MASK, bm, d);
+        const int ok2 = __shfl_xor_sync(FULL_MASK, bk, d);
         if (om > bm || (om == bm && ok2 < bk)) {
             bm = om;
             bk = ok2;
@@ -713,10 +809,7 @@ __device__ void finalize(Frame<T> &F, long long f, int np, int lane) {
     const bool wok = __shfl_sync(FULL_MASK, ok, wnr & 31);
     const int rw = P.lay.root_words;
     if (P.path_cw) {
-        for (int kk = 0; kk < np; ++kk) {
-            uint32_t *dst = P.path_cw + ((size_t)f * P.L + kk) * rw;
-            build_root(F, fo, kk, dst, lane);
-        }
+        for (int kk = 0; kk < np; ++kk) build_root(F, fo, kk, P.path_cw + ((size_t)f * P.L + kk) * rw);
         if (live) {
             P.path_pm[(size_t)f * P.L + lane] = pmk;
             P.path_crc[(size_t)f * P.L + lane] = ok;
@@ -724,7 +817,7 @@ __device__ void finalize(Frame<T> &F, long long f, int np, int lane) {
     }
     if (P.info_out) {
         uint32_t *u = F.root();
-        build_root(F, fo, wnr, u, lane);
+        build_root(F, fo, wnr, u);
         polar_transform_words(u, P.N, lane);
         uint8_t *out = P.info_out + (size_t)f * P.k;
         for (int i = lane; i < P.k; i += 32) {
@@ -743,99 +836,108 @@ __device__ void finalize(Frame<T> &F, long long f, int np, int lane) {
 // ------------------------------------------------------------- kernel
 
 template <typename T>
-__device__ void load_channel(const Frame<T> &F, long long f, int lane) {
+__device__ __forceinline__ float ingest(float a) {
+    if (Elem<T>::kInt) return fminf(fmaxf(rintf(a * 4.f), -127.f), 127.f);  // clip(rint(4x)), half-even
+    return fminf(fmaxf(a, -1048576.f), 1048576.f);                             // clamp_llr (kernels.py:34-36)
+}
+
+template <typename T, int W>
+__device__ __forceinline__ void load_channel(const Dec<T, W> &F, long long f) {
     const Params &P = F.P;
     T *ch = F.channel();
-    const int N = P.N;
+    const int N = P.N, tid = threadIdx.x;
     if (P.in_type == PB_IN_I8) {
         const int8_t *src = reinterpret_cast<const int8_t *>(P.llr) + (size_t)f * N;
-        for (int i = lane; i < N; i += 32) ch[i] = (T)src[i];
+        for (int i = tid; i < N; i += 32 * W) ch[i] = (T)src[i];
         return;
     }
     const float *src = reinterpret_cast<const float *>(P.llr) + (size_t)f * N;
     if ((N & 3) == 0) {
         const float4 *s4 = reinterpret_cast<const float4 *>(src);
-        for (int i = lane; i < (N >> 2); i += 32) {
-            float4 v = __ldcs(s4 + i);  // streamed once: evict-first
-            float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int x = 0; x < 4; ++x) {
-                float a = e[x];
-                if (Elem<T>::kInt)  // clip(rint(4x), -127, 127), half to even
-                    a = fminf(fmaxf(rintf(a * 4.f), -127.f), 127.f);
-                else  // clamp_llr: +-2^20 (kernels.py:34-36)
-                    a = fminf(fmaxf(a, -1048576.f), 1048576.f);
-                Elem<T>::st(ch + 4 * i + x, a);
-            }
+        for (int i = tid; i < (N >> 2); i += 32 * W) {
+            const float4 v = __ldcs(s4 + i);  // read once: evict-first
+            Elem<T>::st(ch + 4 * i + 0, ingest<T>(v.x));
+            Elem<T>::st(ch + 4 * i + 1, ingest<T>(v.y));
+            Elem<T>::st(ch + 4 * i + 2, ingest<T>(v.z));
+            Elem<T>::st(ch + 4 * i + 3, ingest<T>(v.w));
         }
     } else {
-        for (int i = lane; i < N; i += 32) {
-            float a = src[i];
-            if (Elem<T>::kInt)
-                a = fminf(fmaxf(rintf(a * 4.f), -127.f), 127.f);
-            else
-                a = fminf(fmaxf(a, -1048576.f), 1048576.f);
-            Elem<T>::st(ch + i, a);
-        }
+        for (int i = tid; i < N; i += 32 * W) Elem<T>::st(ch + i, ingest<T>(src[i]));
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(32) k_decode(const Params P) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31;
+template <typename T, int W>
+__global__ void __launch_bounds__(32 * W, 1) k_decode(const __grid_constant__ Params P) {
     unsigned char *gs = P.gscratch ? P.gscratch + (size_t)blockIdx.x * P.lay.gbytes : nullptr;
     for (long long f = blockIdx.x; f < P.batch; f += gridDim.x) {
-        Frame<T> F(P, smem, gs);
-        load_channel(F, f, lane);
-        if (lane == 0) {
+        Dec<T, W> F(P, gs);
+        load_channel(F, f);
+        if (threadIdx.x == 0) {
             F.pm(0)[0] = 0.0;
             F.syn(0)[0] = 0u;
         }
-        __syncwarp();
+        F.sync();
         int np = 1;
         for (int oi = 0; oi < P.n_ops; ++oi) {
             const DOp o = P.prog[oi];
             switch (o.kind) {
                 case DK_F:
-                    fg_op<T, false>(F, o, lane);
+                    fg_op<T, W, false>(F, o);
                     break;
                 case DK_G:
-                    fg_op<T, true>(F, o, lane);
+                    fg_op<T, W, true>(F, o);
                     break;
                 case DK_NOP:
                     break;
                 default:
-                    leaf_op(F, o, lane);
+                    leaf_op(F, o);
                     np = o.pout;
                     break;
             }
             __syncwarp();
         }
-        finalize(F, f, np, lane);
+        F.sync();
+        if (F.warp == 0) finalize(F, f, np);
+        F.sync();
     }
+}
+
+template <typename T, int W>
+cudaError_t launch_t(const Params *p, int grid, size_t smem, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(k_decode<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_decode<T, W><<<grid, 32 * W, smem, st>>>(*p);
+    return cudaGetLastError();
+}
+template <typename T, int W>
+cudaError_t occ_t(size_t smem, int *bps) {
+    cudaError_t e = cudaFuncSetAttribute(k_decode<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_decode<T, W>, 32 * W, smem);
 }
 
 }  // namespace pb
 
-// launch wrappers (host)
-extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int grid, size_t smem,
+#define PB_DISPATCH_W(FN, T, ...)                         \
+    switch (warps) {                                      \
+        case 1: return pb::FN<T, 1>(__VA_ARGS__);         \
+        case 2: return pb::FN<T, 2>(__VA_ARGS__);         \
+        case 4: return pb::FN<T, 4>(__VA_ARGS__);         \
+        case 8: return pb::FN<T, 8>(__VA_ARGS__);         \
+        default: return cudaErrorInvalidValue;            \
+    }
+
+extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps, int grid, size_t smem,
                                         cudaStream_t stream) {
     if (mode == 0) {
-        cudaFuncSetAttribute(pb::k_decode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        pb::k_decode<float><<<grid, 32, smem, stream>>>(*p);
-    } else {
-        cudaFuncSetAttribute(pb::k_decode<int8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        pb::k_decode<int8_t><<<grid, 32, smem, stream>>>(*p);
+        PB_DISPATCH_W(launch_t, float, p, grid, smem, stream)
     }
-    return cudaGetLastError();
+    PB_DISPATCH_W(launch_t, int8_t, p, grid, smem, stream)
 }
 
-extern "C" cudaError_t pb_occupancy(int mode, size_t smem, int *blocks_per_sm) {
+extern "C" cudaError_t pb_occupancy(int mode, int warps, size_t smem, int *blocks_per_sm) {
     if (mode == 0) {
-        cudaFuncSetAttribute(pb::k_decode<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pb::k_decode<float>, 32, smem);
+        PB_DISPATCH_W(occ_t, float, smem, blocks_per_sm)
     }
-    cudaFuncSetAttribute(pb::k_decode<int8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, pb::k_decode<int8_t>, 32, smem);
+    PB_DISPATCH_W(occ_t, int8_t, smem, blocks_per_sm)
 }

@@ -1,19 +1,19 @@
 // decoder.cuh -- device program, layouts and launch parameters shared by the
-// host planner (plan.cu) and the decode kernels (decode_kernel.cu).
+// host runtime (runtime.cu) and the decode kernels (decode_kernel.cu).
 #pragma once
 #include <stdint.h>
 
 namespace pb {
 
 constexpr int kMaxLog = 16;     // N <= 65536
-constexpr int kMaxL = 32;       // one warp per frame: one lane per path slot
+constexpr int kMaxL = 32;       // selection runs on one warp: one lane per source path
 constexpr int kMaxCand = 8;
 
 // Device op kinds.  Combines never appear: each leaf carries its chain of
-// combines (see DESIGN.md "partial sums in place").
+// combines (DESIGN.md "partial sums in place").
 enum : int8_t { DK_F = 0, DK_G = 1, DK_R0 = 2, DK_REP = 3, DK_R1 = 4, DK_SPC = 5, DK_NOP = 6 };
 
-// virtual modes for reads of stage n-1 (never stored)
+// how an op reads stage n-1 (never stored): recomputed from the channel
 enum : int8_t { VM_NONE = 0, VM_F = 1, VM_G = 2 };
 
 struct __align__(16) DOp {
@@ -21,34 +21,37 @@ struct __align__(16) DOp {
     int8_t stage;    // F/G: stage read (writes stage-1); leaf: its stage t
     int8_t pin;      // active paths before the op
     int8_t pout;     // active paths after (leaf)
-    int8_t target;   // leaf: slot s* its chain ends in (n = root)
+    int8_t target;   // leaf: slot s* its chain of combines ends in (n = root)
     int8_t ncand;    // leaf: candidates per path C
     int8_t select;   // leaf: pin*ncand > L (a real 2L->L selection)
-    int8_t vmode;    // how this op reads stage n-1 (VM_*), or VM_NONE
+    int8_t vmode;    // how this op reads stage n-1 (VM_*), else VM_NONE
     int32_t off;     // leaf: first u index covered
     uint32_t rep_syn;// Rep leaf: syndrome of the all-ones word
 };
 
-// Per-frame storage plan.  Offsets in bytes from the frame's smem block
-// (or from the frame's global scratch block for stages >= a_gfrom).
+// Per-frame storage plan.  Offsets in bytes from the frame's shared-memory
+// block, or from its global scratch block for alpha stages >= a_gfrom.
+// Alpha rows are block-interleaved: the PPW rows a warp owns are interleaved
+// element by element, row r element i at
+//   a_off[s] + ((r / PPW) * 2^s * PPW + i * PPW + r % PPW) * sizeof(T)
+// so a warp's (path, element) lanes hit 32 distinct banks / one 128-B line.
 struct FrameLayout {
     int ch_off;                 // channel LLRs, N elements of T
-    int a_off[kMaxLog];         // alpha stage s (s <= n-2): L rows
-    int a_stride[kMaxLog];      // row stride, elements
+    int a_off[kMaxLog];         // alpha stage s (s <= n-2)
     int a_gfrom;                // stages >= a_gfrom live in global scratch
     int b_off[kMaxLog];         // beta slot s (s <= n-1): L rows, uint32 words
     int b_stride[kMaxLog];      // row stride, words
-    int pm_off;                 // double [2][L]
-    int syn_off;                // uint32 [2][L]
-    int ia_off;                 // uint8 [2][L][idx_stride]  alpha rows per stage
-    int ib_off;                 // uint8 [2][L][idx_stride]  beta rows per slot
+    int pm_off;                 // double [2][L]    path metrics (double-buffered)
+    int syn_off;                // uint32 [2][L]    CRC syndromes
+    int ia_off;                 // uint8 [2][L][idx_stride]  alpha row per stage
+    int ib_off;                 // uint8 [2][L][idx_stride]  beta row per slot
     int idx_stride;
-    int cd_off;                 // double [L][8] candidate deltas
-    int clrb_off;               // uint16 [L][4] least reliable positions
-    int chs_off;                // uint32 [L] hard-word syndrome
-    int cflag_off;              // uint8 [L] parity / ones-first
-    int asg_off;                // uint8 [L][2] survivor -> (source, cand)
-    int hard_off;               // uint32 [L][hard_words] hard decisions
+    int cd_off;                 // double [2][L][8] candidate deltas (by leaf parity)
+    int clrb_off;               // uint16 [2][L][4] least reliable positions
+    int chs_off;                // uint32 [2][L] hard-word syndrome
+    int cflag_off;              // uint8 [2][L] parity / ones-first
+    int asg_off;                // uint8 [2][L][2] survivor -> (source, cand)
+    int hard_off;               // uint32 [2][L][hard_words] hard decisions
     int hard_words;
     int root_off;               // uint32 [root_words] winner codeword scratch
     int root_words;
@@ -62,6 +65,8 @@ struct Params {
     const uint32_t *msyn;       // [N] leaf-local CRC syndrome rows
     const uint32_t *info_pos;   // [k] payload positions (u index)
     int N, n, k, L;
+    int ppw;                    // paths per warp (rows per interleave block), power of two
+    int lppw;                   // log2(ppw)
     int has_crc;
     uint32_t crc_const;
     int final_op;               // index of the last leaf
@@ -75,7 +80,7 @@ struct Params {
     uint32_t *path_cw;          // paths mode: [B][L][root_words] packed, or null
     double *path_pm;            // [B][L]
     uint8_t *path_crc;          // [B][L]
-    unsigned char *gscratch;    // [frame slots][gbytes]
+    unsigned char *gscratch;    // [CTA slots][gbytes]
     FrameLayout lay;
 };
 

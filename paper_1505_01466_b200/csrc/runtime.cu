@@ -22,9 +22,9 @@
 #include "../../include/polar_b200.h"
 #include "decoder.cuh"
 
-extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int grid, size_t smem,
+extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps, int grid, size_t smem,
                                         cudaStream_t stream);
-extern "C" cudaError_t pb_occupancy(int mode, size_t smem, int *blocks_per_sm);
+extern "C" cudaError_t pb_occupancy(int mode, int warps, size_t smem, int *blocks_per_sm);
 
 namespace {
 
@@ -85,7 +85,7 @@ struct pb_handle {
     std::vector<pb::DOp> prog;
     pb::DOp *d_prog = nullptr;
     uint32_t *d_msyn = nullptr, *d_info = nullptr;
-    int grid = 0, blocks_per_sm = 0, sms = 0;
+    int grid = 0, blocks_per_sm = 0, sms = 0, warps = 1;
     size_t smem_frame = 0;
     unsigned char *d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -309,6 +309,16 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
 
     // ---- storage plan
     const int es = mode == PB_MODE_F32 ? 4 : 1;
+    int warps = env_int("PB_WARPS", L >= 16 ? 4 : (L >= 8 ? 2 : 1));
+    if (warps != 1 && warps != 2 && warps != 4 && warps != 8) warps = 1;
+    while (warps > 1 && warps > L) warps >>= 1;
+    int ppw = 1, lppw = 0;
+    while (ppw * warps < L) {
+        ppw <<= 1;
+        ++lppw;
+    }
+    const int rows = ppw * warps;  // alpha rows, padded to whole interleave blocks
+    h->warps = warps;
     pb::FrameLayout &lay = h->base.lay;
     int off = 0;
     lay.ch_off = off;
@@ -329,44 +339,42 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     lay.ib_off = off;
     off = align_up(off + 2 * L * lay.idx_stride, 16);
     lay.cd_off = off;
-    off = align_up(off + L * pb::kMaxCand * 8, 16);
+    off = align_up(off + 2 * L * pb::kMaxCand * 8, 16);
     lay.clrb_off = off;
-    off = align_up(off + L * 4 * 2, 16);
+    off = align_up(off + 2 * L * 4 * 2, 16);
     lay.chs_off = off;
-    off = align_up(off + L * 4, 16);
+    off = align_up(off + 2 * L * 4, 16);
     lay.cflag_off = off;
-    off = align_up(off + L, 16);
-    lay.asg_off = off;
     off = align_up(off + 2 * L, 16);
+    lay.asg_off = off;
+    off = align_up(off + 2 * 2 * L, 16);
     lay.hard_words = std::max(1, max_hard / 32);
     lay.hard_off = off;
-    off = align_up(off + L * lay.hard_words * 4, 16);
+    off = align_up(off + 2 * L * lay.hard_words * 4, 16);
     lay.root_words = std::max(1, N / 32);
     lay.root_off = off;
     off = align_up(off + lay.root_words * 4, 16);
 
     const int smem_cap = 227 * 1024;
-    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", mode == PB_MODE_F32 ? 3 : 6));
+    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", mode == PB_MODE_F32 ? 2 : 4));
     const int budget = std::max(off, env_int("PB_SMEM_BUDGET", smem_cap / target_fps - 1024));
-    // alpha stages s = 0 .. n-2, lowest stages first into shared memory
-    int s_global = n - 1;  // stages >= s_global go to global scratch
+    // alpha stages s = 0 .. n-2 (n-1 is recomputed), lowest stages first into
+    // shared memory, the rest into per-CTA global scratch (L2-resident)
+    int s_global = n - 1;
     for (int s = 0; s <= n - 2; ++s) {
-        int stride = es == 4 ? (1 << s) + 1 : (1 << s) + 4;
-        int bytes = align_up(L * stride * es, 16);
+        int bytes = align_up(rows * (1 << s) * es, 16);
         if (off + bytes > budget) {
             s_global = s;
             break;
         }
         lay.a_off[s] = off;
-        lay.a_stride[s] = stride;
         off += bytes;
     }
     lay.a_gfrom = s_global;
     int goff = 0;
     for (int s = s_global; s <= n - 2; ++s) {
         lay.a_off[s] = goff;
-        lay.a_stride[s] = std::max(1 << s, 32 / es);
-        goff = align_up(goff + L * lay.a_stride[s] * es, 256);
+        goff = align_up(goff + rows * (1 << s) * es, 256);
     }
     lay.gbytes = goff;
     lay.smem_bytes = align_up(off, 16);
@@ -383,7 +391,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         return cuda_fail(e, "cudaSetDevice");
     }
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
-    e = pb_occupancy(mode, h->smem_frame, &h->blocks_per_sm);
+    e = pb_occupancy(mode, h->warps, h->smem_frame, &h->blocks_per_sm);
     if (e != cudaSuccess || h->blocks_per_sm < 1) {
         delete h;
         return cuda_fail(e == cudaSuccess ? cudaErrorInvalidConfiguration : e, "occupancy");
@@ -420,6 +428,8 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     pr.n = n;
     pr.k = code->k;
     pr.L = L;
+    pr.ppw = ppw;
+    pr.lppw = lppw;
     pr.has_crc = w != 0;
     pr.crc_const = crc_const;
     pr.final_op = final_op;
@@ -429,9 +439,10 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     snprintf(buf, sizeof buf,
              "{\"N\": %d, \"k\": %d, \"L\": %d, \"mode\": \"%s\", \"ops\": %d, \"device_ops\": %d, "
              "\"smem_per_frame\": %d, \"alpha_global_from_stage\": %d, \"global_scratch_per_frame\": %d, "
-             "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": 32}",
+             "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": %d, \"warps_per_frame\": %d}",
              N, code->k, L, mode == PB_MODE_F32 ? "f32" : "int8", n_ops, (int)h->prog.size(),
-             lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm, h->sms, h->grid);
+             lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm, h->sms, h->grid, 32 * h->warps,
+             h->warps);
     h->plan_json = buf;
     *out = h;
     return PB_OK;
@@ -483,7 +494,7 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
     int grid = (int)std::min<long long>(h->grid, pr.batch);
     if (grid < 1) return PB_OK;
     PB_CUDA(cudaEventRecord(h->ev0, st));
-    cudaError_t e = pb_launch_decode(&pr, h->mode, grid, h->smem_frame, st);
+    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, grid, h->smem_frame, st);
     if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
     PB_CUDA(cudaEventRecord(h->ev1, st));
     h->timed = true;

@@ -78,6 +78,19 @@ def _ptr(a):
     return None if a is None else ctypes.c_void_p(a.ctypes.data)
 
 
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _addr(a):
+    """Raw address of a numpy array or torch tensor (None passes through)."""
+    if a is None:
+        return None
+    if _is_torch(a):
+        return ctypes.c_void_p(a.data_ptr())
+    return ctypes.c_void_p(a.ctypes.data)
+
+
 class ListDecoder:
     """List decoder over one schedule, reusable across frames
     (reference ``listdec.py:160-185``).
@@ -151,7 +164,30 @@ class ListDecoder:
 
     # -- input handling --------------------------------------------------
 
-    def _frames(self, llrs) -> tuple[np.ndarray, int]:
+    def _frames(self, llrs):
+        """(keepalive, pointer, in_type, batch) for host frames.  float32
+        input is passed as is (the kernel applies clamp_llr on device, same
+        result); other float dtypes are clamped on the host first
+        (reference kernels.py:34-36); int8 input needs mode='int8'."""
+        if _is_torch(llrs):
+            import torch
+            t = llrs
+            if t.is_cuda:
+                raise ValueError("decode_batch takes host frames; use decode_device for CUDA tensors")
+            if t.dim() == 1:
+                t = t[None, :]
+            if t.dim() != 2 or t.shape[1] != self.spec.N:
+                raise ValueError(f"LLR frame has {t.shape[-1]} values, spec wants {self.spec.N}")
+            if t.dtype == torch.int8:
+                if self.mode != "int8":
+                    raise ValueError("int8 LLRs need a decoder built with mode='int8'")
+                in_type = _native.PB_IN_I8
+            else:
+                if t.dtype != torch.float32:
+                    t = torch.from_numpy(clamp_llr(t.numpy()))
+                in_type = _native.PB_IN_F32
+            t = t.contiguous()
+            return t, t.data_ptr(), in_type, t.shape[0]
         a = np.asarray(llrs)
         if a.ndim == 1:
             a = a[None, :]
@@ -161,23 +197,29 @@ class ListDecoder:
         if a.dtype == np.int8:
             if self.mode != "int8":
                 raise ValueError("int8 LLRs need a decoder built with mode='int8'")
-            return np.ascontiguousarray(a), _native.PB_IN_I8
-        return np.ascontiguousarray(clamp_llr(a)), _native.PB_IN_F32
+            a = np.ascontiguousarray(a)
+            return a, a.ctypes.data, _native.PB_IN_I8, a.shape[0]
+        a = np.ascontiguousarray(a if a.dtype == np.float32 else clamp_llr(a))
+        return a, a.ctypes.data, _native.PB_IN_F32, a.shape[0]
 
     # -- decoding --------------------------------------------------------
 
-    def decode_batch(self, llrs, stream=None) -> BatchResult:
-        """Decode a [B, N] batch; one result row per frame."""
-        frames, in_type = self._frames(llrs)
-        B, k = frames.shape[0], self.spec.k
-        info = np.zeros((B, k), np.uint8)
-        ok = np.zeros(B, np.uint8)
-        pm = np.zeros(B, np.float64)
-        pu = np.zeros(B, np.int32)
-        rc = _native.lib().pb_decode(self._h, _ptr(frames), in_type, B, _ptr(info), _ptr(ok),
-                                     _ptr(pm), _ptr(pu), stream)
+    def decode_batch(self, llrs, stream=None, out: "BatchResult | None" = None) -> BatchResult:
+        """Decode a [B, N] batch of host frames (numpy or torch CPU tensors,
+        pinned for full copy speed); one result row per frame.  ``out`` may
+        hold preallocated host arrays / tensors to decode into."""
+        keep, ptr, in_type, B = self._frames(llrs)
+        k = self.spec.k
+        if out is None:
+            out = BatchResult(np.empty((B, k), np.uint8), np.empty(B, np.bool_),
+                              np.empty(B, np.float64), np.empty(B, np.int32))
+        rc = _native.lib().pb_decode(self._h, ctypes.c_void_p(ptr), in_type, B,
+                                     _addr(out.info_bits), _addr(out.crc_ok),
+                                     _addr(out.chosen_pm), _addr(out.paths_used),
+                                     ctypes.c_void_p(stream) if stream else None)
         _native.check(rc, "pb_decode")
-        return BatchResult(info, ok.astype(bool), pm, pu)
+        del keep
+        return out
 
     def decode_device(self, llrs, info_out=None, crc_ok=None, pm_out=None, paths_used=None,
                       stream=None) -> None:
@@ -221,13 +263,13 @@ class ListDecoder:
     def decode_paths_batch(self, llrs):
         """All survivors of every frame: (codewords [B, L, N], pms [B, L],
         crc_ok [B, L], paths_used [B]); rows past paths_used are zero."""
-        frames, in_type = self._frames(llrs)
-        B, L, N = frames.shape[0], self.list_size, self.spec.N
+        keep, ptr, in_type, B = self._frames(llrs)
+        L, N = self.list_size, self.spec.N
         cw = np.zeros((B, L, N), np.uint8)
         pm = np.zeros((B, L), np.float64)
         ok = np.zeros((B, L), np.uint8)
         pu = np.zeros(B, np.int32)
-        rc = _native.lib().pb_decode_paths(self._h, _ptr(frames), in_type, B, _ptr(cw), _ptr(pm),
+        rc = _native.lib().pb_decode_paths(self._h, ctypes.c_void_p(ptr), in_type, B, _ptr(cw), _ptr(pm),
                                            _ptr(ok), _ptr(pu), None)
         _native.check(rc, "pb_decode_paths")
         return cw, pm, ok.astype(bool), pu
