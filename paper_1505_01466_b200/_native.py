@@ -18,9 +18,9 @@ LIB_DIR = os.path.join(_PKG, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libpolar_b200.so")
 INCLUDE = os.path.join(_REPO, "include")
 
-NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
-              "-Xcompiler", "-fPIC", "-shared"]
-SOURCES = ["decode_kernel.cu", "runtime.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC"]
+BUILD_DIR = os.path.join(LIB_DIR, "obj")
 
 # C ABI constants (include/polar_b200.h)
 PB_OK, PB_EINVAL, PB_ECUDA, PB_EINTERNAL, PB_ENOMEM = 0, -1, -2, -3, -4
@@ -44,15 +44,64 @@ class PbOp(ctypes.Structure):
                 ("side", ctypes.c_int32), ("spc_truncated", ctypes.c_int32)]
 
 
-def build(verbose: bool = False) -> str:
+def shapes() -> list[tuple[str, str, int, int, int]]:
+    """(tag, element type, mode, warps per frame, paths per warp) from csrc/shapes.def."""
+    out = []
+    with open(os.path.join(CSRC, "shapes.def")) as fh:
+        for line in fh:
+            line = line.strip()
+            if line.startswith("PB_SHAPE("):
+                tag, t, mode, w, ppw = [x.strip() for x in line[9:-1].split(",")]
+                out.append((tag, t, int(mode), int(w), int(ppw)))
+    return out
+
+
+def _stale(obj: str, deps: list[str]) -> bool:
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(verbose: bool = False, jobs: int | None = None) -> str:
     """Compile the CUDA sources in-tree for sm_100a (nvcc cross-compiles
-    without a GPU)."""
-    os.makedirs(LIB_DIR, exist_ok=True)
-    cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, *[os.path.join(CSRC, s) for s in SOURCES],
-           "-o", LIB_PATH]
+    without a GPU): one object per kernel shape (compiled in parallel), the
+    dispatcher and the host runtime, linked into one shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(BUILD_DIR, exist_ok=True)
+    hdrs = [os.path.join(CSRC, f) for f in ("decode_kernel.cuh", "decoder.cuh", "shapes.def")]
+    hdrs.append(os.path.join(INCLUDE, "polar_b200.h"))
+    extra = ["-Xptxas=-v"] if verbose else []
+    cmds = []
+    objs = []
+    inst = os.path.join(CSRC, "decode_inst.cu")
+    for tag, t, mode, w, ppw in shapes():
+        obj = os.path.join(BUILD_DIR, f"decode_{tag}.o")
+        objs.append(obj)
+        if _stale(obj, [inst, *hdrs]):
+            cmds.append(["nvcc", *NVCC_FLAGS, *extra, "-I", INCLUDE, f"-DPB_T={t}", f"-DPB_W={w}",
+                         f"-DPB_PPW={ppw}", f"-DPB_TAG={tag}", "-c", inst, "-o", obj])
+    for src in ("dispatch.cu", "runtime.cu"):
+        obj = os.path.join(BUILD_DIR, src.replace(".cu", ".o"))
+        objs.append(obj)
+        if _stale(obj, [os.path.join(CSRC, src), *hdrs]):
+            cmds.append(["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj])
+    jobs = jobs or max(1, min(len(cmds), os.cpu_count() or 1))
+
+    def run(cmd):
+        r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed: {' '.join(cmd)}\n{r.stderr}")
+        return r.stderr
+
+    with ThreadPoolExecutor(jobs) as pool:
+        logs = list(pool.map(run, cmds))
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True, cwd=CSRC)
+        for lg in logs:
+            print(lg)
+    tmp = LIB_PATH + ".tmp"
+    subprocess.run(["nvcc", *ARCH, "-shared", "-o", tmp, *objs], check=True, cwd=CSRC)
+    os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
 

@@ -1,26 +1,31 @@
-// decode_kernel.cu -- Fast-SSC list-CRC decode kernel for sm_100a.
+// decode_kernel.cuh -- Fast-SSC list-CRC decode kernel for sm_100a.
+// Instantiated per (mode, W, PPW) by decode_inst.cu; dispatched in dispatch.cu.
 //
 // One CTA of W warps decodes one frame at a time (persistent loop over
-// frames).  The L path slots are split across the warps (PPW = L/W per warp);
-// a warp only synchronises with the others at leaves.  Per op:
+// frames).  The L path slots are split across the warps, PPW per warp
+// (compile-time, a power of two); a warp only synchronises with the others at
+// leaves.  Per op:
 //   F / G      element-parallel over the warp's (path, element) pairs: its A
 //              active paths split 32 lanes into groups of G = 32/pow2(A)
-//              (kernels.py:39-56, listdec.py:319-326)
-//   leaves     group scans of the node LLRs: pairwise-exact float sums
+//              (kernels.py:39-56, listdec.py:319-326).  In the steady state
+//              (A = PPW) G is a compile-time constant and the loops address
+//              shared memory with immediate offsets.
+//   leaves     per-path scans of the node LLRs: numpy-pairwise-exact float sums
 //              (Rate-0 / Rep, listdec.py:340-359), stable two / four least
 //              reliable positions + hard decisions + parity (Rate-1 / SPC,
 //              listdec.py:360-394)
-//   selection  warp 0, lane = source path: each lane's candidates form a
-//              sorted column; the L-th best metric comes from warp-shuffle
-//              bitonic sorts of the columns (early exit once no column entry
-//              can enter), exact ties resolved by (source, cand) prefix
-//              counts -- listdec.py:63-100
+//   selection  warp 0, lane = source path: candidate metrics as orderable
+//              int64 keys, each lane's candidates a sorted column; the L-th
+//              best key from warp-shuffle bitonic sorts of the columns (early
+//              exit once no column entry can enter), exact ties resolved by
+//              (source, cand) prefix counts -- listdec.py:63-100
 //   materialise survivors copy their source's row-index vectors (lazy copy,
 //              listdec.py:103-143,397-434), write the leaf word and run the
 //              leaf's chain of Combines in place (listdec.py:327-332)
 //   finalise   CRC by per-path GF(2) syndrome == constant, strict-max pick
 //              among CRC-passing paths (listdec.py:289-308), polar transform
 //              of the winner and payload gather (encode.py:29-53,76-87)
+#pragma once
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -36,6 +41,8 @@ extern __shared__ __align__(16) unsigned char g_smem[];
 namespace pb {
 
 #define FULL_MASK 0xffffffffu
+
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
 
 template <typename T>
 struct Elem;
@@ -55,7 +62,7 @@ struct Elem<int8_t> {
 // min-sum F: sign(a) sign(b) min(|a|,|b|); a zero product comes out as a
 // signed zero, numerically equal to the reference's 0 (kernels.py:39-48)
 __device__ __forceinline__ float f_op(float a, float b) {
-    unsigned s = (__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u;
+    const unsigned s = (__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u;
     return __uint_as_float(__float_as_uint(fminf(fabsf(a), fabsf(b))) | s);
 }
 
@@ -68,22 +75,19 @@ __device__ __forceinline__ float g_op(float a, float b, unsigned bit) {
     return v;
 }
 
-__device__ __forceinline__ int pow2ceil(int x) { return x <= 1 ? 1 : 1 << (32 - __clz(x - 1)); }
 __device__ __forceinline__ int log2ceil(int x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
 // ------------------------------------------------------------- sources
-// A stored alpha row (block-interleaved, stride ppw between elements)
-template <typename T>
+// stored alpha row: block-interleaved, element i at p[i * PPW]
+template <typename T, int PPW>
 struct RowSrc {
     const T *p;
-    int ppw;
-    __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(p + i * ppw); }
+    __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(p + i * PPW); }
 };
-template <typename T>
+template <typename T, int PPW>
 struct RowDst {
     T *p;
-    int ppw;
-    __device__ __forceinline__ void put(int i, float v) const { Elem<T>::st(p + i * ppw, v); }
+    __device__ __forceinline__ void put(int i, float v) const { Elem<T>::st(p + i * PPW, v); }
 };
 // stage n-1 in the left half of the tree: f(channel halves)
 template <typename T>
@@ -113,8 +117,11 @@ struct ChanSrc {
 
 // ------------------------------------------------------- frame state
 
-template <typename T, int W>
+template <typename T, int W, int PPW>
 struct Dec {
+    static constexpr int LP = ilog2(PPW);
+    static constexpr int GSS = 32 / PPW;           // steady-state lanes per path
+    static constexpr int NBUF = W > 1 ? 2 : 1;     // candidate buffers
     const Params &P;
     unsigned char *gs;  // this frame's global scratch block
     int lane, warp;
@@ -125,10 +132,8 @@ struct Dec {
     __device__ Dec(const Params &p, unsigned char *g)
         : P(p), gs(g), lane(threadIdx.x & 31), warp(threadIdx.x >> 5), cur(0), par(0), lpar(0) {}
 
-    // row r, element 0 of a block-interleaved stage s (ppw is a power of two)
-    __device__ __forceinline__ int rowoff(int s, int r) const {
-        return ((r >> P.lppw) << (P.lppw + s)) + (r & (P.ppw - 1));
-    }
+    // row r, element 0 of a block-interleaved stage s
+    __device__ __forceinline__ int rowoff(int s, int r) const { return ((r >> LP) << (LP + s)) + (r & (PPW - 1)); }
     __device__ __forceinline__ T *a_sm(int s) const { return reinterpret_cast<T *>(g_smem + P.lay.a_off[s]); }
     __device__ __forceinline__ T *a_gl(int s) const { return reinterpret_cast<T *>(gs + P.lay.a_off[s]); }
     __device__ __forceinline__ uint32_t *beta_row(int s, int row) const {
@@ -141,25 +146,28 @@ struct Dec {
     __device__ __forceinline__ uint32_t *syn(int b) const {
         return reinterpret_cast<uint32_t *>(g_smem + P.lay.syn_off) + b * P.L;
     }
-    __device__ __forceinline__ uint8_t *ia(int b, int q) const {
-        return g_smem + P.lay.ia_off + (b * P.L + q) * P.lay.idx_stride;
+    // alpha / beta row index of path q at stage / slot s: [buf][s][path]
+    __device__ __forceinline__ uint8_t &ia(int b, int s, int q) const {
+        return g_smem[P.lay.ia_off + (b * P.lay.idx_stride + s) * P.L + q];
     }
-    __device__ __forceinline__ uint8_t *ib(int b, int q) const {
-        return g_smem + P.lay.ib_off + (b * P.L + q) * P.lay.idx_stride;
+    __device__ __forceinline__ uint8_t &ib(int b, int s, int q) const {
+        return g_smem[P.lay.ib_off + (b * P.lay.idx_stride + s) * P.L + q];
     }
-    __device__ __forceinline__ double *cd(int b, int q) const {
-        return reinterpret_cast<double *>(g_smem + P.lay.cd_off) + (b * P.L + q) * kMaxCand;
+    __device__ __forceinline__ int bsel(int b) const { return NBUF > 1 ? b : 0; }
+    // candidate data: [buf][entry][source path]
+    __device__ __forceinline__ double &cd(int b, int c, int q) const {
+        return reinterpret_cast<double *>(g_smem + P.lay.cd_off)[(bsel(b) * kMaxCand + c) * P.L + q];
     }
-    __device__ __forceinline__ uint16_t *clrb(int b, int q) const {
-        return reinterpret_cast<uint16_t *>(g_smem + P.lay.clrb_off) + (b * P.L + q) * 4;
+    __device__ __forceinline__ uint16_t &clrb(int b, int j, int q) const {
+        return reinterpret_cast<uint16_t *>(g_smem + P.lay.clrb_off)[(bsel(b) * 4 + j) * P.L + q];
     }
     __device__ __forceinline__ uint32_t *chs(int b) const {
-        return reinterpret_cast<uint32_t *>(g_smem + P.lay.chs_off) + b * P.L;
+        return reinterpret_cast<uint32_t *>(g_smem + P.lay.chs_off) + bsel(b) * P.L;
     }
-    __device__ __forceinline__ uint8_t *cflag(int b) const { return g_smem + P.lay.cflag_off + b * P.L; }
-    __device__ __forceinline__ uint8_t *asg(int b) const { return g_smem + P.lay.asg_off + b * 2 * P.L; }
-    __device__ __forceinline__ uint32_t *hard(int b, int q) const {
-        return reinterpret_cast<uint32_t *>(g_smem + P.lay.hard_off) + (b * P.L + q) * P.lay.hard_words;
+    __device__ __forceinline__ uint8_t *cflag(int b) const { return g_smem + P.lay.cflag_off + bsel(b) * P.L; }
+    __device__ __forceinline__ uint8_t *asg(int b) const { return g_smem + P.lay.asg_off + bsel(b) * 2 * P.L; }
+    __device__ __forceinline__ uint32_t &hard(int b, int w, int q) const {
+        return reinterpret_cast<uint32_t *>(g_smem + P.lay.hard_off)[(bsel(b) * P.lay.hard_words + w) * P.L + q];
     }
     __device__ __forceinline__ uint32_t *root() const { return reinterpret_cast<uint32_t *>(g_smem + P.lay.root_off); }
 
@@ -172,27 +180,29 @@ struct Dec {
 
     // lane -> (path, sub-lane) for this warp when np paths are active
     struct Map {
-        int q, sub, G;
+        int q, sub, G, lg;
         bool active;
     };
     __device__ __forceinline__ Map map(int np) const {
         Map m;
-        int act = np - warp * P.ppw;
-        act = act < 0 ? 0 : (act > P.ppw ? P.ppw : act);
-        const int lg = 5 - log2ceil(act > 0 ? act : 1);
-        m.G = 1 << lg;
-        const int ql = lane >> lg;
+        int act = np - warp * PPW;
+        act = act < 0 ? 0 : (act > PPW ? PPW : act);
+        m.lg = 5 - log2ceil(act > 0 ? act : 1);
+        m.G = 1 << m.lg;
+        const int ql = lane >> m.lg;
         m.sub = lane & (m.G - 1);
         m.active = ql < act;
-        m.q = warp * P.ppw + ql;
+        m.q = warp * PPW + ql;
         return m;
     }
 };
 
 // ---------------------------------------------------------------- F / G
 
-template <typename T, bool IS_G, class S, class D>
-__device__ __forceinline__ void fg_loop(const S &src, const D &dst, const uint32_t *bw, int h, int G, int sub) {
+// G lanes per path; GC > 0: G known at compile time (steady state)
+template <typename T, bool IS_G, int GC, class S, class D>
+__device__ __forceinline__ void fg_loop(const S &src, const D &dst, const uint32_t *bw, int h, int Grt, int sub) {
+    const int G = GC > 0 ? GC : Grt;
     if (!IS_G) {
 #pragma unroll 4
         for (int i = sub; i < h; i += G) dst.put(i, f_op(src.get(i), src.get(i + h)));
@@ -201,42 +211,82 @@ __device__ __forceinline__ void fg_loop(const S &src, const D &dst, const uint32
         for (int c0 = 0; c0 < h; c0 += 32) {
             const uint32_t word = bw[c0 >> 5];
 #pragma unroll 4
-            for (int j = sub; j < lim; j += G) dst.put(c0 + j, g_op<T>(src.get(c0 + j), src.get(c0 + j + h), (word >> j) & 1u));
+            for (int j = sub; j < lim; j += G)
+                dst.put(c0 + j, g_op<T>(src.get(c0 + j), src.get(c0 + j + h), (word >> j) & 1u));
         }
     }
 }
 
-template <typename T, int W, bool IS_G, class S>
-__device__ __forceinline__ void fg_to_dst(const Dec<T, W> &F, const S &src, int s, int q, const uint32_t *bw, int h,
-                                          int G, int sub) {
-    const int off = F.rowoff(s - 1, q);
-    if (s - 1 < F.P.lay.a_gfrom)
-        fg_loop<T, IS_G>(src, RowDst<T>{F.a_sm(s - 1) + off, F.P.ppw}, bw, h, G, sub);
-    else
-        fg_loop<T, IS_G>(src, RowDst<T>{F.a_gl(s - 1) + off, F.P.ppw}, bw, h, G, sub);
+// Steady state (G = GC lanes per path, compile-time) with h >= 32: 32-element
+// chunks, the lane's elements of a chunk in unrolled blocks of U whose loads
+// all issue before the stores (immediate offsets, beta word loaded once).
+template <typename T, bool IS_G, int GC, int PPW, class S>
+__device__ __forceinline__ void fg_chunks(const S &src, T *dst, const uint32_t *bw, int h, int sub) {
+    constexpr int PER = 32 / GC;            // this lane's elements per chunk
+    constexpr int U = PER < 8 ? PER : 8;    // unrolled block
+    for (int c0 = 0; c0 < h; c0 += 32) {
+        const uint32_t wsh = IS_G ? (bw[c0 >> 5] >> sub) : 0u;
+        T *d = dst + (c0 + sub) * PPW;
+#pragma unroll
+        for (int blk = 0; blk < PER; blk += U) {
+            float a[U], b[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = c0 + sub + (blk + u) * GC;
+                a[u] = src.get(i);
+                b[u] = src.get(i + h);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const float v = IS_G ? g_op<T>(a[u], b[u], (wsh >> ((blk + u) * GC)) & 1u) : f_op(a[u], b[u]);
+                Elem<T>::st(d + (blk + u) * GC * PPW, v);
+            }
+        }
+    }
 }
 
-template <typename T, int W, bool IS_G>
-__device__ __forceinline__ void fg_op(Dec<T, W> &F, const DOp &o) {
+template <typename T, int W, int PPW, bool IS_G, class S>
+__device__ __forceinline__ void fg_to_dst(const Dec<T, W, PPW> &F, const S &src, int s, int q, const uint32_t *bw,
+                                          int h, int G, int sub) {
+    constexpr int GS = Dec<T, W, PPW>::GSS;
+    const int off = F.rowoff(s - 1, q);
+    if (s - 1 < F.P.lay.a_gfrom) {
+        T *d = F.a_sm(s - 1) + off;
+        if (G == GS && h >= 32)
+            fg_chunks<T, IS_G, GS, PPW>(src, d, bw, h, sub);
+        else
+            fg_loop<T, IS_G, 0>(src, RowDst<T, PPW>{d}, bw, h, G, sub);
+    } else {
+        T *d = F.a_gl(s - 1) + off;
+        if (G == GS && h >= 32)
+            fg_chunks<T, IS_G, GS, PPW>(src, d, bw, h, sub);
+        else
+            fg_loop<T, IS_G, 0>(src, RowDst<T, PPW>{d}, bw, h, G, sub);
+    }
+}
+
+template <typename T, int W, int PPW, bool IS_G>
+__device__ __forceinline__ void fg_op(Dec<T, W, PPW> &F, const DOp &o) {
     const auto mp = F.map(o.pin);
     if (!mp.active) return;
     const Params &P = F.P;
     const int s = o.stage, h = 1 << (s - 1), q = mp.q;
-    const uint32_t *bw = IS_G ? F.beta_row(s - 1, F.ib(F.cur, q)[s - 1]) : nullptr;
+    const uint32_t *bw = IS_G ? F.beta_row(s - 1, F.ib(F.cur, s - 1, q)) : nullptr;
     if (s == P.n - 1) {
         if (o.vmode == VM_F)
-            fg_to_dst<T, W, IS_G>(F, VirtF<T>{F.channel(), P.N >> 1}, s, q, bw, h, mp.G, mp.sub);
+            fg_to_dst<T, W, PPW, IS_G>(F, VirtF<T>{F.channel(), P.N >> 1}, s, q, bw, h, mp.G, mp.sub);
         else
-            fg_to_dst<T, W, IS_G>(F, VirtG<T>{F.channel(), F.beta_row(P.n - 1, F.ib(F.cur, q)[P.n - 1]), P.N >> 1},
-                                  s, q, bw, h, mp.G, mp.sub);
+            fg_to_dst<T, W, PPW, IS_G>(
+                F, VirtG<T>{F.channel(), F.beta_row(P.n - 1, F.ib(F.cur, P.n - 1, q)), P.N >> 1}, s, q, bw, h, mp.G,
+                mp.sub);
     } else {
-        const int off = F.rowoff(s, F.ia(F.cur, q)[s]);
+        const int off = F.rowoff(s, F.ia(F.cur, s, q));
         if (s < P.lay.a_gfrom)
-            fg_to_dst<T, W, IS_G>(F, RowSrc<T>{F.a_sm(s) + off, P.ppw}, s, q, bw, h, mp.G, mp.sub);
+            fg_to_dst<T, W, PPW, IS_G>(F, RowSrc<T, PPW>{F.a_sm(s) + off}, s, q, bw, h, mp.G, mp.sub);
         else
-            fg_to_dst<T, W, IS_G>(F, RowSrc<T>{F.a_gl(s) + off, P.ppw}, s, q, bw, h, mp.G, mp.sub);
+            fg_to_dst<T, W, PPW, IS_G>(F, RowSrc<T, PPW>{F.a_gl(s) + off}, s, q, bw, h, mp.G, mp.sub);
     }
-    if (mp.sub == 0) F.ia(F.cur, q)[s - 1] = (uint8_t)q;
+    if (mp.sub == 0) F.ia(F.cur, s - 1, q) = (uint8_t)q;
 }
 
 // ------------------------------------------------- pairwise-exact sums
@@ -245,10 +295,11 @@ __device__ __forceinline__ void fg_op(Dec<T, W> &F, const DOp &o) {
 // ((0+1)+(2+3))+((4+5)+(6+7)); larger n halves recursively.  For power-of-
 // two node sizes that is a perfect binary tree over 8*nb accumulators
 // (nb = max(1, n/128)), each a sequential sum of min(n,128)/8 elements.
-// Lane j of an 8-lane group owns accumulator column j of every 128-block.
+// GS lanes of a group share the 8 accumulator columns (lane sub owns columns
+// j = sub + a*GS); tree levels on lane bits shuffle, the rest stay in registers.
 
 template <int NS>
-__device__ __forceinline__ void acc_add(float (&acc)[NS], float a) {
+__device__ __forceinline__ void acc_add(float *acc, float a) {
     acc[0] = __fadd_rn(acc[0], fminf(a, 0.f));
     if (NS == 3) {
         acc[1] = __fadd_rn(acc[1], fmaxf(a, 0.f));
@@ -256,7 +307,7 @@ __device__ __forceinline__ void acc_add(float (&acc)[NS], float a) {
     }
 }
 template <int NS>
-__device__ __forceinline__ void acc_init(float (&acc)[NS], float a) {
+__device__ __forceinline__ void acc_init(float *acc, float a) {
     acc[0] = fminf(a, 0.f);
     if (NS == 3) {
         acc[1] = fmaxf(a, 0.f);
@@ -265,51 +316,84 @@ __device__ __forceinline__ void acc_init(float (&acc)[NS], float a) {
 }
 
 // NS = 1: sum min(a,0); NS = 3: (sum min(a,0), sum max(a,0), sum a).
-// Result valid in every lane of the 8-lane group.
-template <int NS, class S>
-__device__ __forceinline__ void group8_pairwise(const S &src, int m, bool active, int j, float (&out)[NS]) {
+// Valid in the group leader lane.
+template <int NS, int GS, class S>
+__device__ __forceinline__ void pw_sums(const S &src, int m, bool active, int sub, int lead, float (&out)[NS]) {
     if (m < 8) {
         float r[NS];
 #pragma unroll
         for (int t = 0; t < NS; ++t) r[t] = 0.f;
-        if (active && j == 0)
+        if (active && sub == 0)
             for (int i = 0; i < m; ++i) acc_add<NS>(r, src.get(i));
 #pragma unroll
-        for (int t = 0; t < NS; ++t) out[t] = __shfl_sync(FULL_MASK, r[t], (threadIdx.x & 31) & ~7);
+        for (int t = 0; t < NS; ++t) out[t] = r[t];
         return;
     }
+    constexpr int NA = 8 / GS;  // accumulator columns per lane
+    constexpr int LG = ilog2(GS);
     const int blk = m < 128 ? m : 128;
     const int nb = m / blk;
-    const int per = blk / 8;
-    float stk[NS][8];
+    const int per = blk >> 3;
+    const bool act = active && sub < GS;
+    float stk[8][NS];
     float carry[NS];
     for (int b = 0; b < nb; ++b) {
-        float acc[NS];
-        const int base = b * blk + j;
-        if (active) {
-            acc_init<NS>(acc, src.get(base));
-            for (int r = 1; r < per; ++r) acc_add<NS>(acc, src.get(base + 8 * r));
-        } else {
+        float acc[NA][NS];
 #pragma unroll
-            for (int t = 0; t < NS; ++t) acc[t] = 0.f;
+        for (int a = 0; a < NA; ++a) {
+            const int base = b * blk + sub + a * GS;
+            if (act) {
+                acc_init<NS>(acc[a], src.get(base));
+                for (int r = 1; r < per; ++r) acc_add<NS>(acc[a], src.get(base + 8 * r));
+            } else {
+#pragma unroll
+                for (int t = 0; t < NS; ++t) acc[a][t] = 0.f;
+            }
+        }
+        // levels 0..2 of the column tree: lane bits shuffle, register bits add
+#pragma unroll
+        for (int lv = 0; lv < 3; ++lv) {
+            if (lv < LG) {
+#pragma unroll
+                for (int a = 0; a < NA; ++a)
+#pragma unroll
+                    for (int t = 0; t < NS; ++t)
+                        acc[a][t] = __fadd_rn(acc[a][t], __shfl_xor_sync(FULL_MASK, acc[a][t], 1 << lv));
+            } else {
+                const int step = 1 << (lv - LG);
+#pragma unroll
+                for (int a = 0; a < NA; ++a)
+                    if ((a & step) == 0 && a + step < NA)
+#pragma unroll
+                        for (int t = 0; t < NS; ++t) acc[a][t] = __fadd_rn(acc[a][t], acc[a + step][t]);
+            }
         }
 #pragma unroll
-        for (int d = 1; d < 8; d <<= 1)
-#pragma unroll
-            for (int t = 0; t < NS; ++t) acc[t] = __fadd_rn(acc[t], __shfl_xor_sync(FULL_MASK, acc[t], d));
-#pragma unroll
-        for (int t = 0; t < NS; ++t) carry[t] = acc[t];
+        for (int t = 0; t < NS; ++t) carry[t] = acc[0][t];
         int lvl = 0;
         while ((b >> lvl) & 1) {
 #pragma unroll
-            for (int t = 0; t < NS; ++t) carry[t] = __fadd_rn(stk[t][lvl], carry[t]);
+            for (int t = 0; t < NS; ++t) carry[t] = __fadd_rn(stk[lvl][t], carry[t]);
             ++lvl;
         }
 #pragma unroll
-        for (int t = 0; t < NS; ++t) stk[t][lvl] = carry[t];
+        for (int t = 0; t < NS; ++t) stk[lvl][t] = carry[t];
     }
 #pragma unroll
     for (int t = 0; t < NS; ++t) out[t] = carry[t];
+}
+
+template <int NS, class S>
+__device__ __forceinline__ void pw_sums_rt(const S &src, int m, bool active, int G, int sub, int lead,
+                                           float (&out)[NS]) {
+    if (G == 1)
+        pw_sums<NS, 1>(src, m, active, sub, lead, out);
+    else if (G == 2)
+        pw_sums<NS, 2>(src, m, active, sub, lead, out);
+    else if (G == 4)
+        pw_sums<NS, 4>(src, m, active, sub, lead, out);
+    else
+        pw_sums<NS, 8>(src, m, active, sub, lead, out);
 }
 
 // ------------------------------------------------ least reliable positions
@@ -339,27 +423,57 @@ struct TopK {
             }
         }
     }
-    // ascending index scan: a value equal to the current K-th keeps the
-    // earlier index, so only strictly smaller values enter (stable argsort)
+    // ascending index scan: only strictly smaller values enter (stable argsort);
+    // once placed, the displaced entries shift down unconditionally
     __device__ __forceinline__ void push_scan(float v, int idx) {
-        if (v < m[K - 1]) insert(v, idx);
+        if (v < m[K - 1]) {
+            bool placed = false;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const bool lt = placed || v < m[k];
+                placed = lt;
+                const float tm = m[k];
+                const int ti = i[k];
+                if (lt) {
+                    m[k] = v;
+                    i[k] = idx;
+                    v = tm;
+                    idx = ti;
+                }
+            }
+        }
     }
 };
 
 // ------------------------------------------------------------ selection
 
-__device__ __forceinline__ void bitonic_sort(double &v, int Wd, bool desc, int lane) {
+// total order of float64 metrics as int64 (-0.0 folded onto +0.0)
+__device__ __forceinline__ long long okey(double x) {
+    const long long b = __double_as_longlong(x + 0.0);
+    return b ^ ((b >> 63) & 0x7fffffffffffffffLL);
+}
+__device__ __forceinline__ long long shfl_xor_ll(long long v, int j) {
+    const int lo = __shfl_xor_sync(FULL_MASK, (int)(v & 0xffffffff), j);
+    const int hi = __shfl_xor_sync(FULL_MASK, (int)(v >> 32), j);
+    return ((long long)hi << 32) | (unsigned)lo;
+}
+__device__ __forceinline__ long long shfl_ll(long long v, int src) {
+    const int lo = __shfl_sync(FULL_MASK, (int)(v & 0xffffffff), src);
+    const int hi = __shfl_sync(FULL_MASK, (int)(v >> 32), src);
+    return ((long long)hi << 32) | (unsigned)lo;
+}
+__device__ __forceinline__ void bitonic_sort(long long &v, int Wd, bool desc, int lane) {
     for (int k = 2; k <= Wd; k <<= 1)
         for (int j = k >> 1; j > 0; j >>= 1) {
-            const double o = __shfl_xor_sync(FULL_MASK, v, j);
-            const bool seg_desc = ((lane & k) == 0) == desc;
-            v = (((lane & j) == 0) == seg_desc) ? fmax(v, o) : fmin(v, o);
+            const long long o = shfl_xor_ll(v, j);
+            const bool want_max = (((lane & j) == 0) == (((lane & k) == 0) == desc));
+            v = (want_max == (o > v)) ? o : v;
         }
 }
-__device__ __forceinline__ void bitonic_merge_desc(double &v, int Wd, int lane) {
+__device__ __forceinline__ void bitonic_merge_desc(long long &v, int Wd, int lane) {
     for (int j = Wd >> 1; j > 0; j >>= 1) {
-        const double o = __shfl_xor_sync(FULL_MASK, v, j);
-        v = ((lane & j) == 0) ? fmax(v, o) : fmin(v, o);
+        const long long o = shfl_xor_ll(v, j);
+        v = (((lane & j) == 0) == (o > v)) ? o : v;
     }
 }
 __device__ __forceinline__ int excl_scan(int v, int lane) {
@@ -382,68 +496,69 @@ __device__ __forceinline__ int flip_mask(int kind, int c, int odd) {
     return c == 0 ? ml : (kSpcPairs[c - 1] ^ ml);
 }
 
-// Phase B (warp 0, lane = source): survivors -> asg[par][k] = (source, cand)
-// in (source, cand) order.  The L best by (metric desc, source asc, cand asc)
+// Phase B (warp 0, lane = source): survivors -> asg[k] = (source, cand) in
+// (source, cand) order.  The L best by (metric desc, source asc, cand asc)
 // == listdec.py:63-100 (bounded heap == full sort, tests/oracles.py:74-89).
-template <typename T, int W>
-__device__ __forceinline__ void select_phase(const Dec<T, W> &F, const DOp &o) {
+template <typename T, int W, int PPW>
+__device__ __forceinline__ void select_phase(const Dec<T, W, PPW> &F, const DOp &o) {
     const int lane = F.lane, np = o.pin, C = o.ncand, L = F.P.L;
     const bool vl = lane < np;
     const double pm = vl ? F.pm(F.cur)[lane] : 0.0;
-    const double *cd = F.cd(F.par, vl ? lane : 0);
-    double met[kMaxCand];
+    long long key[kMaxCand];
 #pragma unroll
-    for (int c = 0; c < kMaxCand; ++c) met[c] = (vl && c < C) ? pm + cd[c] : -INFINITY;
+    for (int c = 0; c < kMaxCand; ++c) key[c] = (vl && c < C) ? okey(pm + F.cd(F.par, c, lane)) : LLONG_MIN;
     unsigned mask;
     if (!o.select) {
         mask = vl ? (1u << C) - 1u : 0u;
     } else {
-        double srt[kMaxCand];
+        long long srt[kMaxCand];
 #pragma unroll
-        for (int c = 0; c < kMaxCand; ++c) srt[c] = met[c];
+        for (int c = 0; c < kMaxCand; ++c) srt[c] = key[c];
         // best-first column per lane (Rate-1 columns already are:
         // 0 >= -m1 >= -m2 >= -(m1+m2), monotone under rounding)
-        if (C != 4) {
+        if (C == 2) {
+            const long long a = srt[0], b = srt[1];
+            srt[0] = a > b ? a : b;
+            srt[1] = a > b ? b : a;
+        } else if (C == 8) {
 #pragma unroll
-            for (int pass = 0; pass < kMaxCand; ++pass) {
-                if (pass >= C) break;
+            for (int pass = 0; pass < 8; ++pass)
 #pragma unroll
-                for (int c = pass & 1; c + 1 < kMaxCand; c += 2) {
-                    const double a = srt[c], b = srt[c + 1];
-                    srt[c] = fmax(a, b);
-                    srt[c + 1] = fmin(a, b);
+                for (int c = pass & 1; c + 1 < 8; c += 2) {
+                    const long long a = srt[c], b = srt[c + 1];
+                    srt[c] = a > b ? a : b;
+                    srt[c + 1] = a > b ? b : a;
                 }
-            }
         }
-        const int Wd = pow2ceil(L);
-        double R = srt[0];
+        const int Wd = 1 << log2ceil(L);
+        long long R = srt[0];
         bitonic_sort(R, Wd, true, lane);
-        double Tm = __shfl_sync(FULL_MASK, R, L - 1);
+        long long Tk = shfl_ll(R, L - 1);
 #pragma unroll
         for (int j = 1; j < kMaxCand; ++j) {
             if (j >= C) break;
-            double x = srt[j];
-            if (!__any_sync(FULL_MASK, x > Tm)) break;
+            long long x = srt[j];
+            if (!__any_sync(FULL_MASK, x > Tk)) break;
             bitonic_sort(x, Wd, false, lane);
-            R = fmax(R, x);
+            R = R > x ? R : x;
             bitonic_merge_desc(R, Wd, lane);
-            Tm = __shfl_sync(FULL_MASK, R, L - 1);
+            Tk = shfl_ll(R, L - 1);
         }
-        // Tm = the L-th best metric; keep all better, then the earliest ties
+        // Tk = the L-th best key; keep all better, then the earliest ties
         int gt = 0, eq = 0;
 #pragma unroll
         for (int c = 0; c < kMaxCand; ++c) {
-            gt += met[c] > Tm;
-            eq += met[c] == Tm;
+            gt += key[c] > Tk;
+            eq += key[c] == Tk;
         }
         const int need = L - (int)__reduce_add_sync(FULL_MASK, (unsigned)gt);
         int r = excl_scan(eq, lane);
         mask = 0u;
 #pragma unroll
         for (int c = 0; c < kMaxCand; ++c) {
-            if (met[c] > Tm) {
+            if (key[c] > Tk) {
                 mask |= 1u << c;
-            } else if (met[c] == Tm) {
+            } else if (key[c] == Tk) {
                 if (r < need) mask |= 1u << c;
                 ++r;
             }
@@ -463,21 +578,21 @@ __device__ __forceinline__ void select_phase(const Dec<T, W> &F, const DOp &o) {
 // ----------------------------------------------------- leaf word + chain
 
 // 32-bit word w of the leaf word of decision (p, c) (m < 32: the m-bit value)
-template <typename T, int W>
-__device__ __forceinline__ uint32_t leaf_word(const Dec<T, W> &F, int b, int kind, int m, int p, int c, int w) {
+template <typename T, int W, int PPW>
+__device__ __forceinline__ uint32_t leaf_word(const Dec<T, W, PPW> &F, int b, int kind, int m, int p, int c,
+                                              int w) {
     const uint32_t fullw = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
     if (kind == DK_R0) return 0u;
     if (kind == DK_REP) {
         const bool ones = F.cflag(b)[p] ? (c == 0) : (c == 1);
         return ones ? fullw : 0u;
     }
-    uint32_t v = F.hard(b, p)[w];
+    uint32_t v = F.hard(b, w, p);
     const int fm = flip_mask(kind, c, F.cflag(b)[p]);
-    const uint16_t *lrb = F.clrb(b, p);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
         if ((fm >> j) & 1) {
-            const int pos = lrb[j];
+            const int pos = F.clrb(b, j, p);
             if ((pos >> 5) == w) v ^= 1u << (pos & 31);
         }
     return v;
@@ -498,9 +613,10 @@ __device__ __forceinline__ void bits_put(uint32_t *row, int off, int len, uint32
 //   dst[E - 2^(s+1), E - 2^s) = slot_s[row_s] ^ dst[E - 2^s, E)
 // (listdec.py:327-332 with the right child's bits kept where they are).
 // Called by all lanes of a warp (synchronises the warp between steps).
-template <typename T, int W>
-__device__ __forceinline__ void word_and_chain(const Dec<T, W> &F, int b, const DOp &o, int kind, bool active, int G, int sub,
-                               int p, int c, const uint8_t *ibsrc, uint32_t *dst, int sE) {
+template <typename T, int W, int PPW>
+__device__ __forceinline__ void word_and_chain(const Dec<T, W, PPW> &F, int b, const DOp &o, int kind, bool active,
+                                               int G, int sub, int p, int c, int ibuf, int ipath, uint32_t *dst,
+                                               int sE) {
     const int t = o.stage, m = 1 << t, E = 1 << sE;
     if (active) {
         if (m >= 32) {
@@ -513,7 +629,7 @@ __device__ __forceinline__ void word_and_chain(const Dec<T, W> &F, int b, const 
     for (int s = t; s < sE; ++s) {
         const int seg = 1 << s;
         if (active) {
-            const uint32_t *sl = F.beta_row(s, ibsrc[s]);
+            const uint32_t *sl = F.beta_row(s, F.ib(ibuf, s, ipath));
             if (seg >= 32) {
                 const int a = (E - 2 * seg) >> 5, bb = (E - seg) >> 5;
                 for (int w = sub; w < (seg >> 5); w += G) dst[a + w] = sl[w] ^ dst[bb + w];
@@ -528,58 +644,68 @@ __device__ __forceinline__ void word_and_chain(const Dec<T, W> &F, int b, const 
 
 // ------------------------------------------------------------- leaves
 
-template <typename T, int W, class S>
-__device__ __forceinline__ void leaf_sums(Dec<T, W> &F, const DOp &o, int kind, const S &src, int q, bool active, int j) {
+template <typename T, int W, int PPW, class S>
+__device__ __forceinline__ void leaf_sums(Dec<T, W, PPW> &F, const DOp &o, int kind, const S &src, int q, bool active,
+                                          int G, int sub) {
     const int m = 1 << o.stage;
+    const int lead = F.lane - sub;
     if (kind == DK_R0) {
         float r[1];
-        group8_pairwise<1>(src, m, active, j, r);
-        if (active && j == 0) F.pm(F.cur)[q] += (double)r[0];  // listdec.py:341-343
+        pw_sums_rt<1>(src, m, active, G, sub, lead, r);
+        if (active && sub == 0) F.pm(F.cur)[q] += (double)r[0];  // listdec.py:341-343
     } else {
         float r[3];
-        group8_pairwise<3>(src, m, active, j, r);
-        if (active && j == 0) {  // listdec.py:348-358
+        pw_sums_rt<3>(src, m, active, G, sub, lead, r);
+        if (active && sub == 0) {  // listdec.py:348-358
             const bool ones_first = r[2] < 0.f;
-            double *cd = F.cd(F.par, q);
             const double neg = (double)r[0], pos = (double)r[1];
-            cd[0] = ones_first ? -pos : neg;
-            cd[1] = ones_first ? neg : -pos;
+            F.cd(F.par, 0, q) = ones_first ? -pos : neg;
+            F.cd(F.par, 1, q) = ones_first ? neg : -pos;
             F.cflag(F.par)[q] = ones_first;
         }
     }
 }
 
-template <typename T, int W, int K, class S>
-__device__ __forceinline__ void leaf_scan(Dec<T, W> &F, const DOp &o, int kind, const S &src, int q, bool active, int G, int sub) {
+// Gl (<= G) lanes of the path's group scan; the rest idle
+template <typename T, int W, int PPW, int K, class S>
+__device__ __forceinline__ void leaf_scan(Dec<T, W, PPW> &F, const DOp &o, int kind, const S &src, int q,
+                                          bool active, int G, int sub) {
     const Params &P = F.P;
     const int m = 1 << o.stage;
+    int Gl = m >> 4;
+    Gl = Gl < 1 ? 1 : (Gl > G ? G : Gl);
+    const int lgl = 31 - __clz(Gl);
+    const bool scan = active && sub < Gl;
     TopK<K> tk;
     tk.init();
     uint32_t hs = 0u, hword = 0u;
     int par = 0;
-    const int lgG = 31 - __clz(G);
-    const int iters = (m + G - 1) >> lgG;
-    uint32_t *hard = F.hard(F.par, active ? q : 0);
+    const int iters = (m + Gl - 1) >> lgl;
+    const int hq = active ? q : F.warp * PPW;
     const uint32_t *msyn = P.msyn + o.off;
-    const int gshift = (q - F.warp * P.ppw) * G;
-    const uint32_t gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+    const int gshift = F.lane - sub;  // group leader lane
+    const uint32_t gmask = Gl == 32 ? 0xffffffffu : ((1u << Gl) - 1u);
     for (int it = 0; it < iters; ++it) {
-        const int i = it * G + sub;
-        const bool valid = active && i < m;
+        const int i = (it << lgl) + sub;
+        const bool valid = scan && i < m;
         const float a = valid ? src.get(i) : 0.f;
         const bool neg = valid && a < 0.f;
         if (valid) tk.push_scan(fabsf(a), i);
         if (neg) hs ^= __ldg(msyn + i);
-        const uint32_t gb = (__ballot_sync(FULL_MASK, neg) >> (G == 32 ? 0 : gshift)) & gmask;
-        const int base = it * G;
+        uint32_t gb;
+        if (Gl == 1)
+            gb = neg;
+        else
+            gb = (__ballot_sync(FULL_MASK, neg) >> gshift) & gmask;
+        const int base = it << lgl;
         hword |= gb << (base & 31);
-        if (((base + G) & 31) == 0 || it == iters - 1) {
-            if (active && sub == 0) hard[base >> 5] = hword;
+        if (((base + Gl) & 31) == 0 || it == iters - 1) {
+            if (scan && sub == 0) F.hard(F.par, base >> 5, hq) = hword;
             par ^= __popc(hword);
             hword = 0u;
         }
     }
-    for (int d = 1; d < G; d <<= 1) {
+    for (int d = 1; d < Gl; d <<= 1) {
         hs ^= __shfl_xor_sync(FULL_MASK, hs, d);
         float om[K];
         int oi[K];
@@ -592,17 +718,16 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W> &F, const DOp &o, int kind, 
         for (int k = 0; k < K; ++k) tk.insert(om[k], oi[k]);
     }
     if (!(active && sub == 0)) return;
-    double *cd = F.cd(F.par, q);
-    uint16_t *lrb = F.clrb(F.par, q);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) lrb[k] = (uint16_t)(k < K && tk.i[k < K ? k : 0] < m ? tk.i[k < K ? k : 0] : 0);
+    for (int k = 0; k < 4; ++k)
+        F.clrb(F.par, k, q) = (uint16_t)(k < K && tk.i[k < K ? k : 0] < m ? tk.i[k < K ? k : 0] : 0);
     F.chs(F.par)[q] = hs;
     if (kind == DK_R1) {  // listdec.py:360-372
         const double w1 = (double)tk.m[0], w2 = (double)tk.m[1];
-        cd[0] = 0.0;
-        cd[1] = -w1;
-        cd[2] = -w2;
-        cd[3] = -(w1 + w2);
+        F.cd(F.par, 0, q) = 0.0;
+        F.cd(F.par, 1, q) = -w1;
+        F.cd(F.par, 2, q) = -w2;
+        F.cd(F.par, 3, q) = -(w1 + w2);
         F.cflag(F.par)[q] = 0;
         return;
     }
@@ -632,64 +757,55 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W> &F, const DOp &o, int kind, 
                 accd = any ? accd + w[ord[x]] : w[ord[x]];
                 any = true;
             }
-        cd[c] = any ? -accd : 0.0;
+        F.cd(F.par, c, q) = any ? -accd : 0.0;
     }
 }
 
-template <typename T, int W, class S>
-__device__ __forceinline__ void leaf_phase_a(Dec<T, W> &F, const DOp &o, int kind, const S &src, int q, bool active, int G, int sub,
-                             int j8) {
+template <typename T, int W, int PPW, class S>
+__device__ __forceinline__ void leaf_phase_a(Dec<T, W, PPW> &F, const DOp &o, int kind, const S &src, int q,
+                                             bool active, int G, int sub) {
     if (kind == DK_R0 || kind == DK_REP)
-        leaf_sums(F, o, kind, src, q, active, j8);
+        leaf_sums(F, o, kind, src, q, active, G, sub);
     else if (kind == DK_R1)
-        leaf_scan<T, W, 2>(F, o, kind, src, q, active, G, sub);
+        leaf_scan<T, W, PPW, 2>(F, o, kind, src, q, active, G, sub);
     else
-        leaf_scan<T, W, 4>(F, o, kind, src, q, active, G, sub);
+        leaf_scan<T, W, PPW, 4>(F, o, kind, src, q, active, G, sub);
 }
 
 // dispatch on where the node's LLRs live
-template <typename T, int W>
-__device__ __forceinline__ void leaf_read(Dec<T, W> &F, const DOp &o, int kind, int q, bool active, int G, int sub, int j8) {
+template <typename T, int W, int PPW>
+__device__ __forceinline__ void leaf_read(Dec<T, W, PPW> &F, const DOp &o, int kind, int q, bool active, int G,
+                                          int sub) {
     const Params &P = F.P;
     const int t = o.stage;
-    const int qq = active ? q : F.warp * P.ppw;
+    const int qq = active ? q : F.warp * PPW;
     if (t == P.n) {
-        leaf_phase_a(F, o, kind, ChanSrc<T>{F.channel()}, q, active, G, sub, j8);
+        leaf_phase_a(F, o, kind, ChanSrc<T>{F.channel()}, q, active, G, sub);
     } else if (t == P.n - 1) {
         if (o.vmode == VM_F)
-            leaf_phase_a(F, o, kind, VirtF<T>{F.channel(), P.N >> 1}, q, active, G, sub, j8);
+            leaf_phase_a(F, o, kind, VirtF<T>{F.channel(), P.N >> 1}, q, active, G, sub);
         else
-            leaf_phase_a(F, o, kind, VirtG<T>{F.channel(), F.beta_row(P.n - 1, F.ib(F.cur, qq)[P.n - 1]), P.N >> 1}, q,
-                         active, G, sub, j8);
+            leaf_phase_a(F, o, kind, VirtG<T>{F.channel(), F.beta_row(P.n - 1, F.ib(F.cur, P.n - 1, qq)), P.N >> 1}, q,
+                         active, G, sub);
     } else {
-        const int off = F.rowoff(t, F.ia(F.cur, qq)[t]);
+        const int off = F.rowoff(t, F.ia(F.cur, t, qq));
         if (t < P.lay.a_gfrom)
-            leaf_phase_a(F, o, kind, RowSrc<T>{F.a_sm(t) + off, P.ppw}, q, active, G, sub, j8);
+            leaf_phase_a(F, o, kind, RowSrc<T, PPW>{F.a_sm(t) + off}, q, active, G, sub);
         else
-            leaf_phase_a(F, o, kind, RowSrc<T>{F.a_gl(t) + off, P.ppw}, q, active, G, sub, j8);
+            leaf_phase_a(F, o, kind, RowSrc<T, PPW>{F.a_gl(t) + off}, q, active, G, sub);
     }
 }
 
-template <typename T, int W>
-__device__ __forceinline__ void leaf_op(Dec<T, W> &F, const DOp &o) {
+template <typename T, int W, int PPW>
+__device__ __forceinline__ void leaf_op(Dec<T, W, PPW> &F, const DOp &o) {
     const Params &P = F.P;
-    const int np = o.pin;
     int kind = o.kind;
     if (kind == DK_R1 && o.stage == 0) kind = DK_REP;  // listdec.py:347
 
     // Phase A: per-source sums / scans, this warp's sources
-    if (kind == DK_R0 || kind == DK_REP) {
-        // 8 lanes per path, 4 paths per pass
-        int act = np - F.warp * P.ppw;
-        act = act < 0 ? 0 : (act > P.ppw ? P.ppw : act);
-        const int g8 = F.lane >> 3, j8 = F.lane & 7;
-        for (int base = 0; base < act; base += 4) {
-            const int ql = base + g8;
-            leaf_read(F, o, kind, F.warp * P.ppw + ql, ql < act, 32, 0, j8);
-        }
-    } else {
-        const auto mp = F.map(np);
-        leaf_read(F, o, kind, mp.q, mp.active, mp.G, mp.sub, 0);
+    {
+        const auto mp = F.map(o.pin);
+        leaf_read(F, o, kind, mp.q, mp.active, mp.G, mp.sub);
     }
     F.sync();
 
@@ -709,7 +825,6 @@ __device__ __forceinline__ void leaf_op(Dec<T, W> &F, const DOp &o) {
         p = F.asg(b)[2 * k];
         c = F.asg(b)[2 * k + 1];
     }
-    const uint8_t *ibsrc = F.ib(F.cur, mp.active ? p : 0);
     if (fork && mp.active && mp.sub == 0) {
         uint32_t sy = F.syn(F.cur)[p];
         if (kind == DK_REP) {
@@ -718,26 +833,21 @@ __device__ __forceinline__ void leaf_op(Dec<T, W> &F, const DOp &o) {
         } else {
             sy ^= F.chs(b)[p];
             const int fm = flip_mask(kind, c, F.cflag(b)[p]);
-            const uint16_t *lrb = F.clrb(b, p);
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj)
-                if ((fm >> jj) & 1) sy ^= __ldg(P.msyn + o.off + lrb[jj]);
+                if ((fm >> jj) & 1) sy ^= __ldg(P.msyn + o.off + F.clrb(b, jj, p));
         }
         F.syn(nxt)[k] = sy;
-        F.pm(nxt)[k] = F.pm(F.cur)[p] + F.cd(b, p)[c];  // listdec.py:415
-        const uint4 *sa = reinterpret_cast<const uint4 *>(F.ia(F.cur, p));
-        const uint4 *sb = reinterpret_cast<const uint4 *>(F.ib(F.cur, p));
-        uint4 *da = reinterpret_cast<uint4 *>(F.ia(nxt, k));
-        uint4 *db = reinterpret_cast<uint4 *>(F.ib(nxt, k));
-        for (int x = 0; x < (P.lay.idx_stride >> 4); ++x) {
-            da[x] = sa[x];
-            db[x] = sb[x];
+        F.pm(nxt)[k] = F.pm(F.cur)[p] + F.cd(b, c, p);  // listdec.py:415
+        for (int x = 0; x < P.n; ++x) {  // lazy copy: inherit the source's rows
+            F.ia(nxt, x, k) = F.ia(F.cur, x, p);
+            F.ib(nxt, x, k) = F.ib(F.cur, x, p);
         }
     }
     const int sE = o.target;
     if (sE < P.n) {
-        word_and_chain(F, b, o, kind, mp.active, mp.G, mp.sub, p, c, ibsrc, F.beta_row(sE, k), sE);
-        if (mp.active && mp.sub == 0) F.ib(nxt, k)[sE] = (uint8_t)k;
+        word_and_chain(F, b, o, kind, mp.active, mp.G, mp.sub, p, c, F.cur, mp.active ? p : 0, F.beta_row(sE, k), sE);
+        if (mp.active && mp.sub == 0) F.ib(nxt, sE, k) = (uint8_t)k;
     }
     __syncwarp();
     F.cur = nxt;
@@ -768,8 +878,8 @@ __device__ __forceinline__ void polar_transform_words(uint32_t *x, int N, int la
     }
 }
 
-template <typename T, int W>
-__device__ __forceinline__ void build_root(const Dec<T, W> &F, const DOp &fo, int k, uint32_t *dst) {
+template <typename T, int W, int PPW>
+__device__ __forceinline__ void build_root(const Dec<T, W, PPW> &F, const DOp &fo, int k, uint32_t *dst) {
     int kind = fo.kind;
     if (kind == DK_R1 && fo.stage == 0) kind = DK_REP;
     int p = k, c = 0;
@@ -780,11 +890,12 @@ __device__ __forceinline__ void build_root(const Dec<T, W> &F, const DOp &fo, in
     }
     if (F.P.N < 32 && F.lane == 0) dst[0] = 0u;
     __syncwarp();
-    word_and_chain(F, b, fo, kind, true, 32, F.lane, p, c, F.ib(F.cur, k), dst, F.P.n);
+    word_and_chain(F, b, fo, kind, true, 32, F.lane, p, c, F.cur, k, dst, F.P.n);
+    __syncwarp();
 }
 
-template <typename T, int W>
-__device__ __forceinline__ void finalize(Dec<T, W> &F, long long f, int np) {
+template <typename T, int W, int PPW>
+__device__ __forceinline__ void finalize(Dec<T, W, PPW> &F, long long f, int np) {
     const Params &P = F.P;
     const int lane = F.lane;
     const DOp fo = P.prog[P.final_op];
@@ -841,8 +952,8 @@ __device__ __forceinline__ float ingest(float a) {
     return fminf(fmaxf(a, -1048576.f), 1048576.f);                             // clamp_llr (kernels.py:34-36)
 }
 
-template <typename T, int W>
-__device__ __forceinline__ void load_channel(const Dec<T, W> &F, long long f) {
+template <typename T, int W, int PPW>
+__device__ __forceinline__ void load_channel(const Dec<T, W, PPW> &F, long long f) {
     const Params &P = F.P;
     T *ch = F.channel();
     const int N = P.N, tid = threadIdx.x;
@@ -866,11 +977,11 @@ __device__ __forceinline__ void load_channel(const Dec<T, W> &F, long long f) {
     }
 }
 
-template <typename T, int W>
+template <typename T, int W, int PPW>
 __global__ void __launch_bounds__(32 * W, 1) k_decode(const __grid_constant__ Params P) {
     unsigned char *gs = P.gscratch ? P.gscratch + (size_t)blockIdx.x * P.lay.gbytes : nullptr;
     for (long long f = blockIdx.x; f < P.batch; f += gridDim.x) {
-        Dec<T, W> F(P, gs);
+        Dec<T, W, PPW> F(P, gs);
         load_channel(F, f);
         if (threadIdx.x == 0) {
             F.pm(0)[0] = 0.0;
@@ -882,10 +993,10 @@ __global__ void __launch_bounds__(32 * W, 1) k_decode(const __grid_constant__ Pa
             const DOp o = P.prog[oi];
             switch (o.kind) {
                 case DK_F:
-                    fg_op<T, W, false>(F, o);
+                    fg_op<T, W, PPW, false>(F, o);
                     break;
                 case DK_G:
-                    fg_op<T, W, true>(F, o);
+                    fg_op<T, W, PPW, true>(F, o);
                     break;
                 case DK_NOP:
                     break;
@@ -902,42 +1013,19 @@ __global__ void __launch_bounds__(32 * W, 1) k_decode(const __grid_constant__ Pa
     }
 }
 
-template <typename T, int W>
+template <typename T, int W, int PPW>
 cudaError_t launch_t(const Params *p, int grid, size_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_decode<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_decode<T, W, PPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_decode<T, W><<<grid, 32 * W, smem, st>>>(*p);
+    k_decode<T, W, PPW><<<grid, 32 * W, smem, st>>>(*p);
     return cudaGetLastError();
 }
-template <typename T, int W>
+template <typename T, int W, int PPW>
 cudaError_t occ_t(size_t smem, int *bps) {
-    cudaError_t e = cudaFuncSetAttribute(k_decode<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_decode<T, W, PPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_decode<T, W>, 32 * W, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_decode<T, W, PPW>, 32 * W, smem);
 }
 
 }  // namespace pb
 
-#define PB_DISPATCH_W(FN, T, ...)                         \
-    switch (warps) {                                      \
-        case 1: return pb::FN<T, 1>(__VA_ARGS__);         \
-        case 2: return pb::FN<T, 2>(__VA_ARGS__);         \
-        case 4: return pb::FN<T, 4>(__VA_ARGS__);         \
-        case 8: return pb::FN<T, 8>(__VA_ARGS__);         \
-        default: return cudaErrorInvalidValue;            \
-    }
-
-extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps, int grid, size_t smem,
-                                        cudaStream_t stream) {
-    if (mode == 0) {
-        PB_DISPATCH_W(launch_t, float, p, grid, smem, stream)
-    }
-    PB_DISPATCH_W(launch_t, int8_t, p, grid, smem, stream)
-}
-
-extern "C" cudaError_t pb_occupancy(int mode, int warps, size_t smem, int *blocks_per_sm) {
-    if (mode == 0) {
-        PB_DISPATCH_W(occ_t, float, smem, blocks_per_sm)
-    }
-    PB_DISPATCH_W(occ_t, int8_t, smem, blocks_per_sm)
-}

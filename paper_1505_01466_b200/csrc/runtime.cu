@@ -22,9 +22,10 @@
 #include "../../include/polar_b200.h"
 #include "decoder.cuh"
 
-extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps, int grid, size_t smem,
+extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps, int ppw, int grid, size_t smem,
                                         cudaStream_t stream);
-extern "C" cudaError_t pb_occupancy(int mode, int warps, size_t smem, int *blocks_per_sm);
+extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, size_t smem, int *blocks_per_sm);
+extern "C" int pb_shape_supported(int mode, int warps, int ppw);
 
 namespace {
 
@@ -85,7 +86,7 @@ struct pb_handle {
     std::vector<pb::DOp> prog;
     pb::DOp *d_prog = nullptr;
     uint32_t *d_msyn = nullptr, *d_info = nullptr;
-    int grid = 0, blocks_per_sm = 0, sms = 0, warps = 1;
+    int grid = 0, blocks_per_sm = 0, sms = 0, warps = 1, ppw = 1;
     size_t smem_frame = 0;
     unsigned char *d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -309,15 +310,18 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
 
     // ---- storage plan
     const int es = mode == PB_MODE_F32 ? 4 : 1;
-    int warps = env_int("PB_WARPS", L >= 16 ? 4 : (L >= 8 ? 2 : 1));
-    if (warps != 1 && warps != 2 && warps != 4 && warps != 8) warps = 1;
-    while (warps > 1 && warps > L) warps >>= 1;
-    int ppw = 1, lppw = 0;
-    while (ppw * warps < L) {
-        ppw <<= 1;
-        ++lppw;
-    }
+    // frame shape: W warps per frame, PPW (power of two) path slots per warp
+    int warps = env_int("PB_WARPS", 1);
+    auto shape_ppw = [&](int wv) {
+        int p = 1;
+        while (p * wv < L) p <<= 1;
+        return p;
+    };
+    if (!pb_shape_supported(mode, warps, shape_ppw(warps))) warps = 1;
+    int ppw = shape_ppw(warps), lppw = 0;
+    while ((1 << lppw) < ppw) ++lppw;
     const int rows = ppw * warps;  // alpha rows, padded to whole interleave blocks
+    h->ppw = ppw;
     h->warps = warps;
     pb::FrameLayout &lay = h->base.lay;
     int off = 0;
@@ -333,24 +337,25 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     off = align_up(off + 2 * L * 8, 16);
     lay.syn_off = off;
     off = align_up(off + 2 * L * 4, 16);
-    lay.idx_stride = n <= 16 ? 16 : 32;
+    lay.idx_stride = std::max(n, 1);  // entries per path ([buf][entry][path] layout)
     lay.ia_off = off;
     off = align_up(off + 2 * L * lay.idx_stride, 16);
     lay.ib_off = off;
     off = align_up(off + 2 * L * lay.idx_stride, 16);
+    const int nbuf = warps > 1 ? 2 : 1;  // candidate buffers (by leaf parity across warps)
     lay.cd_off = off;
-    off = align_up(off + 2 * L * pb::kMaxCand * 8, 16);
+    off = align_up(off + nbuf * L * pb::kMaxCand * 8, 16);
     lay.clrb_off = off;
-    off = align_up(off + 2 * L * 4 * 2, 16);
+    off = align_up(off + nbuf * L * 4 * 2, 16);
     lay.chs_off = off;
-    off = align_up(off + 2 * L * 4, 16);
+    off = align_up(off + nbuf * L * 4, 16);
     lay.cflag_off = off;
-    off = align_up(off + 2 * L, 16);
+    off = align_up(off + nbuf * L, 16);
     lay.asg_off = off;
-    off = align_up(off + 2 * 2 * L, 16);
+    off = align_up(off + nbuf * 2 * L, 16);
     lay.hard_words = std::max(1, max_hard / 32);
     lay.hard_off = off;
-    off = align_up(off + 2 * L * lay.hard_words * 4, 16);
+    off = align_up(off + nbuf * L * lay.hard_words * 4, 16);
     lay.root_words = std::max(1, N / 32);
     lay.root_off = off;
     off = align_up(off + lay.root_words * 4, 16);
@@ -391,7 +396,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         return cuda_fail(e, "cudaSetDevice");
     }
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
-    e = pb_occupancy(mode, h->warps, h->smem_frame, &h->blocks_per_sm);
+    e = pb_occupancy(mode, h->warps, h->ppw, h->smem_frame, &h->blocks_per_sm);
     if (e != cudaSuccess || h->blocks_per_sm < 1) {
         delete h;
         return cuda_fail(e == cudaSuccess ? cudaErrorInvalidConfiguration : e, "occupancy");
@@ -439,10 +444,11 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     snprintf(buf, sizeof buf,
              "{\"N\": %d, \"k\": %d, \"L\": %d, \"mode\": \"%s\", \"ops\": %d, \"device_ops\": %d, "
              "\"smem_per_frame\": %d, \"alpha_global_from_stage\": %d, \"global_scratch_per_frame\": %d, "
-             "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": %d, \"warps_per_frame\": %d}",
+             "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": %d, \"warps_per_frame\": %d, "
+             "\"paths_per_warp\": %d}",
              N, code->k, L, mode == PB_MODE_F32 ? "f32" : "int8", n_ops, (int)h->prog.size(),
              lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm, h->sms, h->grid, 32 * h->warps,
-             h->warps);
+             h->warps, h->ppw);
     h->plan_json = buf;
     *out = h;
     return PB_OK;
@@ -494,7 +500,7 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
     int grid = (int)std::min<long long>(h->grid, pr.batch);
     if (grid < 1) return PB_OK;
     PB_CUDA(cudaEventRecord(h->ev0, st));
-    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, grid, h->smem_frame, st);
+    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, grid, h->smem_frame, st);
     if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
     PB_CUDA(cudaEventRecord(h->ev1, st));
     h->timed = true;
