@@ -146,12 +146,19 @@ struct Dec {
     __device__ __forceinline__ uint32_t *syn(int b) const {
         return reinterpret_cast<uint32_t *>(g_smem + P.lay.syn_off) + b * P.L;
     }
-    // alpha / beta row index of path q at stage / slot s: [buf][s][path]
+    // alpha / beta row index of path q at stage / slot s, four stages per
+    // word: byte (s & 3) of word [buf][s >> 2][path]
     __device__ __forceinline__ uint8_t &ia(int b, int s, int q) const {
-        return g_smem[P.lay.ia_off + (b * P.lay.idx_stride + s) * P.L + q];
+        return g_smem[P.lay.ia_off + ((b * P.lay.idx_stride + (s >> 2)) * P.L + q) * 4 + (s & 3)];
     }
     __device__ __forceinline__ uint8_t &ib(int b, int s, int q) const {
-        return g_smem[P.lay.ib_off + (b * P.lay.idx_stride + s) * P.L + q];
+        return g_smem[P.lay.ib_off + ((b * P.lay.idx_stride + (s >> 2)) * P.L + q) * 4 + (s & 3)];
+    }
+    __device__ __forceinline__ uint32_t &iaw(int b, int x, int q) const {
+        return reinterpret_cast<uint32_t *>(g_smem + P.lay.ia_off)[(b * P.lay.idx_stride + x) * P.L + q];
+    }
+    __device__ __forceinline__ uint32_t &ibw(int b, int x, int q) const {
+        return reinterpret_cast<uint32_t *>(g_smem + P.lay.ib_off)[(b * P.lay.idx_stride + x) * P.L + q];
     }
     __device__ __forceinline__ int bsel(int b) const { return NBUF > 1 ? b : 0; }
     // candidate data: [buf][entry][source path]
@@ -496,9 +503,30 @@ __device__ __forceinline__ int flip_mask(int kind, int c, int odd) {
     return c == 0 ? ml : (kSpcPairs[c - 1] ^ ml);
 }
 
+// warp-wide max / min of an int64 key via two REDUX steps on its halves
+__device__ __forceinline__ long long warp_max_ll(long long v) {
+    const int hi = (int)(v >> 32);
+    const int mh = __reduce_max_sync(FULL_MASK, hi);
+    const unsigned ml = __reduce_max_sync(FULL_MASK, hi == mh ? (unsigned)v : 0u);
+    return ((long long)mh << 32) | ml;
+}
+__device__ __forceinline__ long long warp_min_ll(long long v) {
+    const int hi = (int)(v >> 32);
+    const int mh = __reduce_min_sync(FULL_MASK, hi);
+    const unsigned ml = __reduce_min_sync(FULL_MASK, hi == mh ? (unsigned)v : 0xffffffffu);
+    return ((long long)mh << 32) | ml;
+}
+
 // Phase B (warp 0, lane = source): survivors -> asg[k] = (source, cand) in
 // (source, cand) order.  The L best by (metric desc, source asc, cand asc)
 // == listdec.py:63-100 (bounded heap == full sort, tests/oracles.py:74-89).
+//
+// The L-th best key Tk comes from a k-way merge: slot r of the kept set
+// lives in lane r (lanes < L), each source lane exposes its best unconsumed
+// candidate (candidates sorted best-first per lane); while the best exposed
+// candidate beats the worst kept key it replaces it (REDUX max / min).  Then
+// every key > Tk survives, plus the earliest ties == Tk in (source, cand)
+// order until L are kept.
 template <typename T, int W, int PPW>
 __device__ __forceinline__ void select_phase(const Dec<T, W, PPW> &F, const DOp &o) {
     const int lane = F.lane, np = o.pin, C = o.ncand, L = F.P.L;
@@ -517,33 +545,36 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW> &F, const DOp 
         // best-first column per lane (Rate-1 columns already are:
         // 0 >= -m1 >= -m2 >= -(m1+m2), monotone under rounding)
         if (C == 2) {
-            const long long a = srt[0], b = srt[1];
-            srt[0] = a > b ? a : b;
-            srt[1] = a > b ? b : a;
+            const long long x = srt[0], y = srt[1];
+            srt[0] = x > y ? x : y;
+            srt[1] = x > y ? y : x;
         } else if (C == 8) {
 #pragma unroll
             for (int pass = 0; pass < 8; ++pass)
 #pragma unroll
                 for (int c = pass & 1; c + 1 < 8; c += 2) {
-                    const long long a = srt[c], b = srt[c + 1];
-                    srt[c] = a > b ? a : b;
-                    srt[c + 1] = a > b ? b : a;
+                    const long long x = srt[c], y = srt[c + 1];
+                    srt[c] = x > y ? x : y;
+                    srt[c + 1] = x > y ? y : x;
                 }
         }
-        const int Wd = 1 << log2ceil(L);
-        long long R = srt[0];
-        bitonic_sort(R, Wd, true, lane);
-        long long Tk = shfl_ll(R, L - 1);
+        // kept set: slot = lane (< L); start from every source's best
+        long long kept = lane < L ? srt[0] : LLONG_MAX;
+        int ptr = 1;
+        for (;;) {
+            long long cand = LLONG_MIN;
 #pragma unroll
-        for (int j = 1; j < kMaxCand; ++j) {
-            if (j >= C) break;
-            long long x = srt[j];
-            if (!__any_sync(FULL_MASK, x > Tk)) break;
-            bitonic_sort(x, Wd, false, lane);
-            R = R > x ? R : x;
-            bitonic_merge_desc(R, Wd, lane);
-            Tk = shfl_ll(R, L - 1);
+            for (int c = 1; c < kMaxCand; ++c)
+                if (c == ptr && c < C) cand = srt[c];
+            const long long best = warp_max_ll(cand);
+            const long long worst = warp_min_ll(kept);
+            if (best <= worst) break;
+            const int from = __ffs(__ballot_sync(FULL_MASK, cand == best)) - 1;
+            const int into = __ffs(__ballot_sync(FULL_MASK, kept == worst)) - 1;
+            if (lane == from) ++ptr;
+            if (lane == into) kept = best;
         }
+        const long long Tk = warp_min_ll(kept);
         // Tk = the L-th best key; keep all better, then the earliest ties
         int gt = 0, eq = 0;
 #pragma unroll
@@ -666,7 +697,22 @@ __device__ __forceinline__ void leaf_sums(Dec<T, W, PPW> &F, const DOp &o, int k
     }
 }
 
-// Gl (<= G) lanes of the path's group scan; the rest idle
+// CRC syndrome contribution of a hard-decision word whose bit j sits at u
+// index pos + j (j < cnt; pos + cnt stays inside one aligned 32-block):
+// XOR of the leaf-local syndrome rows of its set bits, by nibble tables.
+__device__ __forceinline__ uint32_t syn_word(const uint32_t *T4, uint32_t word, int pos, int cnt) {
+    const int sh = pos & 31;
+    const uint32_t x = word << sh;
+    const uint32_t *t = T4 + ((pos & ~31) >> 2) * 16;
+    uint32_t s = 0u;
+    const int n1 = (sh + cnt + 3) >> 2;
+    for (int nb = sh >> 2; nb < n1; ++nb) s ^= __ldg(t + nb * 16 + ((x >> (4 * nb)) & 15u));
+    return s;
+}
+
+// Rate-1 / SPC scan: stable K least reliable positions, hard decisions,
+// parity and syndrome of the hard word.  Gl (<= G) lanes of the path's group
+// scan (one lane unless the node is large); the rest idle.
 template <typename T, int W, int PPW, int K, class S>
 __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW> &F, const DOp &o, int kind, const S &src, int q,
                                           bool active, int G, int sub) {
@@ -674,48 +720,63 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW> &F, const DOp &o, int k
     const int m = 1 << o.stage;
     int Gl = m >> 4;
     Gl = Gl < 1 ? 1 : (Gl > G ? G : Gl);
-    const int lgl = 31 - __clz(Gl);
-    const bool scan = active && sub < Gl;
     TopK<K> tk;
     tk.init();
-    uint32_t hs = 0u, hword = 0u;
+    uint32_t hs = 0u;
     int par = 0;
-    const int iters = (m + Gl - 1) >> lgl;
-    const int hq = active ? q : F.warp * PPW;
-    const uint32_t *msyn = P.msyn + o.off;
-    const int gshift = F.lane - sub;  // group leader lane
-    const uint32_t gmask = Gl == 32 ? 0xffffffffu : ((1u << Gl) - 1u);
-    for (int it = 0; it < iters; ++it) {
-        const int i = (it << lgl) + sub;
-        const bool valid = scan && i < m;
-        const float a = valid ? src.get(i) : 0.f;
-        const bool neg = valid && a < 0.f;
-        if (valid) tk.push_scan(fabsf(a), i);
-        if (neg) hs ^= __ldg(msyn + i);
-        uint32_t gb;
-        if (Gl == 1)
-            gb = neg;
-        else
-            gb = (__ballot_sync(FULL_MASK, neg) >> gshift) & gmask;
-        const int base = it << lgl;
-        hword |= gb << (base & 31);
-        if (((base + Gl) & 31) == 0 || it == iters - 1) {
-            if (scan && sub == 0) F.hard(F.par, base >> 5, hq) = hword;
-            par ^= __popc(hword);
-            hword = 0u;
+    if (Gl == 1) {
+        if (active && sub == 0) {
+            for (int w0 = 0; w0 < m; w0 += 32) {
+                const int cnt = m - w0 < 32 ? m - w0 : 32;
+                uint32_t word = 0u;
+#pragma unroll 4
+                for (int j = 0; j < cnt; ++j) {
+                    const float a = src.get(w0 + j);
+                    word |= (a < 0.f ? 1u : 0u) << j;
+                    tk.push_scan(fabsf(a), w0 + j);
+                }
+                F.hard(F.par, w0 >> 5, q) = word;
+                par ^= __popc(word);
+                hs ^= syn_word(P.msyn4, word, o.off + w0, cnt);
+            }
         }
-    }
-    for (int d = 1; d < Gl; d <<= 1) {
-        hs ^= __shfl_xor_sync(FULL_MASK, hs, d);
-        float om[K];
-        int oi[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            om[k] = __shfl_xor_sync(FULL_MASK, tk.m[k], d);
-            oi[k] = __shfl_xor_sync(FULL_MASK, tk.i[k], d);
+    } else {
+        const int lgl = 31 - __clz(Gl);
+        const bool scan = active && sub < Gl;
+        uint32_t hword = 0u;
+        const int iters = (m + Gl - 1) >> lgl;
+        const int hq = active ? q : F.warp * PPW;
+        const int gshift = F.lane - sub;  // group leader lane
+        const uint32_t gmask = Gl == 32 ? 0xffffffffu : ((1u << Gl) - 1u);
+        for (int it = 0; it < iters; ++it) {
+            const int i = (it << lgl) + sub;
+            const bool valid = scan && i < m;
+            const float a = valid ? src.get(i) : 0.f;
+            const bool neg = valid && a < 0.f;
+            if (valid) tk.push_scan(fabsf(a), i);
+            const uint32_t gb = (__ballot_sync(FULL_MASK, neg) >> gshift) & gmask;
+            const int base = it << lgl;
+            hword |= gb << (base & 31);
+            if (((base + Gl) & 31) == 0 || it == iters - 1) {
+                if (scan && sub == 0) {
+                    F.hard(F.par, base >> 5, hq) = hword;
+                    hs ^= syn_word(P.msyn4, hword, o.off + ((base >> 5) << 5), m < 32 ? m : 32);
+                }
+                par ^= __popc(hword);
+                hword = 0u;
+            }
         }
+        for (int d = 1; d < Gl; d <<= 1) {
+            float om[K];
+            int oi[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) tk.insert(om[k], oi[k]);
+            for (int k = 0; k < K; ++k) {
+                om[k] = __shfl_xor_sync(FULL_MASK, tk.m[k], d);
+                oi[k] = __shfl_xor_sync(FULL_MASK, tk.i[k], d);
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) tk.insert(om[k], oi[k]);
+        }
     }
     if (!(active && sub == 0)) return;
 #pragma unroll
@@ -839,9 +900,9 @@ __device__ __forceinline__ void leaf_op(Dec<T, W, PPW> &F, const DOp &o) {
         }
         F.syn(nxt)[k] = sy;
         F.pm(nxt)[k] = F.pm(F.cur)[p] + F.cd(b, c, p);  // listdec.py:415
-        for (int x = 0; x < P.n; ++x) {  // lazy copy: inherit the source's rows
-            F.ia(nxt, x, k) = F.ia(F.cur, x, p);
-            F.ib(nxt, x, k) = F.ib(F.cur, x, p);
+        for (int x = 0; x < P.lay.idx_stride; ++x) {  // lazy copy: inherit the source's rows
+            F.iaw(nxt, x, k) = F.iaw(F.cur, x, p);
+            F.ibw(nxt, x, k) = F.ibw(F.cur, x, p);
         }
     }
     const int sE = o.target;

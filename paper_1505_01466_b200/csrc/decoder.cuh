@@ -43,9 +43,9 @@ struct FrameLayout {
     int b_stride[kMaxLog];      // row stride, words
     int pm_off;                 // double [2][L]    path metrics (double-buffered)
     int syn_off;                // uint32 [2][L]    CRC syndromes
-    int ia_off;                 // uint8 [2][L][idx_stride]  alpha row per stage
-    int ib_off;                 // uint8 [2][L][idx_stride]  beta row per slot
-    int idx_stride;
+    int ia_off;                 // uint32 [2][idx_stride][L] alpha row per stage, 4 per word
+    int ib_off;                 // uint32 [2][idx_stride][L] beta row per slot, 4 per word
+    int idx_stride;             // words per path = ceil(n / 4)
     int cd_off;                 // double [2][L][8] candidate deltas (by leaf parity)
     int clrb_off;               // uint16 [2][L][4] least reliable positions
     int chs_off;                // uint32 [2][L] hard-word syndrome
@@ -63,6 +63,7 @@ struct Params {
     const DOp *prog;
     int n_ops;
     const uint32_t *msyn;       // [N] leaf-local CRC syndrome rows
+    const uint32_t *msyn4;      // [N/4][16] nibble tables of msyn (XOR of a nibble's rows)
     const uint32_t *info_pos;   // [k] payload positions (u index)
     int N, n, k, L;
     int ppw;                    // paths per warp (rows per interleave block), power of two

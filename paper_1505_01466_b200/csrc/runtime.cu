@@ -85,7 +85,7 @@ struct pb_handle {
     pb::Params base{};
     std::vector<pb::DOp> prog;
     pb::DOp *d_prog = nullptr;
-    uint32_t *d_msyn = nullptr, *d_info = nullptr;
+    uint32_t *d_msyn = nullptr, *d_msyn4 = nullptr, *d_info = nullptr;
     int grid = 0, blocks_per_sm = 0, sms = 0, warps = 1, ppw = 1;
     size_t smem_frame = 0;
     unsigned char *d_scratch = nullptr;
@@ -337,11 +337,11 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     off = align_up(off + 2 * L * 8, 16);
     lay.syn_off = off;
     off = align_up(off + 2 * L * 4, 16);
-    lay.idx_stride = std::max(n, 1);  // entries per path ([buf][entry][path] layout)
+    lay.idx_stride = std::max(1, (n + 3) / 4);  // index words per path (4 stages per word)
     lay.ia_off = off;
-    off = align_up(off + 2 * L * lay.idx_stride, 16);
+    off = align_up(off + 2 * L * lay.idx_stride * 4, 16);
     lay.ib_off = off;
-    off = align_up(off + 2 * L * lay.idx_stride, 16);
+    off = align_up(off + 2 * L * lay.idx_stride * 4, 16);
     const int nbuf = warps > 1 ? 2 : 1;  // candidate buffers (by leaf parity across warps)
     lay.cd_off = off;
     off = align_up(off + nbuf * L * pb::kMaxCand * 8, 16);
@@ -406,6 +406,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     // ---- device tables
     if ((e = cudaMalloc(&h->d_prog, sizeof(pb::DOp) * h->prog.size())) != cudaSuccess ||
         (e = cudaMalloc(&h->d_msyn, sizeof(uint32_t) * N)) != cudaSuccess ||
+        (e = cudaMalloc(&h->d_msyn4, sizeof(uint32_t) * 16 * std::max(1, N / 4))) != cudaSuccess ||
         (e = cudaMalloc(&h->d_info, sizeof(uint32_t) * std::max(1, code->k))) != cudaSuccess) {
         pb_destroy(h);
         return cuda_fail(e, "cudaMalloc tables");
@@ -413,6 +414,16 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     std::vector<uint32_t> info_k(info.begin(), info.begin() + code->k);
     cudaMemcpy(h->d_prog, h->prog.data(), sizeof(pb::DOp) * h->prog.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(h->d_msyn, M.data(), sizeof(uint32_t) * N, cudaMemcpyHostToDevice);
+    {
+        // nibble tables: T4[nb][v] = XOR of M[4 nb + j] over the set bits j of v
+        const int nnib = std::max(1, N / 4);
+        std::vector<uint32_t> T4((size_t)nnib * 16, 0u);
+        for (int nb = 0; nb < nnib; ++nb)
+            for (int v = 0; v < 16; ++v)
+                for (int j = 0; j < 4; ++j)
+                    if (((v >> j) & 1) && 4 * nb + j < N) T4[(size_t)nb * 16 + v] ^= M[4 * nb + j];
+        cudaMemcpy(h->d_msyn4, T4.data(), sizeof(uint32_t) * T4.size(), cudaMemcpyHostToDevice);
+    }
     cudaMemcpy(h->d_info, info_k.data(), sizeof(uint32_t) * code->k, cudaMemcpyHostToDevice);
     if (lay.gbytes) {
         h->scratch_bytes = (size_t)h->grid * lay.gbytes;
@@ -428,6 +439,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     pr.prog = h->d_prog;
     pr.n_ops = (int)h->prog.size();
     pr.msyn = h->d_msyn;
+    pr.msyn4 = h->d_msyn4;
     pr.info_pos = h->d_info;
     pr.N = N;
     pr.n = n;
@@ -458,6 +470,7 @@ int pb_destroy(pb_handle *h) {
     if (!h) return PB_OK;
     cudaFree(h->d_prog);
     cudaFree(h->d_msyn);
+    cudaFree(h->d_msyn4);
     cudaFree(h->d_info);
     cudaFree(h->d_scratch);
     cudaFree(h->d_in);
