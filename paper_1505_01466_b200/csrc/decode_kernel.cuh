@@ -128,9 +128,13 @@ struct Dec {
     int cur;            // live half of the double-buffered path state
     int par;            // candidate-buffer parity (toggles at forking leaves)
     int lpar;           // parity used by the last forking leaf
+    long long *ph;      // debug: phase timestamps of the current op (or null)
 
     __device__ Dec(const Params &p, unsigned char *g)
-        : P(p), gs(g), lane(threadIdx.x & 31), warp(threadIdx.x >> 5), cur(0), par(0), lpar(0) {}
+        : P(p), gs(g), lane(threadIdx.x & 31), warp(threadIdx.x >> 5), cur(0), par(0), lpar(0), ph(nullptr) {}
+    __device__ __forceinline__ void mark(int i) const {
+        if (ph) ph[i] = clock64();
+    }
 
     // row r, element 0 of a block-interleaved stage s
     __device__ __forceinline__ int rowoff(int s, int r) const { return ((r >> LP) << (LP + s)) + (r & (PPW - 1)); }
@@ -869,12 +873,14 @@ __device__ __forceinline__ void leaf_op(Dec<T, W, PPW> &F, const DOp &o) {
         leaf_read(F, o, kind, mp.q, mp.active, mp.G, mp.sub);
     }
     F.sync();
+    F.mark(0);
 
     const bool fork = kind != DK_R0;
     if (fork) {
         if (F.warp == 0) select_phase(F, o);
         F.sync();
     }
+    F.mark(1);
 
     // Phase C: materialise survivors k < pout (this warp's)
     const auto mp = F.map(o.pout);
@@ -1050,7 +1056,11 @@ __global__ void __launch_bounds__(32 * W, 1) k_decode(const __grid_constant__ Pa
         }
         F.sync();
         int np = 1;
+        const bool prof = P.op_cycles && blockIdx.x == 0 && f == 0 && threadIdx.x == 0;
+        long long phbuf[2] = {0, 0};
+        if (prof) F.ph = phbuf;
         for (int oi = 0; oi < P.n_ops; ++oi) {
+            const long long t0 = prof ? clock64() : 0;
             const DOp o = P.prog[oi];
             switch (o.kind) {
                 case DK_F:
@@ -1067,6 +1077,15 @@ __global__ void __launch_bounds__(32 * W, 1) k_decode(const __grid_constant__ Pa
                     break;
             }
             __syncwarp();
+            if (prof) {
+            const long long t1 = clock64();
+            P.op_cycles[oi * 4] = t1 - t0;
+            if (F.ph) {
+                P.op_cycles[oi * 4 + 1] = F.ph[0] - t0;
+                P.op_cycles[oi * 4 + 2] = F.ph[1] - F.ph[0];
+                P.op_cycles[oi * 4 + 3] = t1 - F.ph[1];
+            }
+        }
         }
         F.sync();
         if (F.warp == 0) finalize(F, f, np);

@@ -82,6 +82,7 @@ struct Params {
     double *path_pm;            // [B][L]
     uint8_t *path_crc;          // [B][L]
     unsigned char *gscratch;    // [CTA slots][gbytes]
+    long long *op_cycles;       // debug: per-op clock64 deltas of CTA 0's first frame, or null
     FrameLayout lay;
 };
 

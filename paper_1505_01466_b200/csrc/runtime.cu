@@ -361,7 +361,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     off = align_up(off + lay.root_words * 4, 16);
 
     const int smem_cap = 227 * 1024;
-    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", mode == PB_MODE_F32 ? 2 : 4));
+    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", mode == PB_MODE_F32 ? 3 : 4));
     const int budget = std::max(off, env_int("PB_SMEM_BUDGET", smem_cap / target_fps - 1024));
     // alpha stages s = 0 .. n-2 (n-1 is recomputed), lowest stages first into
     // shared memory, the rest into per-CTA global scratch (L2-resident)
@@ -451,6 +451,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     pr.crc_const = crc_const;
     pr.final_op = final_op;
     pr.gscratch = h->d_scratch;
+    pr.op_cycles = nullptr;
 
     char buf[1024];
     snprintf(buf, sizeof buf,
@@ -585,6 +586,43 @@ extern "C" int pb_decode(pb_handle *h, const void *llr, int in_type, int64_t bat
         PB_CUDA(cudaMemcpyAsync(paths_used, pr.paths_used, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
     PB_CUDA(cudaStreamSynchronize(st));
     PB_CUDA(cudaGetLastError());
+    return PB_OK;
+}
+
+// Debug: decode `batch` host frames and return the clock64 cycles each device
+// op took for CTA 0's first frame (out: [pb_device_op_count] int64), plus
+// the op kinds/stages (kinds/stages may be null).
+extern "C" int pb_device_op_count(pb_handle *h) { return h ? (int)h->prog.size() : 0; }
+extern "C" int pb_profile_ops(pb_handle *h, const void *llr, int in_type, int64_t batch, long long *cycles,
+                              int8_t *kinds, int8_t *stages) {
+    if (!h || !llr || !cycles) return fail(PB_EINVAL, "null argument");
+    PB_CUDA(cudaSetDevice(h->device));
+    const size_t in_bytes = (size_t)batch * h->N * (in_type == PB_IN_F32 ? 4 : 1);
+    int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
+    if (rc) return rc;
+    long long *d_cyc = nullptr;
+    PB_CUDA(cudaMalloc(&d_cyc, sizeof(long long) * 4 * h->prog.size()));
+    PB_CUDA(cudaMemset(d_cyc, 0, sizeof(long long) * 4 * h->prog.size()));
+    PB_CUDA(cudaMemcpy(h->d_in, llr, in_bytes, cudaMemcpyHostToDevice));
+    pb::Params pr = h->base;
+    pr.llr = h->d_in;
+    pr.in_type = in_type;
+    pr.batch = batch;
+    pr.info_out = nullptr;
+    pr.crc_ok = nullptr;
+    pr.pm_out = nullptr;
+    pr.paths_used = nullptr;
+    pr.path_cw = nullptr;
+    pr.op_cycles = d_cyc;
+    rc = launch(h, pr, 0);
+    if (rc) return rc;
+    PB_CUDA(cudaDeviceSynchronize());
+    PB_CUDA(cudaMemcpy(cycles, d_cyc, sizeof(long long) * 4 * h->prog.size(), cudaMemcpyDeviceToHost));
+    cudaFree(d_cyc);
+    for (size_t i = 0; i < h->prog.size(); ++i) {
+        if (kinds) kinds[i] = h->prog[i].kind;
+        if (stages) stages[i] = h->prog[i].stage;
+    }
     return PB_OK;
 }
 

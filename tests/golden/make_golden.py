@@ -129,6 +129,11 @@ def main():
         else:
             feed = llrs
         digest = hashlib.sha256(llrs.tobytes()).hexdigest()
+        # the reference's own construction outputs, to pin the host mirror
+        arrays[f"{case['name']}.mask"] = np.packbits(spec.frozen_mask)
+        case["schedule_text_sha256"] = hashlib.sha256(ref.emit_source(sch).encode()).hexdigest()
+        case["schedule_ops"] = [[op.kind.value, op.size, op.stage, op.side, int(op.spc_truncated)]
+                                for op in sch.ops] if len(sch.ops) <= 600 else None
 
         def run(clip: bool):
             orig = ref_ld.g_op
@@ -177,6 +182,34 @@ def main():
         case["frame_errors"] = int(np.sum(np.any(info != pays, axis=1)))
         manifest.append(case)
         print(f"{key}: {B} frames, frame errors {case['frame_errors']}", flush=True)
+
+    # known answers the reference's own tests pin (test_codes.py:78-89,
+    # test_encode.py:24-30, test_schedule.py:29-44, test_fastssc.py:12-34)
+    kats = {}
+    data = b"123456789"
+    msb = [(b >> i) & 1 for b in data for i in range(7, -1, -1)]
+    lsb = [(b >> i) & 1 for b in data for i in range(8)]
+    kats["crc"] = {"crc8_msb": ref.crc_compute(msb, ref.CRC8), "crc16_msb": ref.crc_compute(msb, ref.CRC16),
+                   "crc32_lsb": ref.crc_compute(lsb, ref.CRC32)}
+    kats["schedules"] = {f"{n},{k}": ref.emit_source(ref.build_schedule(ref.CodeSpec.construct(n, k, None)))
+                         for n, k in ((8, 4), (16, 8), (64, 30))}
+    kats["schedules_spc_none"] = {"16,8": ref.emit_source(
+        ref.build_schedule(ref.CodeSpec.construct(16, 8, None), ref.ScheduleConfig(spc_cap=None)))}
+    from polaris.fastssc import execute_schedule
+    sch84 = ref.build_schedule(ref.CodeSpec.construct(8, 4, None))
+    kats["fastssc_8_4"] = []
+    for llr in ([1, -2, 3, -4, 5, -6, 7, -8], [1, -2, 3, -4, -5, 6, 7, 8]):
+        w, pm = execute_schedule(np.array(llr, np.float32), sch84)
+        kats["fastssc_8_4"].append({"llr": llr, "codeword": w[0].tolist(), "pm": float(pm[0])})
+    pools = [[0.0, [0.0, -0.5, -1.0, -1.5]], [-1.0, [0.0, -1.0, -2.0, -3.0]]]
+    kats["select"] = [{"pools": pools, "L": 2, "out": ref_ld.select_candidates(pools, 2)},
+                      {"pools": [[0.0, [0.0, -1.0]], [-1.0, [0.0, -2.0]]], "L": 2,
+                       "out": ref_ld.select_candidates([(0.0, [0.0, -1.0]), (-1.0, [0.0, -2.0])], 2)},
+                      {"pools": [[0.0, [0.0, -1.0, -1.0]]], "L": 2,
+                       "out": ref_ld.select_candidates([(0.0, [0.0, -1.0, -1.0])], 2)}]
+    kats["select"] = [{**k, "out": [list(x) for x in k["out"]]} for k in kats["select"]]
+    with open(os.path.join(HERE, "reference_kats.json"), "w") as fh:
+        json.dump(kats, fh, indent=1)
 
     np.savez_compressed(os.path.join(HERE, "reference_decodes.npz"), **arrays)
     with open(os.path.join(HERE, "reference_cases.json"), "w") as fh:

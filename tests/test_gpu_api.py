@@ -1,0 +1,139 @@
+"""GPU decoder through its public API: host / pinned / device buffers, the
+single-frame calls, batch edge cases, error behaviour, int8 inputs."""
+
+import numpy as np
+import pytest
+
+import paper_1505_01466_b200 as pb
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c1():
+    spec = pb.CodeSpec.from_design_ebn0(1024, 504, pb.CrcConfig(width=8, polynomial=0xD5), 2.0)
+    sch = pb.build_schedule(spec)
+    fb = pb.generate_frames(spec, 2.0, seed=5, start=0, count=300, workers=1)
+    return spec, sch, fb
+
+
+def test_single_frame_calls_match_batch(c1):
+    spec, sch, fb = c1
+    dec = pb.ListDecoder(sch, 4)
+    batch = dec.decode_batch(fb.llrs[:20])
+    for f in range(20):
+        r = dec.decode(fb.llrs[f].astype(np.float64))   # float64 input -> host clamp path
+        assert np.array_equal(r.info_bits, batch.info_bits[f])
+        assert r.crc_ok == batch.crc_ok[f] and r.chosen_pm == batch.chosen_pm[f]
+        assert r.paths_used == batch.paths_used[f] and r.invoked_list
+        one = pb.decode(fb.llrs[f], sch, 4)
+        assert np.array_equal(one.info_bits, r.info_bits)
+    outs = dec.decode_paths(fb.llrs[3])
+    assert len(outs) == batch.paths_used[3]
+    best = [o for o in outs if o.crc_ok] or outs
+    assert max(o.pm for o in best) == batch.chosen_pm[3]
+    for o in outs:
+        assert np.array_equal(pb.polar_encode(o.u), o.codeword)
+
+
+def test_device_and_pinned_buffers(c1):
+    import torch
+    spec, sch, fb = c1
+    dec = pb.ListDecoder(sch, 4)
+    ref = dec.decode_batch(fb.llrs)
+    x = torch.from_numpy(fb.llrs).cuda()
+    B = x.shape[0]
+    info = torch.empty((B, spec.k), dtype=torch.uint8, device="cuda")
+    ok = torch.empty(B, dtype=torch.uint8, device="cuda")
+    pm = torch.empty(B, dtype=torch.float64, device="cuda")
+    pu = torch.empty(B, dtype=torch.int32, device="cuda")
+    n0 = dec.launches
+    dec.decode_device(x, info, ok, pm, pu)
+    torch.cuda.synchronize()
+    assert dec.launches == n0 + 1
+    assert np.array_equal(info.cpu().numpy(), ref.info_bits)
+    assert np.array_equal(ok.cpu().numpy().astype(bool), ref.crc_ok)
+    assert np.array_equal(pm.cpu().numpy(), ref.chosen_pm)
+    assert np.array_equal(pu.cpu().numpy(), ref.paths_used)
+    assert dec.last_kernel_ms() > 0
+    # pinned host tensors in and out
+    xh = torch.from_numpy(fb.llrs).pin_memory()
+    out = pb.BatchResult(torch.empty((B, spec.k), dtype=torch.uint8).pin_memory(),
+                         torch.empty(B, dtype=torch.uint8).pin_memory(),
+                         torch.empty(B, dtype=torch.float64).pin_memory(),
+                         torch.empty(B, dtype=torch.int32).pin_memory())
+    dec.decode_batch(xh, out=out)
+    assert np.array_equal(out.info_bits.numpy(), ref.info_bits)
+
+
+def test_batch_edge_cases(c1):
+    spec, sch, fb = c1
+    dec = pb.ListDecoder(sch, 4)
+    empty = dec.decode_batch(np.zeros((0, spec.N), np.float32))
+    assert empty.info_bits.shape == (0, spec.k)
+    # odd sizes around the grid size
+    for B in (1, 2, 31, 299):
+        r = dec.decode_batch(fb.llrs[:B])
+        o = oracle.decode_batch(sch, 4, fb.llrs[:B])
+        assert np.array_equal(r.info_bits, o.info_bits) and np.array_equal(r.chosen_pm, o.chosen_pm)
+    # saturated / noiseless / zero LLRs
+    pay = fb.payloads[0]
+    clean = (1.0 - 2.0 * pb.attach_and_encode(pay, spec).codeword) * 1e9
+    r = dec.decode(clean)
+    assert np.array_equal(r.info_bits, pay) and r.crc_ok and r.chosen_pm == 0.0
+    z = dec.decode_batch(np.zeros((2, spec.N), np.float32))
+    o = oracle.decode_batch(sch, 4, np.zeros((2, spec.N), np.float32))
+    assert np.array_equal(z.info_bits, o.info_bits) and np.array_equal(z.chosen_pm, o.chosen_pm)
+
+
+def test_errors(c1):
+    spec, sch, fb = c1
+    dec = pb.ListDecoder(sch, 4)
+    with pytest.raises(ValueError, match="spec wants 1024"):
+        dec.decode(np.zeros(1023))
+    with pytest.raises(ValueError):
+        dec.decode_batch(np.zeros((2, 1000), np.float32))
+    with pytest.raises(ValueError):
+        dec.decode_batch(np.zeros((2, spec.N), np.int8))      # int8 input on an f32 decoder
+    with pytest.raises(ValueError):
+        pb.ListDecoder(sch, 0)
+    with pytest.raises(ValueError):
+        pb.ListDecoder(sch, 33)
+
+
+def test_int8_inputs_match_float_quantised_inputs(c1):
+    spec, sch, fb = c1
+    dec = pb.ListDecoder(sch, 8, mode="int8")
+    q = pb.quantize_int8(fb.llrs)
+    a = dec.decode_batch(q)                 # int8 frames
+    b = dec.decode_batch(fb.llrs)           # float frames quantised on the device
+    o = oracle.decode_batch(sch, 8, q.astype(np.float32), int8=True)
+    for r in (a, b):
+        assert np.array_equal(r.info_bits, o.info_bits)
+        assert np.array_equal(r.chosen_pm, o.chosen_pm)
+        assert np.array_equal(r.paths_used, o.paths_used)
+
+
+def test_several_handles_coexist(c1):
+    spec, sch, fb = c1
+    decs = [pb.ListDecoder(sch, L) for L in (1, 2, 4, 8)]
+    for L, d in zip((1, 2, 4, 8), decs):
+        r = d.decode_batch(fb.llrs[:50])
+        o = oracle.decode_batch(sch, L, fb.llrs[:50])
+        assert np.array_equal(r.info_bits, o.info_bits)
+    import json
+    plan = json.loads(decs[-1].plan)
+    assert plan["L"] == 8 and plan["smem_per_frame"] > 0
+
+
+@pytest.mark.parametrize("warps", ["1", "2", "4", "8"])
+def test_warp_shapes_agree(c1, warps, monkeypatch):
+    spec, sch, fb = c1
+    monkeypatch.setenv("PB_WARPS", warps)
+    for L in (8, 32):
+        d = pb.ListDecoder(sch, L)
+        r = d.decode_batch(fb.llrs[:96])
+        o = oracle.decode_batch(sch, L, fb.llrs[:96])
+        assert np.array_equal(r.info_bits, o.info_bits)
+        assert np.array_equal(r.chosen_pm, o.chosen_pm)

@@ -1,0 +1,40 @@
+"""Dev helper: per-op cycle profile of one frame (CTA 0, clock64)."""
+import ctypes, sys, collections
+import numpy as np
+sys.path.insert(0, '.')
+import paper_1505_01466_b200 as pb
+from paper_1505_01466_b200 import _native
+import bench
+cfg = sys.argv[1] if len(sys.argv) > 1 else 'c3_L32'
+spec, sch, L, ebn0, mode, label = bench.make_code(cfg)
+dec = pb.ListDecoder(sch, L, mode=mode)
+lib = _native.lib()
+lib.pb_device_op_count.restype = ctypes.c_int
+lib.pb_device_op_count.argtypes = [ctypes.c_void_p]
+lib.pb_profile_ops.restype = ctypes.c_int
+lib.pb_profile_ops.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+n = lib.pb_device_op_count(dec._h)
+fb = pb.generate_frames(spec, ebn0, seed=1, start=0, count=4096)
+llr = np.ascontiguousarray(fb.llrs)
+cyc4 = np.zeros((n, 4), np.int64); kinds = np.zeros(n, np.int8); stages = np.zeros(n, np.int8)
+rc = lib.pb_profile_ops(dec._h, llr.ctypes.data, 0, len(llr), cyc4.ctypes.data, kinds.ctypes.data, stages.ctypes.data)
+_native.check(rc, 'pb_profile_ops')
+cyc = cyc4[:, 0]
+names = {0: 'F', 1: 'G', 2: 'R0', 3: 'REP', 4: 'R1', 5: 'SPC', 6: 'NOP'}
+tot = cyc.sum()
+print(f'{cfg}: {n} device ops, {tot} cycles for one frame (CTA 0, warps sharing the SM)')
+agg = collections.defaultdict(lambda: [0, 0])
+for k, s, c in zip(kinds, stages, cyc):
+    agg[(names[int(k)], int(s))][0] += 1; agg[(names[int(k)], int(s))][1] += int(c)
+byk = collections.defaultdict(int)
+for (k, s), (cnt, c) in agg.items(): byk[k] += c
+print(' '.join(f'{k}={v/tot*100:.1f}%' for k, v in sorted(byk.items(), key=lambda t: -t[1])))
+for (k, s), (cnt, c) in sorted(agg.items(), key=lambda t: -t[1][1])[:25]:
+    print(f'{k:4s} stage {s:2d}: {cnt:4d} ops  {c:9d} cycles  {c/cnt:8.0f}/op  {c/tot*100:5.1f}%')
+
+print('leaf phases (A scan / B select / C materialise) mean cycles:')
+for kk in (2, 3, 4, 5):
+    sel = kinds == kk
+    if sel.any():
+        print(f'  {names[kk]:4s} n={int(sel.sum()):3d}  A {cyc4[sel,1].mean():7.0f}  B {cyc4[sel,2].mean():7.0f}  C {cyc4[sel,3].mean():7.0f}  total {cyc4[sel,0].mean():7.0f}')
