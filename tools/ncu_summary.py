@@ -23,12 +23,16 @@ def main():
     rep, frames = sys.argv[1], int(sys.argv[2])
     raw = list(csv.reader(io.StringIO(ncu(rep, "--page", "raw", "--csv"))))
     d = dict(zip(raw[0], raw[2]))
+    units = dict(zip(raw[0], raw[1]))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+             "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
 
     def f(k):
         try:
-            return float(d[k])
+            v = float(d[k])
         except (KeyError, ValueError):
             return None
+        return v * scale.get(units.get(k, ""), 1.0)
 
     st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v)
           for k, v in d.items()
@@ -36,8 +40,8 @@ def main():
           and v.replace(".", "").isdigit()}
     tot = sum(st.values()) or 1.0
     out = {
-        "kernel_ms": f("gpu__time_duration.sum") and f("gpu__time_duration.sum") / 1e6
-        if (f("gpu__time_duration.sum") or 0) > 1e3 else f("gpu__time_duration.sum"),
+        "kernel_ms": f("gpu__time_duration.sum"),
+        "frames": frames,
         "inst_per_frame": (f("smsp__inst_executed.sum") or 0) / frames,
         "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "warps_active_pct": f("sm__warps_active.avg.pct_of_peak_sustained_active"),
@@ -46,6 +50,8 @@ def main():
         "shared_ld_per_frame": (f("smsp__sass_inst_executed_op_shared_ld.sum") or 0) / frames,
         "global_ld_per_frame": (f("smsp__sass_inst_executed_op_global_ld.sum") or 0) / frames,
         "dram_bytes_per_frame": ((f("dram__bytes_read.sum") or 0) + (f("dram__bytes_write.sum") or 0)) / frames,
+        "dram_bytes_per_launch_per_frame": ((f("dram__bytes_read.sum") or 0) + (f("dram__bytes_write.sum") or 0)) / frames,
+        "lts_bytes_per_frame": (f("lts__t_bytes.sum") or 0) / frames,
         "stalls_pct": {k: round(100 * v / tot, 1) for k, v in sorted(st.items(), key=lambda t: -t[1])[:8]},
     }
     # per-function instruction attribution (innermost source line)
