@@ -113,10 +113,11 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("PB_LIB_PATH") or LIB_PATH  # A/B experiments only
+    if not os.path.exists(path):
         raise RuntimeError(
-            f"native decoder library missing: {LIB_PATH} (run __graft_entry__.build())")
-    L = ctypes.CDLL(LIB_PATH)
+            f"native decoder library missing: {path} (run __graft_entry__.build())")
+    L = ctypes.CDLL(path)
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
     L.pb_create.restype = i32
     L.pb_create.argtypes = [ctypes.POINTER(PbCode), ctypes.POINTER(PbOp), i32, i32, i32, i32,

@@ -9,4 +9,6 @@
 extern "C" cudaError_t PB_CAT(pb_launch_, PB_TAG)(const pb::Params *p, int grid, size_t smem, cudaStream_t st) {
     return pb::launch_t<PB_T, PB_W, PB_PPW>(p, grid, smem, st);
 }
-extern "C" cudaError_t PB_CAT(pb_occ_, PB_TAG)(size_t smem, int *bps) { return pb::occ_t<PB_T, PB_W, PB_PPW>(smem, bps); }
+extern "C" cudaError_t PB_CAT(pb_occ_, PB_TAG)(size_t smem, int fpc, int *bps) {
+    return pb::occ_t<PB_T, PB_W, PB_PPW>(smem, fpc, bps);
+}

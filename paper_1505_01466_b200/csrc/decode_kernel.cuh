@@ -26,9 +26,24 @@
 //              among CRC-passing paths (listdec.py:289-308), polar transform
 //              of the winner and payload gather (encode.py:29-53,76-87)
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <math.h>
 #include <stdint.h>
+#else
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef short int16_t;
+typedef unsigned short uint16_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#define LLONG_MIN (-9223372036854775807LL - 1)
+#define LLONG_MAX 9223372036854775807LL
+#define INFINITY __int_as_float(0x7f800000)
+#endif
 
 #include "decoder.cuh"
 
@@ -115,14 +130,49 @@ struct ChanSrc {
     __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(ch + i); }
 };
 
+// ------------------------------------------------------- configuration
+// Code / layout constants.  RtCfg reads them from the launch parameters
+// (the interpreted kernel); generated kernels supply a type with the same
+// members returning literals, so every address folds at compile time.
+struct RtCfg {
+    const Params *p;
+    __device__ __forceinline__ int N() const { return p->N; }
+    __device__ __forceinline__ int n() const { return p->n; }
+    __device__ __forceinline__ int L() const { return p->L; }
+    __device__ __forceinline__ int k() const { return p->k; }
+    __device__ __forceinline__ int has_crc() const { return p->has_crc; }
+    __device__ __forceinline__ uint32_t crc_const() const { return p->crc_const; }
+    __device__ __forceinline__ int ch_off() const { return p->lay.ch_off; }
+    __device__ __forceinline__ int a_off(int s) const { return p->lay.a_off[s]; }
+    __device__ __forceinline__ int a_gfrom() const { return p->lay.a_gfrom; }
+    __device__ __forceinline__ int b_off(int s) const { return p->lay.b_off[s]; }
+    __device__ __forceinline__ int b_stride(int s) const { return p->lay.b_stride[s]; }
+    __device__ __forceinline__ int pm_off() const { return p->lay.pm_off; }
+    __device__ __forceinline__ int ia_off() const { return p->lay.ia_off; }
+    __device__ __forceinline__ int ib_off() const { return p->lay.ib_off; }
+    __device__ __forceinline__ int idx_stride() const { return p->lay.idx_stride; }
+    __device__ __forceinline__ int cd_off() const { return p->lay.cd_off; }
+    __device__ __forceinline__ int clrb_off() const { return p->lay.clrb_off; }
+    __device__ __forceinline__ int cflag_off() const { return p->lay.cflag_off; }
+    __device__ __forceinline__ int asg_off() const { return p->lay.asg_off; }
+    __device__ __forceinline__ int hard_off() const { return p->lay.hard_off; }
+    __device__ __forceinline__ int hard_words() const { return p->lay.hard_words; }
+    __device__ __forceinline__ int root_off() const { return p->lay.root_off; }
+    __device__ __forceinline__ int root_words() const { return p->lay.root_words; }
+    __device__ __forceinline__ int gbytes() const { return p->lay.gbytes; }
+    __device__ __forceinline__ int smem_bytes() const { return p->lay.smem_bytes; }
+};
+
 // ------------------------------------------------------- frame state
 
-template <typename T, int W, int PPW>
+template <typename T, int W, int PPW, class CFG = RtCfg>
 struct Dec {
     static constexpr int LP = ilog2(PPW);
     static constexpr int GSS = 32 / PPW;           // steady-state lanes per path
     static constexpr int NBUF = W > 1 ? 2 : 1;     // candidate buffers
     const Params &P;
+    CFG cfg;
+    unsigned char *sm;  // this frame's shared-memory block
     unsigned char *gs;  // this frame's global scratch block
     int lane, warp;
     int cur;            // live half of the double-buffered path state
@@ -130,57 +180,52 @@ struct Dec {
     int lpar;           // parity used by the last forking leaf
     long long *ph;      // debug: phase timestamps of the current op (or null)
 
-    __device__ Dec(const Params &p, unsigned char *g)
-        : P(p), gs(g), lane(threadIdx.x & 31), warp(threadIdx.x >> 5), cur(0), par(0), lpar(0), ph(nullptr) {}
+    __device__ Dec(const Params &p, CFG c, unsigned char *s, unsigned char *g)
+        : P(p), cfg(c), sm(s), gs(g), lane(threadIdx.x & 31), warp((threadIdx.x >> 5) & (W - 1)), cur(0), par(0),
+          lpar(0), ph(nullptr) {}
     __device__ __forceinline__ void mark(int i) const {
-        if (ph) ph[i] = clock64();
+        if (ph && lane == 0) ph[i] = clock64();
     }
 
     // row r, element 0 of a block-interleaved stage s
     __device__ __forceinline__ int rowoff(int s, int r) const { return ((r >> LP) << (LP + s)) + (r & (PPW - 1)); }
-    __device__ __forceinline__ T *a_sm(int s) const { return reinterpret_cast<T *>(g_smem + P.lay.a_off[s]); }
-    __device__ __forceinline__ T *a_gl(int s) const { return reinterpret_cast<T *>(gs + P.lay.a_off[s]); }
+    __device__ __forceinline__ T *a_sm(int s) const { return reinterpret_cast<T *>(sm + cfg.a_off(s)); }
+    __device__ __forceinline__ T *a_gl(int s) const { return reinterpret_cast<T *>(gs + cfg.a_off(s)); }
     __device__ __forceinline__ uint32_t *beta_row(int s, int row) const {
-        return reinterpret_cast<uint32_t *>(g_smem + P.lay.b_off[s]) + row * P.lay.b_stride[s];
+        return reinterpret_cast<uint32_t *>(sm + cfg.b_off(s)) + row * cfg.b_stride(s);
     }
-    __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(g_smem + P.lay.ch_off); }
+    __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(sm + cfg.ch_off()); }
     __device__ __forceinline__ double *pm(int b) const {
-        return reinterpret_cast<double *>(g_smem + P.lay.pm_off) + b * P.L;
-    }
-    __device__ __forceinline__ uint32_t *syn(int b) const {
-        return reinterpret_cast<uint32_t *>(g_smem + P.lay.syn_off) + b * P.L;
+        return reinterpret_cast<double *>(sm + cfg.pm_off()) + b * cfg.L();
     }
     // alpha / beta row index of path q at stage / slot s, four stages per
     // word: byte (s & 3) of word [buf][s >> 2][path]
     __device__ __forceinline__ uint8_t &ia(int b, int s, int q) const {
-        return g_smem[P.lay.ia_off + ((b * P.lay.idx_stride + (s >> 2)) * P.L + q) * 4 + (s & 3)];
+        return sm[cfg.ia_off() + ((b * cfg.idx_stride() + (s >> 2)) * cfg.L() + q) * 4 + (s & 3)];
     }
     __device__ __forceinline__ uint8_t &ib(int b, int s, int q) const {
-        return g_smem[P.lay.ib_off + ((b * P.lay.idx_stride + (s >> 2)) * P.L + q) * 4 + (s & 3)];
+        return sm[cfg.ib_off() + ((b * cfg.idx_stride() + (s >> 2)) * cfg.L() + q) * 4 + (s & 3)];
     }
     __device__ __forceinline__ uint32_t &iaw(int b, int x, int q) const {
-        return reinterpret_cast<uint32_t *>(g_smem + P.lay.ia_off)[(b * P.lay.idx_stride + x) * P.L + q];
+        return reinterpret_cast<uint32_t *>(sm + cfg.ia_off())[(b * cfg.idx_stride() + x) * cfg.L() + q];
     }
     __device__ __forceinline__ uint32_t &ibw(int b, int x, int q) const {
-        return reinterpret_cast<uint32_t *>(g_smem + P.lay.ib_off)[(b * P.lay.idx_stride + x) * P.L + q];
+        return reinterpret_cast<uint32_t *>(sm + cfg.ib_off())[(b * cfg.idx_stride() + x) * cfg.L() + q];
     }
     __device__ __forceinline__ int bsel(int b) const { return NBUF > 1 ? b : 0; }
     // candidate data: [buf][entry][source path]
     __device__ __forceinline__ double &cd(int b, int c, int q) const {
-        return reinterpret_cast<double *>(g_smem + P.lay.cd_off)[(bsel(b) * kMaxCand + c) * P.L + q];
+        return reinterpret_cast<double *>(sm + cfg.cd_off())[(bsel(b) * kMaxCand + c) * cfg.L() + q];
     }
     __device__ __forceinline__ uint16_t &clrb(int b, int j, int q) const {
-        return reinterpret_cast<uint16_t *>(g_smem + P.lay.clrb_off)[(bsel(b) * 4 + j) * P.L + q];
+        return reinterpret_cast<uint16_t *>(sm + cfg.clrb_off())[(bsel(b) * 4 + j) * cfg.L() + q];
     }
-    __device__ __forceinline__ uint32_t *chs(int b) const {
-        return reinterpret_cast<uint32_t *>(g_smem + P.lay.chs_off) + bsel(b) * P.L;
-    }
-    __device__ __forceinline__ uint8_t *cflag(int b) const { return g_smem + P.lay.cflag_off + bsel(b) * P.L; }
-    __device__ __forceinline__ uint8_t *asg(int b) const { return g_smem + P.lay.asg_off + bsel(b) * 2 * P.L; }
+    __device__ __forceinline__ uint8_t *cflag(int b) const { return sm + cfg.cflag_off() + bsel(b) * cfg.L(); }
+    __device__ __forceinline__ uint8_t *asg(int b) const { return sm + cfg.asg_off() + bsel(b) * 2 * cfg.L(); }
     __device__ __forceinline__ uint32_t &hard(int b, int w, int q) const {
-        return reinterpret_cast<uint32_t *>(g_smem + P.lay.hard_off)[(bsel(b) * P.lay.hard_words + w) * P.L + q];
+        return reinterpret_cast<uint32_t *>(sm + cfg.hard_off())[(bsel(b) * cfg.hard_words() + w) * cfg.L() + q];
     }
-    __device__ __forceinline__ uint32_t *root() const { return reinterpret_cast<uint32_t *>(g_smem + P.lay.root_off); }
+    __device__ __forceinline__ uint32_t *root() const { return reinterpret_cast<uint32_t *>(sm + cfg.root_off()); }
 
     __device__ __forceinline__ void sync() const {
         if (W > 1)
@@ -256,12 +301,12 @@ __device__ __forceinline__ void fg_chunks(const S &src, T *dst, const uint32_t *
     }
 }
 
-template <typename T, int W, int PPW, bool IS_G, class S>
-__device__ __forceinline__ void fg_to_dst(const Dec<T, W, PPW> &F, const S &src, int s, int q, const uint32_t *bw,
+template <typename T, int W, int PPW, class CFG, bool IS_G, class S>
+__device__ __forceinline__ void fg_to_dst(const Dec<T, W, PPW, CFG> &F, const S &src, int s, int q, const uint32_t *bw,
                                           int h, int G, int sub) {
-    constexpr int GS = Dec<T, W, PPW>::GSS;
+    constexpr int GS = Dec<T, W, PPW, CFG>::GSS;
     const int off = F.rowoff(s - 1, q);
-    if (s - 1 < F.P.lay.a_gfrom) {
+    if (s - 1 < F.cfg.a_gfrom()) {
         T *d = F.a_sm(s - 1) + off;
         if (G == GS && h >= 32)
             fg_chunks<T, IS_G, GS, PPW>(src, d, bw, h, sub);
@@ -276,26 +321,27 @@ __device__ __forceinline__ void fg_to_dst(const Dec<T, W, PPW> &F, const S &src,
     }
 }
 
-template <typename T, int W, int PPW, bool IS_G>
-__device__ __forceinline__ void fg_op(Dec<T, W, PPW> &F, const DOp &o) {
+template <typename T, int W, int PPW, class CFG, bool IS_G>
+__device__ __forceinline__ void fg_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
     const auto mp = F.map(o.pin);
-    if (!mp.active) return;
+    if (!mp.active || (F.P.ablate & 8)) return;
     const Params &P = F.P;
+    const CFG &cfg = F.cfg;
     const int s = o.stage, h = 1 << (s - 1), q = mp.q;
     const uint32_t *bw = IS_G ? F.beta_row(s - 1, F.ib(F.cur, s - 1, q)) : nullptr;
-    if (s == P.n - 1) {
+    if (s == cfg.n() - 1) {
         if (o.vmode == VM_F)
-            fg_to_dst<T, W, PPW, IS_G>(F, VirtF<T>{F.channel(), P.N >> 1}, s, q, bw, h, mp.G, mp.sub);
+            fg_to_dst<T, W, PPW, CFG, IS_G>(F, VirtF<T>{F.channel(), cfg.N() >> 1}, s, q, bw, h, mp.G, mp.sub);
         else
-            fg_to_dst<T, W, PPW, IS_G>(
-                F, VirtG<T>{F.channel(), F.beta_row(P.n - 1, F.ib(F.cur, P.n - 1, q)), P.N >> 1}, s, q, bw, h, mp.G,
+            fg_to_dst<T, W, PPW, CFG, IS_G>(
+                F, VirtG<T>{F.channel(), F.beta_row(cfg.n() - 1, F.ib(F.cur, cfg.n() - 1, q)), cfg.N() >> 1}, s, q, bw, h, mp.G,
                 mp.sub);
     } else {
         const int off = F.rowoff(s, F.ia(F.cur, s, q));
-        if (s < P.lay.a_gfrom)
-            fg_to_dst<T, W, PPW, IS_G>(F, RowSrc<T, PPW>{F.a_sm(s) + off}, s, q, bw, h, mp.G, mp.sub);
+        if (s < cfg.a_gfrom())
+            fg_to_dst<T, W, PPW, CFG, IS_G>(F, RowSrc<T, PPW>{F.a_sm(s) + off}, s, q, bw, h, mp.G, mp.sub);
         else
-            fg_to_dst<T, W, PPW, IS_G>(F, RowSrc<T, PPW>{F.a_gl(s) + off}, s, q, bw, h, mp.G, mp.sub);
+            fg_to_dst<T, W, PPW, CFG, IS_G>(F, RowSrc<T, PPW>{F.a_gl(s) + off}, s, q, bw, h, mp.G, mp.sub);
     }
     if (mp.sub == 0) F.ia(F.cur, s - 1, q) = (uint8_t)q;
 }
@@ -346,7 +392,7 @@ __device__ __forceinline__ void pw_sums(const S &src, int m, bool active, int su
     const int nb = m / blk;
     const int per = blk >> 3;
     const bool act = active && sub < GS;
-    float stk[8][NS];
+    float stk[7][NS];
     float carry[NS];
     for (int b = 0; b < nb; ++b) {
         float acc[NA][NS];
@@ -379,16 +425,23 @@ __device__ __forceinline__ void pw_sums(const S &src, int m, bool active, int su
                         for (int t = 0; t < NS; ++t) acc[a][t] = __fadd_rn(acc[a][t], acc[a + step][t]);
             }
         }
+        // combine block sums in numpy's halving order: registers for the
+        // common nb <= 2, a binary-counter stack (local memory) beyond
+        if (nb <= 2) {
 #pragma unroll
-        for (int t = 0; t < NS; ++t) carry[t] = acc[0][t];
-        int lvl = 0;
-        while ((b >> lvl) & 1) {
+            for (int t = 0; t < NS; ++t) carry[t] = b == 0 ? acc[0][t] : __fadd_rn(carry[t], acc[0][t]);
+        } else {
 #pragma unroll
-            for (int t = 0; t < NS; ++t) carry[t] = __fadd_rn(stk[lvl][t], carry[t]);
-            ++lvl;
+            for (int t = 0; t < NS; ++t) carry[t] = acc[0][t];
+            int lvl = 0;
+            while ((b >> lvl) & 1) {
+#pragma unroll
+                for (int t = 0; t < NS; ++t) carry[t] = __fadd_rn(stk[lvl][t], carry[t]);
+                ++lvl;
+            }
+#pragma unroll
+            for (int t = 0; t < NS; ++t) stk[lvl][t] = carry[t];
         }
-#pragma unroll
-        for (int t = 0; t < NS; ++t) stk[lvl][t] = carry[t];
     }
 #pragma unroll
     for (int t = 0; t < NS; ++t) out[t] = carry[t];
@@ -437,6 +490,14 @@ struct TopK {
     // ascending index scan: only strictly smaller values enter (stable argsort);
     // once placed, the displaced entries shift down unconditionally
     __device__ __forceinline__ void push_scan(float v, int idx) {
+        if (K == 2) {  // branch-free
+            const bool lt0 = v < m[0], lt1 = v < m[K - 1];
+            m[K - 1] = lt0 ? m[0] : (lt1 ? v : m[K - 1]);
+            i[K - 1] = lt0 ? i[0] : (lt1 ? idx : i[K - 1]);
+            m[0] = lt0 ? v : m[0];
+            i[0] = lt0 ? idx : i[0];
+            return;
+        }
         if (v < m[K - 1]) {
             bool placed = false;
 #pragma unroll
@@ -531,9 +592,9 @@ __device__ __forceinline__ long long warp_min_ll(long long v) {
 // candidate beats the worst kept key it replaces it (REDUX max / min).  Then
 // every key > Tk survives, plus the earliest ties == Tk in (source, cand)
 // order until L are kept.
-template <typename T, int W, int PPW>
-__device__ __forceinline__ void select_phase(const Dec<T, W, PPW> &F, const DOp &o) {
-    const int lane = F.lane, np = o.pin, C = o.ncand, L = F.P.L;
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const DOp &o) {
+    const int lane = F.lane, np = o.pin, C = o.ncand, L = F.cfg.L();
     const bool vl = lane < np;
     const double pm = vl ? F.pm(F.cur)[lane] : 0.0;
     long long key[kMaxCand];
@@ -562,6 +623,7 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW> &F, const DOp 
                     srt[c + 1] = x > y ? y : x;
                 }
         }
+        F.mark(4);
         // kept set: slot = lane (< L); start from every source's best
         long long kept = lane < L ? srt[0] : LLONG_MAX;
         int ptr = 1;
@@ -579,6 +641,7 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW> &F, const DOp 
             if (lane == into) kept = best;
         }
         const long long Tk = warp_min_ll(kept);
+        F.mark(5);
         // Tk = the L-th best key; keep all better, then the earliest ties
         int gt = 0, eq = 0;
 #pragma unroll
@@ -599,6 +662,7 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW> &F, const DOp 
             }
         }
     }
+    F.mark(6);
     int k = excl_scan(__popc(mask), lane);
     uint8_t *asg = F.asg(F.par);
     while (mask) {
@@ -613,8 +677,8 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW> &F, const DOp 
 // ----------------------------------------------------- leaf word + chain
 
 // 32-bit word w of the leaf word of decision (p, c) (m < 32: the m-bit value)
-template <typename T, int W, int PPW>
-__device__ __forceinline__ uint32_t leaf_word(const Dec<T, W, PPW> &F, int b, int kind, int m, int p, int c,
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ uint32_t leaf_word(const Dec<T, W, PPW, CFG> &F, int b, int kind, int m, int p, int c,
                                               int w) {
     const uint32_t fullw = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
     if (kind == DK_R0) return 0u;
@@ -648,8 +712,8 @@ __device__ __forceinline__ void bits_put(uint32_t *row, int off, int len, uint32
 //   dst[E - 2^(s+1), E - 2^s) = slot_s[row_s] ^ dst[E - 2^s, E)
 // (listdec.py:327-332 with the right child's bits kept where they are).
 // Called by all lanes of a warp (synchronises the warp between steps).
-template <typename T, int W, int PPW>
-__device__ __forceinline__ void word_and_chain(const Dec<T, W, PPW> &F, int b, const DOp &o, int kind, bool active,
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ void word_and_chain(const Dec<T, W, PPW, CFG> &F, int b, const DOp &o, int kind, bool active,
                                                int G, int sub, int p, int c, int ibuf, int ipath, uint32_t *dst,
                                                int sE) {
     const int t = o.stage, m = 1 << t, E = 1 << sE;
@@ -679,8 +743,8 @@ __device__ __forceinline__ void word_and_chain(const Dec<T, W, PPW> &F, int b, c
 
 // ------------------------------------------------------------- leaves
 
-template <typename T, int W, int PPW, class S>
-__device__ __forceinline__ void leaf_sums(Dec<T, W, PPW> &F, const DOp &o, int kind, const S &src, int q, bool active,
+template <typename T, int W, int PPW, class CFG, class S>
+__device__ __forceinline__ void leaf_sums(Dec<T, W, PPW, CFG> &F, const DOp &o, int kind, const S &src, int q, bool active,
                                           int G, int sub) {
     const int m = 1 << o.stage;
     const int lead = F.lane - sub;
@@ -701,32 +765,20 @@ __device__ __forceinline__ void leaf_sums(Dec<T, W, PPW> &F, const DOp &o, int k
     }
 }
 
-// CRC syndrome contribution of a hard-decision word whose bit j sits at u
-// index pos + j (j < cnt; pos + cnt stays inside one aligned 32-block):
-// XOR of the leaf-local syndrome rows of its set bits, by nibble tables.
-__device__ __forceinline__ uint32_t syn_word(const uint32_t *T4, uint32_t word, int pos, int cnt) {
-    const int sh = pos & 31;
-    const uint32_t x = word << sh;
-    const uint32_t *t = T4 + ((pos & ~31) >> 2) * 16;
-    uint32_t s = 0u;
-    const int n1 = (sh + cnt + 3) >> 2;
-    for (int nb = sh >> 2; nb < n1; ++nb) s ^= __ldg(t + nb * 16 + ((x >> (4 * nb)) & 15u));
-    return s;
-}
 
 // Rate-1 / SPC scan: stable K least reliable positions, hard decisions,
 // parity and syndrome of the hard word.  Gl (<= G) lanes of the path's group
 // scan (one lane unless the node is large); the rest idle.
-template <typename T, int W, int PPW, int K, class S>
-__device__ __forceinline__ void leaf_scan(Dec<T, W, PPW> &F, const DOp &o, int kind, const S &src, int q,
+template <typename T, int W, int PPW, class CFG, int K, class S>
+__device__ __forceinline__ void leaf_scan(Dec<T, W, PPW, CFG> &F, const DOp &o, int kind, const S &src, int q,
                                           bool active, int G, int sub) {
     const Params &P = F.P;
+    const CFG &cfg = F.cfg;
     const int m = 1 << o.stage;
     int Gl = m >> 4;
     Gl = Gl < 1 ? 1 : (Gl > G ? G : Gl);
     TopK<K> tk;
     tk.init();
-    uint32_t hs = 0u;
     int par = 0;
     if (Gl == 1) {
         if (active && sub == 0) {
@@ -741,9 +793,9 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW> &F, const DOp &o, int k
                 }
                 F.hard(F.par, w0 >> 5, q) = word;
                 par ^= __popc(word);
-                hs ^= syn_word(P.msyn4, word, o.off + w0, cnt);
             }
         }
+        F.mark(2);
     } else {
         const int lgl = 31 - __clz(Gl);
         const bool scan = active && sub < Gl;
@@ -762,10 +814,7 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW> &F, const DOp &o, int k
             const int base = it << lgl;
             hword |= gb << (base & 31);
             if (((base + Gl) & 31) == 0 || it == iters - 1) {
-                if (scan && sub == 0) {
-                    F.hard(F.par, base >> 5, hq) = hword;
-                    hs ^= syn_word(P.msyn4, hword, o.off + ((base >> 5) << 5), m < 32 ? m : 32);
-                }
+                if (scan && sub == 0) F.hard(F.par, base >> 5, hq) = hword;
                 par ^= __popc(hword);
                 hword = 0u;
             }
@@ -784,9 +833,7 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW> &F, const DOp &o, int k
     }
     if (!(active && sub == 0)) return;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-        F.clrb(F.par, k, q) = (uint16_t)(k < K && tk.i[k < K ? k : 0] < m ? tk.i[k < K ? k : 0] : 0);
-    F.chs(F.par)[q] = hs;
+    for (int k = 0; k < K; ++k) F.clrb(F.par, k, q) = (uint16_t)(tk.i[k] < m ? tk.i[k] : 0);
     if (kind == DK_R1) {  // listdec.py:360-372
         const double w1 = (double)tk.m[0], w2 = (double)tk.m[1];
         F.cd(F.par, 0, q) = 0.0;
@@ -799,76 +846,88 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW> &F, const DOp &o, int k
     // SPC, listdec.py:373-394: deltas sum the net flips in ascending position
     const int odd = par & 1;
     F.cflag(F.par)[q] = (uint8_t)odd;
-    int ord[4] = {0, 1, 2, 3};
+    // rank of each LRB slot by position (the reference sums net flips in
+    // ascending position order); all indices static
+    int rk[4];
 #pragma unroll
-    for (int x = 1; x < 4; ++x)
+    for (int x = 0; x < 4; ++x) {
+        rk[x] = 0;
 #pragma unroll
-        for (int y = x; y > 0; --y)
-            if (tk.i[ord[y] & (K - 1)] < tk.i[ord[y - 1] & (K - 1)]) {
-                const int tt = ord[y];
-                ord[y] = ord[y - 1];
-                ord[y - 1] = tt;
-            }
-    double w[4];
+        for (int y = 0; y < 4; ++y) rk[x] += tk.i[y & (K - 1)] < tk.i[x & (K - 1)] ? 1 : 0;
+    }
+    double wr[4];  // magnitudes by position rank
 #pragma unroll
-    for (int k = 0; k < 4; ++k) w[k] = (double)tk.m[k & (K - 1)];
-    for (int c = 0; c < o.ncand; ++c) {
-        const int fm = flip_mask(DK_SPC, c, odd);
-        double accd = 0.0;
-        bool any = false;
+    for (int r = 0; r < 4; ++r) {
+        double v = 0.0;
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
-            if ((fm >> ord[x]) & 1) {
-                accd = any ? accd + w[ord[x]] : w[ord[x]];
-                any = true;
-            }
-        F.cd(F.par, c, q) = any ? -accd : 0.0;
+        for (int x = 0; x < 4; ++x) v = rk[x] == r ? (double)tk.m[x & (K - 1)] : v;
+        wr[r] = v;
+    }
+#pragma unroll
+    for (int c = 0; c < kMaxCand; ++c) {
+        if (c < o.ncand) {
+            const int fm = flip_mask(DK_SPC, c, odd);
+            int fr = 0;  // flip set in rank order
+#pragma unroll
+            for (int x = 0; x < 4; ++x) fr |= ((fm >> x) & 1) << rk[x];
+            double accd = 0.0;
+            bool any = false;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if ((fr >> r) & 1) {
+                    accd = any ? accd + wr[r] : wr[r];
+                    any = true;
+                }
+            F.cd(F.par, c, q) = any ? -accd : 0.0;
+        }
     }
 }
 
-template <typename T, int W, int PPW, class S>
-__device__ __forceinline__ void leaf_phase_a(Dec<T, W, PPW> &F, const DOp &o, int kind, const S &src, int q,
+template <typename T, int W, int PPW, class CFG, class S>
+__device__ __forceinline__ void leaf_phase_a(Dec<T, W, PPW, CFG> &F, const DOp &o, int kind, const S &src, int q,
                                              bool active, int G, int sub) {
     if (kind == DK_R0 || kind == DK_REP)
         leaf_sums(F, o, kind, src, q, active, G, sub);
     else if (kind == DK_R1)
-        leaf_scan<T, W, PPW, 2>(F, o, kind, src, q, active, G, sub);
+        leaf_scan<T, W, PPW, CFG, 2>(F, o, kind, src, q, active, G, sub);
     else
-        leaf_scan<T, W, PPW, 4>(F, o, kind, src, q, active, G, sub);
+        leaf_scan<T, W, PPW, CFG, 4>(F, o, kind, src, q, active, G, sub);
 }
 
 // dispatch on where the node's LLRs live
-template <typename T, int W, int PPW>
-__device__ __forceinline__ void leaf_read(Dec<T, W, PPW> &F, const DOp &o, int kind, int q, bool active, int G,
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ void leaf_read(Dec<T, W, PPW, CFG> &F, const DOp &o, int kind, int q, bool active, int G,
                                           int sub) {
     const Params &P = F.P;
+    const CFG &cfg = F.cfg;
     const int t = o.stage;
     const int qq = active ? q : F.warp * PPW;
-    if (t == P.n) {
+    if (t == cfg.n()) {
         leaf_phase_a(F, o, kind, ChanSrc<T>{F.channel()}, q, active, G, sub);
-    } else if (t == P.n - 1) {
+    } else if (t == cfg.n() - 1) {
         if (o.vmode == VM_F)
-            leaf_phase_a(F, o, kind, VirtF<T>{F.channel(), P.N >> 1}, q, active, G, sub);
+            leaf_phase_a(F, o, kind, VirtF<T>{F.channel(), cfg.N() >> 1}, q, active, G, sub);
         else
-            leaf_phase_a(F, o, kind, VirtG<T>{F.channel(), F.beta_row(P.n - 1, F.ib(F.cur, P.n - 1, qq)), P.N >> 1}, q,
+            leaf_phase_a(F, o, kind, VirtG<T>{F.channel(), F.beta_row(cfg.n() - 1, F.ib(F.cur, cfg.n() - 1, qq)), cfg.N() >> 1}, q,
                          active, G, sub);
     } else {
         const int off = F.rowoff(t, F.ia(F.cur, t, qq));
-        if (t < P.lay.a_gfrom)
+        if (t < cfg.a_gfrom())
             leaf_phase_a(F, o, kind, RowSrc<T, PPW>{F.a_sm(t) + off}, q, active, G, sub);
         else
             leaf_phase_a(F, o, kind, RowSrc<T, PPW>{F.a_gl(t) + off}, q, active, G, sub);
     }
 }
 
-template <typename T, int W, int PPW>
-__device__ __forceinline__ void leaf_op(Dec<T, W, PPW> &F, const DOp &o) {
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ void leaf_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
     const Params &P = F.P;
+    const CFG &cfg = F.cfg;
     int kind = o.kind;
     if (kind == DK_R1 && o.stage == 0) kind = DK_REP;  // listdec.py:347
 
     // Phase A: per-source sums / scans, this warp's sources
-    {
+    if (!(P.ablate & 1)) {
         const auto mp = F.map(o.pin);
         leaf_read(F, o, kind, mp.q, mp.active, mp.G, mp.sub);
     }
@@ -877,7 +936,11 @@ __device__ __forceinline__ void leaf_op(Dec<T, W, PPW> &F, const DOp &o) {
 
     const bool fork = kind != DK_R0;
     if (fork) {
-        if (F.warp == 0) select_phase(F, o);
+        if (F.warp == 0 && !(P.ablate & 2)) select_phase(F, o);
+        if (F.warp == 0 && (P.ablate & 2) && F.lane < o.pout) {  // timing only: a valid dummy choice
+            F.asg(F.par)[2 * F.lane] = (uint8_t)(F.lane % o.pin);
+            F.asg(F.par)[2 * F.lane + 1] = 0;
+        }
         F.sync();
     }
     F.mark(1);
@@ -893,26 +956,15 @@ __device__ __forceinline__ void leaf_op(Dec<T, W, PPW> &F, const DOp &o) {
         c = F.asg(b)[2 * k + 1];
     }
     if (fork && mp.active && mp.sub == 0) {
-        uint32_t sy = F.syn(F.cur)[p];
-        if (kind == DK_REP) {
-            const bool ones = F.cflag(b)[p] ? (c == 0) : (c == 1);
-            if (ones) sy ^= o.rep_syn;
-        } else {
-            sy ^= F.chs(b)[p];
-            const int fm = flip_mask(kind, c, F.cflag(b)[p]);
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-                if ((fm >> jj) & 1) sy ^= __ldg(P.msyn + o.off + F.clrb(b, jj, p));
-        }
-        F.syn(nxt)[k] = sy;
         F.pm(nxt)[k] = F.pm(F.cur)[p] + F.cd(b, c, p);  // listdec.py:415
-        for (int x = 0; x < P.lay.idx_stride; ++x) {  // lazy copy: inherit the source's rows
+        for (int x = 0; x < cfg.idx_stride(); ++x) {  // lazy copy: inherit the source's rows
             F.iaw(nxt, x, k) = F.iaw(F.cur, x, p);
             F.ibw(nxt, x, k) = F.ibw(F.cur, x, p);
         }
     }
+    F.mark(7);
     const int sE = o.target;
-    if (sE < P.n) {
+    if (sE < cfg.n() && !(P.ablate & 4)) {
         word_and_chain(F, b, o, kind, mp.active, mp.G, mp.sub, p, c, F.cur, mp.active ? p : 0, F.beta_row(sE, k), sE);
         if (mp.active && mp.sub == 0) F.ib(nxt, sE, k) = (uint8_t)k;
     }
@@ -945,8 +997,8 @@ __device__ __forceinline__ void polar_transform_words(uint32_t *x, int N, int la
     }
 }
 
-template <typename T, int W, int PPW>
-__device__ __forceinline__ void build_root(const Dec<T, W, PPW> &F, const DOp &fo, int k, uint32_t *dst) {
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ void build_root(const Dec<T, W, PPW, CFG> &F, const DOp &fo, int k, uint32_t *dst) {
     int kind = fo.kind;
     if (kind == DK_R1 && fo.stage == 0) kind = DK_REP;
     int p = k, c = 0;
@@ -955,57 +1007,104 @@ __device__ __forceinline__ void build_root(const Dec<T, W, PPW> &F, const DOp &f
         p = F.asg(b)[2 * k];
         c = F.asg(b)[2 * k + 1];
     }
-    if (F.P.N < 32 && F.lane == 0) dst[0] = 0u;
+    if (F.cfg.N() < 32 && F.lane == 0) dst[0] = 0u;
     __syncwarp();
-    word_and_chain(F, b, fo, kind, true, 32, F.lane, p, c, F.cur, k, dst, F.P.n);
+    word_and_chain(F, b, fo, kind, true, 32, F.lane, p, c, F.cur, k, dst, F.cfg.n());
     __syncwarp();
 }
 
-template <typename T, int W, int PPW>
-__device__ __forceinline__ void finalize(Dec<T, W, PPW> &F, long long f, int np) {
+// CRC syndrome of codeword x (N bits, packed) in the codeword domain:
+// XOR of the syndrome rows of its set bits by nibble tables, warp-parallel;
+// equal to the u-domain check of extract_payload + crc_check
+// (encode.py:76-87, codes.py:150-156) because u = x G_N (G_N involution).
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ uint32_t codeword_syndrome(const Dec<T, W, PPW, CFG> &F, const uint32_t *x) {
+    const int N = F.cfg.N(), nw = N >= 32 ? N >> 5 : 1;
+    uint32_t s = 0u;
+    for (int w = F.lane; w < nw; w += 32) {
+        uint32_t v = x[w];
+        if (N < 32) v &= (1u << N) - 1u;
+        const uint32_t *t = F.P.xsyn4 + (size_t)w * 128;  // 8 nibbles x 16 entries per word
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) s ^= __ldg(t + nb * 16 + ((v >> (4 * nb)) & 15u));
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) s ^= __shfl_xor_sync(FULL_MASK, s, d);
+    return s;
+}
+
+// listdec.py:289-308: among CRC-passing survivors the strictly greater
+// metric wins, earliest survivor on ties; with none passing, the best metric
+// overall.  Equivalently: visit survivors by (metric desc, index asc) and
+// take the first that passes -- normally the very first, so only one or two
+// codewords are built and checked per frame.
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ void finalize(Dec<T, W, PPW, CFG> &F, long long f, int np) {
     const Params &P = F.P;
+    const CFG &cfg = F.cfg;
     const int lane = F.lane;
     const DOp fo = P.prog[P.final_op];
     const bool live = lane < np;
     const double pmk = live ? F.pm(F.cur)[lane] : -INFINITY;
-    const bool ok = live && P.has_crc && F.syn(F.cur)[lane] == P.crc_const;
-    const bool anyok = __any_sync(FULL_MASK, ok);
-    const bool elig = live && (!anyok || ok);
-    // listdec.py:297-301: strictly greater metric wins, earliest on ties
-    double bm = elig ? pmk : -INFINITY;
-    int bk = elig ? lane : 64;
+    const int rw = cfg.root_words();
+    uint32_t *u = F.root();
+    if (P.path_cw) {  // decode_paths: every survivor's codeword, metric and CRC flag
+        for (int kk = 0; kk < np; ++kk) {
+            uint32_t *dst = P.path_cw + ((size_t)f * cfg.L() + kk) * rw;
+            build_root(F, fo, kk, dst);
+            const uint32_t syn = codeword_syndrome(F, dst);
+            if (lane == 0) P.path_crc[(size_t)f * cfg.L() + kk] = cfg.has_crc() && syn == cfg.crc_const();
+        }
+        if (live) P.path_pm[(size_t)f * cfg.L() + lane] = pmk;
+        __syncwarp();
+    }
+    unsigned tried = 0u;
+    int first = -1, wnr = -1;
+    double wpm = -INFINITY;
+    for (int it = 0; it < np; ++it) {
+        // best untried survivor: max metric, lowest index
+        double bm = (live && !((tried >> lane) & 1u)) ? pmk : -INFINITY;
+        int bk = (live && !((tried >> lane) & 1u)) ? lane : 64;
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        const double om = __shfl_xor_sync(FULL_MASK, bm, d);
-        const int ok2 = __shfl_xor_sync(FULL_MASK, bk, d);
-        if (om > bm || (om == bm && ok2 < bk)) {
-            bm = om;
-            bk = ok2;
+        for (int d = 16; d > 0; d >>= 1) {
+            const double om = __shfl_xor_sync(FULL_MASK, bm, d);
+            const int ok2 = __shfl_xor_sync(FULL_MASK, bk, d);
+            if (om > bm || (om == bm && ok2 < bk)) {
+                bm = om;
+                bk = ok2;
+            }
+        }
+        if (first < 0) first = bk;
+        tried |= 1u << bk;
+        if (!cfg.has_crc() || (P.ablate & 16)) {
+            wnr = bk;
+            wpm = bm;
+            break;
+        }
+        build_root(F, fo, bk, u);
+        if (codeword_syndrome(F, u) == cfg.crc_const()) {
+            wnr = bk;
+            wpm = bm;
+            break;
         }
     }
-    const int wnr = bk;
-    const bool wok = __shfl_sync(FULL_MASK, ok, wnr & 31);
-    const int rw = P.lay.root_words;
-    if (P.path_cw) {
-        for (int kk = 0; kk < np; ++kk) build_root(F, fo, kk, P.path_cw + ((size_t)f * P.L + kk) * rw);
-        if (live) {
-            P.path_pm[(size_t)f * P.L + lane] = pmk;
-            P.path_crc[(size_t)f * P.L + lane] = ok;
-        }
+    const bool wok = wnr >= 0 && cfg.has_crc();
+    if (wnr < 0) {
+        wnr = first;
+        wpm = __shfl_sync(FULL_MASK, pmk, first & 31);
     }
     if (P.info_out) {
-        uint32_t *u = F.root();
-        build_root(F, fo, wnr, u);
-        polar_transform_words(u, P.N, lane);
-        uint8_t *out = P.info_out + (size_t)f * P.k;
-        for (int i = lane; i < P.k; i += 32) {
+        if (!wok) build_root(F, fo, wnr, u);  // the passing winner's codeword is already in u
+        polar_transform_words(u, cfg.N(), lane);
+        uint8_t *out = P.info_out + (size_t)f * cfg.k();
+        for (int i = lane; i < cfg.k(); i += 32) {
             const uint32_t pos = __ldg(P.info_pos + i);
             out[i] = (uint8_t)((u[pos >> 5] >> (pos & 31)) & 1u);
         }
     }
     if (lane == 0) {
         if (P.crc_ok) P.crc_ok[f] = wok;
-        if (P.pm_out) P.pm_out[f] = bm;
+        if (P.pm_out) P.pm_out[f] = wpm;
         if (P.paths_used) P.paths_used[f] = np;
     }
     __syncwarp();
@@ -1019,11 +1118,12 @@ __device__ __forceinline__ float ingest(float a) {
     return fminf(fmaxf(a, -1048576.f), 1048576.f);                             // clamp_llr (kernels.py:34-36)
 }
 
-template <typename T, int W, int PPW>
-__device__ __forceinline__ void load_channel(const Dec<T, W, PPW> &F, long long f) {
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ void load_channel(const Dec<T, W, PPW, CFG> &F, long long f) {
     const Params &P = F.P;
+    const CFG &cfg = F.cfg;
     T *ch = F.channel();
-    const int N = P.N, tid = threadIdx.x;
+    const int N = cfg.N(), tid = threadIdx.x & (32 * W - 1);
     if (P.in_type == PB_IN_I8) {
         const int8_t *src = reinterpret_cast<const int8_t *>(P.llr) + (size_t)f * N;
         for (int i = tid; i < N; i += 32 * W) ch[i] = (T)src[i];
@@ -1044,30 +1144,22 @@ __device__ __forceinline__ void load_channel(const Dec<T, W, PPW> &F, long long 
     }
 }
 
-template <typename T, int W, int PPW>
-__global__ void __launch_bounds__(32 * W, 1) k_decode(const __grid_constant__ Params P) {
-    unsigned char *gs = P.gscratch ? P.gscratch + (size_t)blockIdx.x * P.lay.gbytes : nullptr;
-    for (long long f = blockIdx.x; f < P.batch; f += gridDim.x) {
-        Dec<T, W, PPW> F(P, gs);
-        load_channel(F, f);
-        if (threadIdx.x == 0) {
-            F.pm(0)[0] = 0.0;
-            F.syn(0)[0] = 0u;
-        }
-        F.sync();
-        int np = 1;
-        const bool prof = P.op_cycles && blockIdx.x == 0 && f == 0 && threadIdx.x == 0;
-        long long phbuf[2] = {0, 0};
-        if (prof) F.ph = phbuf;
+// The op program interpreted from the schedule (runtime configuration).
+struct RtOps {
+    template <typename T, int W, int PPW, class CFG>
+    __device__ __forceinline__ static void run(Dec<T, W, PPW, CFG> &F, int &np, bool prof) {
+        const Params &P = F.P;
+        DOp onext = P.prog[0];
         for (int oi = 0; oi < P.n_ops; ++oi) {
             const long long t0 = prof ? clock64() : 0;
-            const DOp o = P.prog[oi];
+            const DOp o = onext;
+            if (oi + 1 < P.n_ops) onext = P.prog[oi + 1];
             switch (o.kind) {
                 case DK_F:
-                    fg_op<T, W, PPW, false>(F, o);
+                    fg_op<T, W, PPW, CFG, false>(F, o);
                     break;
                 case DK_G:
-                    fg_op<T, W, PPW, true>(F, o);
+                    fg_op<T, W, PPW, CFG, true>(F, o);
                     break;
                 case DK_NOP:
                     break;
@@ -1076,36 +1168,78 @@ __global__ void __launch_bounds__(32 * W, 1) k_decode(const __grid_constant__ Pa
                     np = o.pout;
                     break;
             }
-            __syncwarp();
+            if (P.lockstep)
+                __syncthreads();
+            else
+                __syncwarp();
             if (prof) {
-            const long long t1 = clock64();
-            P.op_cycles[oi * 4] = t1 - t0;
-            if (F.ph) {
-                P.op_cycles[oi * 4 + 1] = F.ph[0] - t0;
-                P.op_cycles[oi * 4 + 2] = F.ph[1] - F.ph[0];
-                P.op_cycles[oi * 4 + 3] = t1 - F.ph[1];
+                const long long t1 = clock64();
+                long long *oc = P.op_cycles + oi * 12;
+                oc[0] = t1 - t0;
+                oc[1] = t0;
+                for (int x = 0; x < 10; ++x) {
+                    oc[2 + x] = F.ph[x];
+                    F.ph[x] = 0;
+                }
             }
         }
-        }
+    }
+};
+
+// Persistent frame loop shared by the interpreted and the generated kernels.
+// A CTA holds P.fpc frames of W warps each; all of them step through the same
+// op program (the schedule is per code, not per frame), optionally with a
+// CTA barrier per op so the SM's warps fetch the same instructions.
+template <typename T, int W, int PPW, class CFG, class OPS>
+__device__ __forceinline__ void decode_frames(const Params &P, const CFG &cfg) {
+    const int grp = threadIdx.x / (32 * W);
+    const long long slot = (long long)blockIdx.x * P.fpc + grp;
+    unsigned char *gs = P.gscratch ? P.gscratch + (size_t)slot * cfg.gbytes() : nullptr;
+    unsigned char *sm = g_smem + (size_t)grp * cfg.smem_bytes();
+    const long long stride = (long long)gridDim.x * P.fpc;
+    for (long long f0 = (long long)blockIdx.x * P.fpc; f0 < P.batch; f0 += stride) {
+        // tail: idle slots decode the last frame again and write nothing
+        const long long f = f0 + grp < P.batch ? f0 + grp : P.batch - 1;
+        const bool own = f0 + grp < P.batch;
+        Dec<T, W, PPW, CFG> F(P, cfg, sm, gs);
+        load_channel(F, f);
+        if ((threadIdx.x & (32 * W - 1)) == 0) F.pm(0)[0] = 0.0;
         F.sync();
-        if (F.warp == 0) finalize(F, f, np);
+        int np = 1;
+        const bool prof = P.op_cycles && blockIdx.x == 0 && f == 0 && threadIdx.x == 0;
+        long long phbuf[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (prof) F.ph = phbuf;
+        OPS::run(F, np, prof);
         F.sync();
+        if (F.warp == 0 && own) finalize(F, f, np);
+        if (P.fpc > 1)
+            __syncthreads();
+        else
+            F.sync();
     }
 }
 
 template <typename T, int W, int PPW>
+__global__ void __launch_bounds__(256, 1) k_decode(const __grid_constant__ Params P) {
+    decode_frames<T, W, PPW, RtCfg, RtOps>(P, RtCfg{&P});
+}
+
+#ifndef __CUDACC_RTC__
+template <typename T, int W, int PPW>
 cudaError_t launch_t(const Params *p, int grid, size_t smem, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k_decode<T, W, PPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_decode<T, W, PPW><<<grid, 32 * W, smem, st>>>(*p);
+    k_decode<T, W, PPW><<<grid, 32 * W * p->fpc, smem, st>>>(*p);
     return cudaGetLastError();
 }
 template <typename T, int W, int PPW>
-cudaError_t occ_t(size_t smem, int *bps) {
+cudaError_t occ_t(size_t smem, int fpc, int *bps) {
     cudaError_t e = cudaFuncSetAttribute(k_decode<T, W, PPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_decode<T, W, PPW>, 32 * W, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_decode<T, W, PPW>, 32 * W * fpc, smem);
 }
+
+#endif
 
 }  // namespace pb
 

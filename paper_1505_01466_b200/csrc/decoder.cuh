@@ -1,7 +1,9 @@
 // decoder.cuh -- device program, layouts and launch parameters shared by the
 // host runtime (runtime.cu) and the decode kernels (decode_kernel.cu).
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <stdint.h>
+#endif
 
 namespace pb {
 
@@ -26,7 +28,6 @@ struct __align__(16) DOp {
     int8_t select;   // leaf: pin*ncand > L (a real 2L->L selection)
     int8_t vmode;    // how this op reads stage n-1 (VM_*), else VM_NONE
     int32_t off;     // leaf: first u index covered
-    uint32_t rep_syn;// Rep leaf: syndrome of the all-ones word
 };
 
 // Per-frame storage plan.  Offsets in bytes from the frame's shared-memory
@@ -42,13 +43,11 @@ struct FrameLayout {
     int b_off[kMaxLog];         // beta slot s (s <= n-1): L rows, uint32 words
     int b_stride[kMaxLog];      // row stride, words
     int pm_off;                 // double [2][L]    path metrics (double-buffered)
-    int syn_off;                // uint32 [2][L]    CRC syndromes
     int ia_off;                 // uint32 [2][idx_stride][L] alpha row per stage, 4 per word
     int ib_off;                 // uint32 [2][idx_stride][L] beta row per slot, 4 per word
     int idx_stride;             // words per path = ceil(n / 4)
     int cd_off;                 // double [2][L][8] candidate deltas (by leaf parity)
     int clrb_off;               // uint16 [2][L][4] least reliable positions
-    int chs_off;                // uint32 [2][L] hard-word syndrome
     int cflag_off;              // uint8 [2][L] parity / ones-first
     int asg_off;                // uint8 [2][L][2] survivor -> (source, cand)
     int hard_off;               // uint32 [2][L][hard_words] hard decisions
@@ -62,8 +61,7 @@ struct FrameLayout {
 struct Params {
     const DOp *prog;
     int n_ops;
-    const uint32_t *msyn;       // [N] leaf-local CRC syndrome rows
-    const uint32_t *msyn4;      // [N/4][16] nibble tables of msyn (XOR of a nibble's rows)
+    const uint32_t *xsyn4;      // [N/32][8][16] codeword-domain syndrome nibble tables
     const uint32_t *info_pos;   // [k] payload positions (u index)
     int N, n, k, L;
     int ppw;                    // paths per warp (rows per interleave block), power of two
@@ -83,6 +81,9 @@ struct Params {
     uint8_t *path_crc;          // [B][L]
     unsigned char *gscratch;    // [CTA slots][gbytes]
     long long *op_cycles;       // debug: per-op clock64 deltas of CTA 0's first frame, or null
+    int ablate;                 // timing experiments only (PB_ABLATE): skip parts, wrong results
+    int fpc;                    // frames per CTA (W warps each), decoded in op lockstep
+    int lockstep;               // CTA barrier after every op (keeps the frames' I-fetch shared)
     FrameLayout lay;
 };
 

@@ -7,7 +7,7 @@
 
 #define PB_SHAPE(tag, T, mode, W, P)                                                                         \
     extern "C" cudaError_t pb_launch_##tag(const pb::Params *p, int grid, size_t smem, cudaStream_t st); \
-    extern "C" cudaError_t pb_occ_##tag(size_t smem, int *bps);
+    extern "C" cudaError_t pb_occ_##tag(size_t smem, int fpc, int *bps);
 #include "shapes.def"
 #undef PB_SHAPE
 
@@ -28,9 +28,9 @@ extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps
     return cudaErrorInvalidValue;
 }
 
-extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, size_t smem, int *blocks_per_sm) {
+extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, size_t smem, int fpc, int *blocks_per_sm) {
 #define PB_SHAPE(tag, T, md, W, P) \
-    if (mode == md && warps == W && ppw == P) return pb_occ_##tag(smem, blocks_per_sm);
+    if (mode == md && warps == W && ppw == P) return pb_occ_##tag(smem, fpc, blocks_per_sm);
 #include "shapes.def"
 #undef PB_SHAPE
     return cudaErrorInvalidValue;

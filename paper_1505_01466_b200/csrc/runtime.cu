@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -24,7 +25,7 @@
 
 extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps, int ppw, int grid, size_t smem,
                                         cudaStream_t stream);
-extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, size_t smem, int *blocks_per_sm);
+extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, size_t smem, int fpc, int *blocks_per_sm);
 extern "C" int pb_shape_supported(int mode, int warps, int ppw);
 
 namespace {
@@ -85,8 +86,9 @@ struct pb_handle {
     pb::Params base{};
     std::vector<pb::DOp> prog;
     pb::DOp *d_prog = nullptr;
-    uint32_t *d_msyn = nullptr, *d_msyn4 = nullptr, *d_info = nullptr;
+    uint32_t *d_xsyn4 = nullptr, *d_info = nullptr;
     int grid = 0, blocks_per_sm = 0, sms = 0, warps = 1, ppw = 1;
+    int fpc = 1, lockstep = 0;  // frames per CTA, per-op CTA barrier
     size_t smem_frame = 0;
     unsigned char *d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -232,7 +234,6 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     }
 
     // ---- lower the schedule
-    std::vector<uint32_t> M = Hu;
     int P = 1, vstate = pb::VM_F, leaf_off = 0, final_op = -1, max_hard = 1;
     for (int i = 0; i < n_ops; ++i) {
         const pb_op &op = ops[i];
@@ -292,22 +293,6 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         final_op = (int)h->prog.size();
         h->prog.push_back(d);
     }
-    // leaf-local subset transform of the syndrome rows:
-    // M[o + j] = XOR_{i subset of j} Hu[o + i]  (u = beta G_m, G_m involution)
-    for (auto &d : h->prog) {
-        if (d.kind < pb::DK_R0 || d.kind > pb::DK_SPC) continue;
-        const int m = 1 << d.stage, o = d.off;
-        for (int hb = 1; hb < m; hb <<= 1)
-            for (int j = 0; j < m; ++j)
-                if (j & hb) M[o + j] ^= M[o + (j ^ hb)];
-    }
-    for (auto &d : h->prog) {
-        if (d.kind != pb::DK_REP && !(d.kind == pb::DK_R1 && d.stage == 0)) continue;
-        uint32_t s = 0;
-        for (int j = 0; j < (1 << d.stage); ++j) s ^= M[d.off + j];
-        d.rep_syn = s;
-    }
-
     // ---- storage plan
     const int es = mode == PB_MODE_F32 ? 4 : 1;
     // frame shape: W warps per frame, PPW (power of two) path slots per warp
@@ -335,8 +320,6 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     }
     lay.pm_off = off;
     off = align_up(off + 2 * L * 8, 16);
-    lay.syn_off = off;
-    off = align_up(off + 2 * L * 4, 16);
     lay.idx_stride = std::max(1, (n + 3) / 4);  // index words per path (4 stages per word)
     lay.ia_off = off;
     off = align_up(off + 2 * L * lay.idx_stride * 4, 16);
@@ -347,8 +330,6 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     off = align_up(off + nbuf * L * pb::kMaxCand * 8, 16);
     lay.clrb_off = off;
     off = align_up(off + nbuf * L * 4 * 2, 16);
-    lay.chs_off = off;
-    off = align_up(off + nbuf * L * 4, 16);
     lay.cflag_off = off;
     off = align_up(off + nbuf * L, 16);
     lay.asg_off = off;
@@ -390,43 +371,86 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     }
     h->smem_frame = lay.smem_bytes;
 
+    {
+        // host-side launch parameters (device pointers are filled in below)
+        pb::Params &pr = h->base;
+        pr.N = N;
+        pr.n = n;
+        pr.k = code->k;
+        pr.L = L;
+        pr.ppw = ppw;
+        pr.lppw = lppw;
+        pr.has_crc = w != 0;
+        pr.crc_const = crc_const;
+        pr.final_op = final_op;
+        pr.n_ops = (int)h->prog.size();
+        pr.fpc = 1;
+    }
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
         delete h;
         return cuda_fail(e, "cudaSetDevice");
     }
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
-    e = pb_occupancy(mode, h->warps, h->ppw, h->smem_frame, &h->blocks_per_sm);
+    e = pb_occupancy(mode, h->warps, h->ppw, h->smem_frame, 1, &h->blocks_per_sm);
     if (e != cudaSuccess || h->blocks_per_sm < 1) {
         delete h;
         return cuda_fail(e == cudaSuccess ? cudaErrorInvalidConfiguration : e, "occupancy");
+    }
+    // Every frame resident on an SM goes into one CTA (frames per CTA = frames
+    // per SM).  The frames run the same op program and start together, so the
+    // SM's warps stay close in the code and share instruction fetch; one CTA
+    // per frame lets them drift apart over the batch and thrash the I-cache
+    // (measured: no_instructions stalls 8.7% -> 16.5%, -25% throughput).
+    // PB_LOCKSTEP=1 adds a CTA barrier after every op (measured slower).
+    {
+        const int fpc_env = env_int("PB_FPC", 0);
+        int fpc = std::min(fpc_env > 0 ? fpc_env : h->blocks_per_sm, 8 / h->warps);  // 256-thread bound
+        while (fpc > 1 && (size_t)fpc * h->smem_frame > (size_t)smem_cap) --fpc;
+        int bps = 0;
+        while (fpc > 1) {
+            e = pb_occupancy(mode, h->warps, h->ppw, fpc * h->smem_frame, fpc, &bps);
+            if (e == cudaSuccess && bps >= 1) break;
+            --fpc;
+        }
+        if (fpc == 1) bps = h->blocks_per_sm;
+        h->fpc = fpc;
+        h->blocks_per_sm = bps;
+        h->lockstep = fpc > 1 ? env_int("PB_LOCKSTEP", 0) : 0;
     }
     h->grid = h->sms * h->blocks_per_sm;
 
     // ---- device tables
     if ((e = cudaMalloc(&h->d_prog, sizeof(pb::DOp) * h->prog.size())) != cudaSuccess ||
-        (e = cudaMalloc(&h->d_msyn, sizeof(uint32_t) * N)) != cudaSuccess ||
-        (e = cudaMalloc(&h->d_msyn4, sizeof(uint32_t) * 16 * std::max(1, N / 4))) != cudaSuccess ||
+        (e = cudaMalloc(&h->d_xsyn4, sizeof(uint32_t) * 128 * std::max(1, N / 32))) != cudaSuccess ||
         (e = cudaMalloc(&h->d_info, sizeof(uint32_t) * std::max(1, code->k))) != cudaSuccess) {
         pb_destroy(h);
         return cuda_fail(e, "cudaMalloc tables");
     }
     std::vector<uint32_t> info_k(info.begin(), info.begin() + code->k);
     cudaMemcpy(h->d_prog, h->prog.data(), sizeof(pb::DOp) * h->prog.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(h->d_msyn, M.data(), sizeof(uint32_t) * N, cudaMemcpyHostToDevice);
-    {
-        // nibble tables: T4[nb][v] = XOR of M[4 nb + j] over the set bits j of v
-        const int nnib = std::max(1, N / 4);
-        std::vector<uint32_t> T4((size_t)nnib * 16, 0u);
-        for (int nb = 0; nb < nnib; ++nb)
-            for (int v = 0; v < 16; ++v)
-                for (int j = 0; j < 4; ++j)
-                    if (((v >> j) & 1) && 4 * nb + j < N) T4[(size_t)nb * 16 + v] ^= M[4 * nb + j];
-        cudaMemcpy(h->d_msyn4, T4.data(), sizeof(uint32_t) * T4.size(), cudaMemcpyHostToDevice);
-    }
     cudaMemcpy(h->d_info, info_k.data(), sizeof(uint32_t) * code->k, cudaMemcpyHostToDevice);
+    {
+        // codeword-domain syndrome rows Hx[j] = XOR_{i subset of j} Hu[i]
+        // (x = u G_N, G_N[j][i] = 1 iff i subset of j), as nibble tables per
+        // 32-bit codeword word: T[w][nb][v] = XOR of Hx[32 w + 4 nb + b], b in v
+        std::vector<uint32_t> Hx = Hu;
+        for (int hb = 1; hb < N; hb <<= 1)
+            for (int j = 0; j < N; ++j)
+                if (j & hb) Hx[j] ^= Hx[j ^ hb];
+        const int nw = std::max(1, N / 32);
+        std::vector<uint32_t> T((size_t)nw * 128, 0u);
+        for (int wi = 0; wi < nw; ++wi)
+            for (int nb = 0; nb < 8; ++nb)
+                for (int v = 0; v < 16; ++v)
+                    for (int b = 0; b < 4; ++b) {
+                        const int j = 32 * wi + 4 * nb + b;
+                        if (((v >> b) & 1) && j < N) T[(size_t)wi * 128 + nb * 16 + v] ^= Hx[j];
+                    }
+        cudaMemcpy(h->d_xsyn4, T.data(), sizeof(uint32_t) * T.size(), cudaMemcpyHostToDevice);
+    }
     if (lay.gbytes) {
-        h->scratch_bytes = (size_t)h->grid * lay.gbytes;
+        h->scratch_bytes = (size_t)h->grid * h->fpc * lay.gbytes;
         if ((e = cudaMalloc(&h->d_scratch, h->scratch_bytes)) != cudaSuccess) {
             pb_destroy(h);
             return cuda_fail(e, "cudaMalloc scratch");
@@ -438,8 +462,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     pb::Params &pr = h->base;
     pr.prog = h->d_prog;
     pr.n_ops = (int)h->prog.size();
-    pr.msyn = h->d_msyn;
-    pr.msyn4 = h->d_msyn4;
+    pr.xsyn4 = h->d_xsyn4;
     pr.info_pos = h->d_info;
     pr.N = N;
     pr.n = n;
@@ -452,16 +475,19 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     pr.final_op = final_op;
     pr.gscratch = h->d_scratch;
     pr.op_cycles = nullptr;
+    pr.ablate = env_int("PB_ABLATE", 0);
+    pr.fpc = h->fpc;
+    pr.lockstep = h->lockstep;
 
     char buf[1024];
     snprintf(buf, sizeof buf,
              "{\"N\": %d, \"k\": %d, \"L\": %d, \"mode\": \"%s\", \"ops\": %d, \"device_ops\": %d, "
              "\"smem_per_frame\": %d, \"alpha_global_from_stage\": %d, \"global_scratch_per_frame\": %d, "
              "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": %d, \"warps_per_frame\": %d, "
-             "\"paths_per_warp\": %d}",
+             "\"paths_per_warp\": %d, \"frames_per_cta\": %d, \"lockstep\": %d}",
              N, code->k, L, mode == PB_MODE_F32 ? "f32" : "int8", n_ops, (int)h->prog.size(),
-             lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm, h->sms, h->grid, 32 * h->warps,
-             h->warps, h->ppw);
+             lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm * h->fpc, h->sms, h->grid,
+             32 * h->warps * h->fpc, h->warps, h->ppw, h->fpc, h->lockstep);
     h->plan_json = buf;
     *out = h;
     return PB_OK;
@@ -470,8 +496,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
 int pb_destroy(pb_handle *h) {
     if (!h) return PB_OK;
     cudaFree(h->d_prog);
-    cudaFree(h->d_msyn);
-    cudaFree(h->d_msyn4);
+    cudaFree(h->d_xsyn4);
     cudaFree(h->d_info);
     cudaFree(h->d_scratch);
     cudaFree(h->d_in);
@@ -511,10 +536,10 @@ int ensure(void **p, size_t *cap, size_t need) {
 }
 
 int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
-    int grid = (int)std::min<long long>(h->grid, pr.batch);
+    int grid = (int)std::min<long long>(h->grid, (pr.batch + h->fpc - 1) / h->fpc);
     if (grid < 1) return PB_OK;
     PB_CUDA(cudaEventRecord(h->ev0, st));
-    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, grid, h->smem_frame, st);
+    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, grid, h->smem_frame * h->fpc, st);
     if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
     PB_CUDA(cudaEventRecord(h->ev1, st));
     h->timed = true;
@@ -523,6 +548,7 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
 }
 
 }  // namespace
+
 
 extern "C" int pb_decode(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *info_out,
                          uint8_t *crc_ok, double *pm_out, int32_t *paths_used, void *stream) {
@@ -601,8 +627,8 @@ extern "C" int pb_profile_ops(pb_handle *h, const void *llr, int in_type, int64_
     int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
     if (rc) return rc;
     long long *d_cyc = nullptr;
-    PB_CUDA(cudaMalloc(&d_cyc, sizeof(long long) * 4 * h->prog.size()));
-    PB_CUDA(cudaMemset(d_cyc, 0, sizeof(long long) * 4 * h->prog.size()));
+    PB_CUDA(cudaMalloc(&d_cyc, sizeof(long long) * 12 * h->prog.size()));
+    PB_CUDA(cudaMemset(d_cyc, 0, sizeof(long long) * 12 * h->prog.size()));
     PB_CUDA(cudaMemcpy(h->d_in, llr, in_bytes, cudaMemcpyHostToDevice));
     pb::Params pr = h->base;
     pr.llr = h->d_in;
@@ -617,7 +643,7 @@ extern "C" int pb_profile_ops(pb_handle *h, const void *llr, int in_type, int64_
     rc = launch(h, pr, 0);
     if (rc) return rc;
     PB_CUDA(cudaDeviceSynchronize());
-    PB_CUDA(cudaMemcpy(cycles, d_cyc, sizeof(long long) * 4 * h->prog.size(), cudaMemcpyDeviceToHost));
+    PB_CUDA(cudaMemcpy(cycles, d_cyc, sizeof(long long) * 12 * h->prog.size(), cudaMemcpyDeviceToHost));
     cudaFree(d_cyc);
     for (size_t i = 0; i < h->prog.size(); ++i) {
         if (kinds) kinds[i] = h->prog[i].kind;

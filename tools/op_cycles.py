@@ -17,9 +17,12 @@ lib.pb_profile_ops.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, c
 n = lib.pb_device_op_count(dec._h)
 fb = pb.generate_frames(spec, ebn0, seed=1, start=0, count=4096)
 llr = np.ascontiguousarray(fb.llrs)
-cyc4 = np.zeros((n, 4), np.int64); kinds = np.zeros(n, np.int8); stages = np.zeros(n, np.int8)
+cyc4 = np.zeros((n, 12), np.int64); kinds = np.zeros(n, np.int8); stages = np.zeros(n, np.int8)
 rc = lib.pb_profile_ops(dec._h, llr.ctypes.data, 0, len(llr), cyc4.ctypes.data, kinds.ctypes.data, stages.ctypes.data)
 _native.check(rc, 'pb_profile_ops')
+import os
+if os.environ.get('OPC_STRIDE') == '4':  # older builds: 4 longs per op
+    cyc4 = np.concatenate([cyc4.ravel()[:4 * n].reshape(n, 4), np.zeros((n, 8), np.int64)], 1)
 cyc = cyc4[:, 0]
 names = {0: 'F', 1: 'G', 2: 'R0', 3: 'REP', 4: 'R1', 5: 'SPC', 6: 'NOP'}
 tot = cyc.sum()
@@ -33,8 +36,20 @@ print(' '.join(f'{k}={v/tot*100:.1f}%' for k, v in sorted(byk.items(), key=lambd
 for (k, s), (cnt, c) in sorted(agg.items(), key=lambda t: -t[1][1])[:25]:
     print(f'{k:4s} stage {s:2d}: {cnt:4d} ops  {c:9d} cycles  {c/cnt:8.0f}/op  {c/tot*100:5.1f}%')
 
-print('leaf phases (A scan / B select / C materialise) mean cycles:')
+
+# marks: 0 A end, 1 B end, 2 scan loop end, 4 B keys+sort, 5 B merge, 6 B counting, 7 C copies
+t0 = cyc4[:, 1]
+def rel(col):
+    v = cyc4[:, 2 + col]
+    return np.where(v > 0, v - t0, 0)
+marks = {m: rel(m) for m in range(10)}
+print('leaf timeline (mean cycles since op start): scanloop A_end keys merge count B_end C_copies end')
 for kk in (2, 3, 4, 5):
     sel = kinds == kk
-    if sel.any():
-        print(f'  {names[kk]:4s} n={int(sel.sum()):3d}  A {cyc4[sel,1].mean():7.0f}  B {cyc4[sel,2].mean():7.0f}  C {cyc4[sel,3].mean():7.0f}  total {cyc4[sel,0].mean():7.0f}')
+    if not sel.any():
+        continue
+    def mm(m):
+        v = marks[m][sel]
+        v = v[v > 0]
+        return f"{v.mean():7.0f}" if v.size else "      -"
+    print(f'  {names[kk]:4s} n={int(sel.sum()):3d} ' + ' '.join(mm(m) for m in (2, 0, 4, 5, 6, 1, 7)) + f' {cyc4[sel,0].mean():7.0f}')
