@@ -63,11 +63,16 @@ def _stale(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, jobs: int | None = None) -> str:
+def build(verbose: bool = False, jobs: int | None = None, profile: bool = False) -> str:
     """Compile the CUDA sources in-tree for sm_100a (nvcc cross-compiles
     without a GPU): one object per kernel shape (compiled in parallel), the
-    dispatcher and the host runtime, linked into one shared library."""
+    dispatcher and the host runtime, linked into one shared library.
+    ``profile`` builds the instrumented variant (per-op clock64 marks,
+    PB_ABLATE) into libpolar_b200_prof.so for tools/op_cycles.py."""
     from concurrent.futures import ThreadPoolExecutor
+    BUILD_DIR = os.path.join(LIB_DIR, "obj_prof" if profile else "obj")
+    NVCC_FLAGS = globals()["NVCC_FLAGS"] + (["-DPB_PROFILE=1"] if profile else [])
+    LIB_PATH = os.path.join(LIB_DIR, "libpolar_b200_prof.so") if profile else globals()["LIB_PATH"]
     os.makedirs(BUILD_DIR, exist_ok=True)
     hdrs = [os.path.join(CSRC, f) for f in ("decode_kernel.cuh", "decoder.cuh", "shapes.def")]
     hdrs.append(os.path.join(INCLUDE, "polar_b200.h"))

@@ -47,6 +47,13 @@ typedef unsigned long long uint64_t;
 
 #include "decoder.cuh"
 
+// Profiling build (-DPB_PROFILE=1, tools/op_cycles.py, PB_ABLATE): per-op
+// clock64 phase marks and ablation switches; compiled out otherwise.
+#ifndef PB_PROFILE
+#define PB_PROFILE 0
+#endif
+#define PB_ABL(P, bit) (PB_PROFILE && ((P).ablate & (bit)))
+
 #define PB_IN_F32 0
 #define PB_IN_I8 1
 
@@ -184,7 +191,7 @@ struct Dec {
         : P(p), cfg(c), sm(s), gs(g), lane(threadIdx.x & 31), warp((threadIdx.x >> 5) & (W - 1)), cur(0), par(0),
           lpar(0), ph(nullptr) {}
     __device__ __forceinline__ void mark(int i) const {
-        if (ph && lane == 0) ph[i] = clock64();
+        if (PB_PROFILE && ph && lane == 0) ph[i] = clock64();
     }
 
     // row r, element 0 of a block-interleaved stage s
@@ -227,9 +234,10 @@ struct Dec {
     }
     __device__ __forceinline__ uint32_t *root() const { return reinterpret_cast<uint32_t *>(sm + cfg.root_off()); }
 
+    // the frame's W warps (named barrier per frame slot; the CTA may hold several frames)
     __device__ __forceinline__ void sync() const {
         if (W > 1)
-            __syncthreads();
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / (32 * W))), "r"(32 * W) : "memory");
         else
             __syncwarp();
     }
@@ -324,7 +332,7 @@ __device__ __forceinline__ void fg_to_dst(const Dec<T, W, PPW, CFG> &F, const S 
 template <typename T, int W, int PPW, class CFG, bool IS_G>
 __device__ __forceinline__ void fg_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
     const auto mp = F.map(o.pin);
-    if (!mp.active || (F.P.ablate & 8)) return;
+    if (!mp.active || PB_ABL(F.P, 8)) return;
     const Params &P = F.P;
     const CFG &cfg = F.cfg;
     const int s = o.stage, h = 1 << (s - 1), q = mp.q;
@@ -927,7 +935,7 @@ __device__ __forceinline__ void leaf_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
     if (kind == DK_R1 && o.stage == 0) kind = DK_REP;  // listdec.py:347
 
     // Phase A: per-source sums / scans, this warp's sources
-    if (!(P.ablate & 1)) {
+    if (!PB_ABL(P, 1)) {
         const auto mp = F.map(o.pin);
         leaf_read(F, o, kind, mp.q, mp.active, mp.G, mp.sub);
     }
@@ -936,8 +944,8 @@ __device__ __forceinline__ void leaf_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
 
     const bool fork = kind != DK_R0;
     if (fork) {
-        if (F.warp == 0 && !(P.ablate & 2)) select_phase(F, o);
-        if (F.warp == 0 && (P.ablate & 2) && F.lane < o.pout) {  // timing only: a valid dummy choice
+        if (F.warp == 0 && !PB_ABL(P, 2)) select_phase(F, o);
+        if (F.warp == 0 && PB_ABL(P, 2) && F.lane < o.pout) {  // timing only: a valid dummy choice
             F.asg(F.par)[2 * F.lane] = (uint8_t)(F.lane % o.pin);
             F.asg(F.par)[2 * F.lane + 1] = 0;
         }
@@ -964,7 +972,7 @@ __device__ __forceinline__ void leaf_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
     }
     F.mark(7);
     const int sE = o.target;
-    if (sE < cfg.n() && !(P.ablate & 4)) {
+    if (sE < cfg.n() && !PB_ABL(P, 4)) {
         word_and_chain(F, b, o, kind, mp.active, mp.G, mp.sub, p, c, F.cur, mp.active ? p : 0, F.beta_row(sE, k), sE);
         if (mp.active && mp.sub == 0) F.ib(nxt, sE, k) = (uint8_t)k;
     }
@@ -1076,7 +1084,7 @@ __device__ __forceinline__ void finalize(Dec<T, W, PPW, CFG> &F, long long f, in
         }
         if (first < 0) first = bk;
         tried |= 1u << bk;
-        if (!cfg.has_crc() || (P.ablate & 16)) {
+        if (!cfg.has_crc() || PB_ABL(P, 16)) {
             wnr = bk;
             wpm = bm;
             break;
@@ -1168,10 +1176,7 @@ struct RtOps {
                     np = o.pout;
                     break;
             }
-            if (P.lockstep)
-                __syncthreads();
-            else
-                __syncwarp();
+            __syncwarp();
             if (prof) {
                 const long long t1 = clock64();
                 long long *oc = P.op_cycles + oi * 12;
@@ -1186,10 +1191,9 @@ struct RtOps {
     }
 };
 
-// Persistent frame loop shared by the interpreted and the generated kernels.
-// A CTA holds P.fpc frames of W warps each; all of them step through the same
-// op program (the schedule is per code, not per frame), optionally with a
-// CTA barrier per op so the SM's warps fetch the same instructions.
+// Persistent frame loop.  A CTA holds P.fpc frames of W warps each; all of
+// them step through the same op program (the schedule is per code, not per
+// frame) and start together, so the SM's warps share instruction fetch.
 template <typename T, int W, int PPW, class CFG, class OPS>
 __device__ __forceinline__ void decode_frames(const Params &P, const CFG &cfg) {
     const int grp = threadIdx.x / (32 * W);
@@ -1206,7 +1210,7 @@ __device__ __forceinline__ void decode_frames(const Params &P, const CFG &cfg) {
         if ((threadIdx.x & (32 * W - 1)) == 0) F.pm(0)[0] = 0.0;
         F.sync();
         int np = 1;
-        const bool prof = P.op_cycles && blockIdx.x == 0 && f == 0 && threadIdx.x == 0;
+        const bool prof = PB_PROFILE && P.op_cycles && blockIdx.x == 0 && f == 0 && threadIdx.x == 0;
         long long phbuf[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         if (prof) F.ph = phbuf;
         OPS::run(F, np, prof);

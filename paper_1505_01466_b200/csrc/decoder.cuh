@@ -82,8 +82,7 @@ struct Params {
     unsigned char *gscratch;    // [CTA slots][gbytes]
     long long *op_cycles;       // debug: per-op clock64 deltas of CTA 0's first frame, or null
     int ablate;                 // timing experiments only (PB_ABLATE): skip parts, wrong results
-    int fpc;                    // frames per CTA (W warps each), decoded in op lockstep
-    int lockstep;               // CTA barrier after every op (keeps the frames' I-fetch shared)
+    int fpc;                    // frames per CTA (W warps each)
     FrameLayout lay;
 };
 

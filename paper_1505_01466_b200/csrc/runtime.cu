@@ -23,6 +23,10 @@
 #include "../../include/polar_b200.h"
 #include "decoder.cuh"
 
+#ifndef PB_PROFILE
+#define PB_PROFILE 0
+#endif
+
 extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps, int ppw, int grid, size_t smem,
                                         cudaStream_t stream);
 extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, size_t smem, int fpc, int *blocks_per_sm);
@@ -88,7 +92,7 @@ struct pb_handle {
     pb::DOp *d_prog = nullptr;
     uint32_t *d_xsyn4 = nullptr, *d_info = nullptr;
     int grid = 0, blocks_per_sm = 0, sms = 0, warps = 1, ppw = 1;
-    int fpc = 1, lockstep = 0;  // frames per CTA, per-op CTA barrier
+    int fpc = 1;  // frames per CTA
     size_t smem_frame = 0;
     unsigned char *d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -342,7 +346,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     off = align_up(off + lay.root_words * 4, 16);
 
     const int smem_cap = 227 * 1024;
-    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", mode == PB_MODE_F32 ? 3 : 4));
+    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", mode == PB_MODE_F32 ? 3 : 8));
     const int budget = std::max(off, env_int("PB_SMEM_BUDGET", smem_cap / target_fps - 1024));
     // alpha stages s = 0 .. n-2 (n-1 is recomputed), lowest stages first into
     // shared memory, the rest into per-CTA global scratch (L2-resident)
@@ -402,7 +406,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     // SM's warps stay close in the code and share instruction fetch; one CTA
     // per frame lets them drift apart over the batch and thrash the I-cache
     // (measured: no_instructions stalls 8.7% -> 16.5%, -25% throughput).
-    // PB_LOCKSTEP=1 adds a CTA barrier after every op (measured slower).
+    // (A CTA barrier after every op to force lockstep measured slower.)
     {
         const int fpc_env = env_int("PB_FPC", 0);
         int fpc = std::min(fpc_env > 0 ? fpc_env : h->blocks_per_sm, 8 / h->warps);  // 256-thread bound
@@ -416,7 +420,6 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         if (fpc == 1) bps = h->blocks_per_sm;
         h->fpc = fpc;
         h->blocks_per_sm = bps;
-        h->lockstep = fpc > 1 ? env_int("PB_LOCKSTEP", 0) : 0;
     }
     h->grid = h->sms * h->blocks_per_sm;
 
@@ -477,17 +480,16 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     pr.op_cycles = nullptr;
     pr.ablate = env_int("PB_ABLATE", 0);
     pr.fpc = h->fpc;
-    pr.lockstep = h->lockstep;
 
     char buf[1024];
     snprintf(buf, sizeof buf,
              "{\"N\": %d, \"k\": %d, \"L\": %d, \"mode\": \"%s\", \"ops\": %d, \"device_ops\": %d, "
              "\"smem_per_frame\": %d, \"alpha_global_from_stage\": %d, \"global_scratch_per_frame\": %d, "
              "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": %d, \"warps_per_frame\": %d, "
-             "\"paths_per_warp\": %d, \"frames_per_cta\": %d, \"lockstep\": %d}",
+             "\"paths_per_warp\": %d, \"frames_per_cta\": %d}",
              N, code->k, L, mode == PB_MODE_F32 ? "f32" : "int8", n_ops, (int)h->prog.size(),
              lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm * h->fpc, h->sms, h->grid,
-             32 * h->warps * h->fpc, h->warps, h->ppw, h->fpc, h->lockstep);
+             32 * h->warps * h->fpc, h->warps, h->ppw, h->fpc);
     h->plan_json = buf;
     *out = h;
     return PB_OK;
@@ -622,6 +624,10 @@ extern "C" int pb_device_op_count(pb_handle *h) { return h ? (int)h->prog.size()
 extern "C" int pb_profile_ops(pb_handle *h, const void *llr, int in_type, int64_t batch, long long *cycles,
                               int8_t *kinds, int8_t *stages) {
     if (!h || !llr || !cycles) return fail(PB_EINVAL, "null argument");
+#if !PB_PROFILE
+    (void)in_type, (void)batch, (void)kinds, (void)stages;
+    return fail(PB_EINVAL, "per-op profile needs the profiling build (_native.build(profile=True))");
+#endif
     PB_CUDA(cudaSetDevice(h->device));
     const size_t in_bytes = (size_t)batch * h->N * (in_type == PB_IN_F32 ? 4 : 1);
     int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);

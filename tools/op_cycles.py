@@ -1,7 +1,9 @@
 """Dev helper: per-op cycle profile of one frame (CTA 0, clock64)."""
-import ctypes, sys, collections
+import ctypes, os, sys, collections
 import numpy as np
 sys.path.insert(0, '.')
+# needs the instrumented build: _native.build(profile=True)
+os.environ.setdefault('PB_LIB_PATH', 'paper_1505_01466_b200/_lib/libpolar_b200_prof.so')
 import paper_1505_01466_b200 as pb
 from paper_1505_01466_b200 import _native
 import bench
@@ -20,7 +22,6 @@ llr = np.ascontiguousarray(fb.llrs)
 cyc4 = np.zeros((n, 12), np.int64); kinds = np.zeros(n, np.int8); stages = np.zeros(n, np.int8)
 rc = lib.pb_profile_ops(dec._h, llr.ctypes.data, 0, len(llr), cyc4.ctypes.data, kinds.ctypes.data, stages.ctypes.data)
 _native.check(rc, 'pb_profile_ops')
-import os
 if os.environ.get('OPC_STRIDE') == '4':  # older builds: 4 longs per op
     cyc4 = np.concatenate([cyc4.ravel()[:4 * n].reshape(n, 4), np.zeros((n, 8), np.int64)], 1)
 cyc = cyc4[:, 0]
@@ -44,12 +45,13 @@ def rel(col):
     return np.where(v > 0, v - t0, 0)
 marks = {m: rel(m) for m in range(10)}
 print('leaf timeline (mean cycles since op start): scanloop A_end keys merge count B_end C_copies end')
-for kk in (2, 3, 4, 5):
-    sel = kinds == kk
+groups = [(kk, None) for kk in (2, 3, 4, 5)] + sorted({(int(k), int(st)) for k, st in zip(kinds, stages) if 2 <= k <= 5})
+for kk, sg in groups:
+    sel = (kinds == kk) & ((stages == sg) if sg is not None else True)
     if not sel.any():
         continue
     def mm(m):
         v = marks[m][sel]
         v = v[v > 0]
         return f"{v.mean():7.0f}" if v.size else "      -"
-    print(f'  {names[kk]:4s} n={int(sel.sum()):3d} ' + ' '.join(mm(m) for m in (2, 0, 4, 5, 6, 1, 7)) + f' {cyc4[sel,0].mean():7.0f}')
+    print(f'  {names[kk]:4s}{"" if sg is None else sg:>3} n={int(sel.sum()):3d} ' + ' '.join(mm(m) for m in (2, 0, 4, 5, 6, 1, 7)) + f' {cyc4[sel,0].mean():7.0f}')
