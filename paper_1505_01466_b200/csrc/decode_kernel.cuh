@@ -404,16 +404,19 @@ __device__ __forceinline__ void pw_sums(const S &src, int m, bool active, int su
     float carry[NS];
     for (int b = 0; b < nb; ++b) {
         float acc[NA][NS];
+        // the NA column chains are independent: interleave them (ILP)
+        const int base = b * blk + sub;
+        if (act) {
 #pragma unroll
-        for (int a = 0; a < NA; ++a) {
-            const int base = b * blk + sub + a * GS;
-            if (act) {
-                acc_init<NS>(acc[a], src.get(base));
-                for (int r = 1; r < per; ++r) acc_add<NS>(acc[a], src.get(base + 8 * r));
-            } else {
+            for (int a = 0; a < NA; ++a) acc_init<NS>(acc[a], src.get(base + a * GS));
+            for (int r = 1; r < per; ++r)
+#pragma unroll
+                for (int a = 0; a < NA; ++a) acc_add<NS>(acc[a], src.get(base + a * GS + 8 * r));
+        } else {
+#pragma unroll
+            for (int a = 0; a < NA; ++a)
 #pragma unroll
                 for (int t = 0; t < NS; ++t) acc[a][t] = 0.f;
-            }
         }
         // levels 0..2 of the column tree: lane bits shuffle, register bits add
 #pragma unroll

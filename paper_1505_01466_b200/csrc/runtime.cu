@@ -396,6 +396,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         return cuda_fail(e, "cudaSetDevice");
     }
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+    if (env_int("PB_GRID_SMS", 0) > 0) h->sms = std::min(h->sms, env_int("PB_GRID_SMS", 0));  // experiments
     e = pb_occupancy(mode, h->warps, h->ppw, h->smem_frame, 1, &h->blocks_per_sm);
     if (e != cudaSuccess || h->blocks_per_sm < 1) {
         delete h;
