@@ -284,10 +284,10 @@ __device__ __forceinline__ void fg_loop(const S &src, const D &dst, const uint32
 // Steady state (G = GC lanes per path, compile-time) with h >= 32: 32-element
 // chunks, the lane's elements of a chunk in unrolled blocks of U whose loads
 // all issue before the stores (immediate offsets, beta word loaded once).
-template <typename T, bool IS_G, int GC, int PPW, class S>
+template <typename T, bool IS_G, int GC, int PPW, int UMAX, class S>
 __device__ __forceinline__ void fg_chunks(const S &src, T *dst, const uint32_t *bw, int h, int sub) {
-    constexpr int PER = 32 / GC;            // this lane's elements per chunk
-    constexpr int U = PER < 8 ? PER : 8;    // unrolled block
+    constexpr int PER = 32 / GC;              // this lane's elements per chunk
+    constexpr int U = PER < UMAX ? PER : UMAX;  // unrolled block (loads in flight)
     for (int c0 = 0; c0 < h; c0 += 32) {
         const uint32_t wsh = IS_G ? (bw[c0 >> 5] >> sub) : 0u;
         T *d = dst + (c0 + sub) * PPW;
@@ -309,21 +309,23 @@ __device__ __forceinline__ void fg_chunks(const S &src, T *dst, const uint32_t *
     }
 }
 
-template <typename T, int W, int PPW, class CFG, bool IS_G, class S>
+// SRC_GL: the source rows are in global scratch (L2 latency: more loads in flight)
+template <typename T, int W, int PPW, class CFG, bool IS_G, bool SRC_GL = false, class S>
 __device__ __forceinline__ void fg_to_dst(const Dec<T, W, PPW, CFG> &F, const S &src, int s, int q, const uint32_t *bw,
                                           int h, int G, int sub) {
     constexpr int GS = Dec<T, W, PPW, CFG>::GSS;
+    constexpr int UM = SRC_GL ? 32 : 8;
     const int off = F.rowoff(s - 1, q);
     if (s - 1 < F.cfg.a_gfrom()) {
         T *d = F.a_sm(s - 1) + off;
         if (G == GS && h >= 32)
-            fg_chunks<T, IS_G, GS, PPW>(src, d, bw, h, sub);
+            fg_chunks<T, IS_G, GS, PPW, UM>(src, d, bw, h, sub);
         else
             fg_loop<T, IS_G, 0>(src, RowDst<T, PPW>{d}, bw, h, G, sub);
     } else {
         T *d = F.a_gl(s - 1) + off;
         if (G == GS && h >= 32)
-            fg_chunks<T, IS_G, GS, PPW>(src, d, bw, h, sub);
+            fg_chunks<T, IS_G, GS, PPW, UM>(src, d, bw, h, sub);
         else
             fg_loop<T, IS_G, 0>(src, RowDst<T, PPW>{d}, bw, h, G, sub);
     }
@@ -349,7 +351,7 @@ __device__ __forceinline__ void fg_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
         if (s < cfg.a_gfrom())
             fg_to_dst<T, W, PPW, CFG, IS_G>(F, RowSrc<T, PPW>{F.a_sm(s) + off}, s, q, bw, h, mp.G, mp.sub);
         else
-            fg_to_dst<T, W, PPW, CFG, IS_G>(F, RowSrc<T, PPW>{F.a_gl(s) + off}, s, q, bw, h, mp.G, mp.sub);
+            fg_to_dst<T, W, PPW, CFG, IS_G, true>(F, RowSrc<T, PPW>{F.a_gl(s) + off}, s, q, bw, h, mp.G, mp.sub);
     }
     if (mp.sub == 0) F.ia(F.cur, s - 1, q) = (uint8_t)q;
 }
@@ -792,7 +794,22 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW, CFG> &F, const DOp &o, 
     tk.init();
     int par = 0;
     if (Gl == 1) {
-        if (active && sub == 0) {
+        if (active && sub == 0 && m >= 32) {
+            // whole 32-element blocks: all loads in flight before the serial scan
+            for (int w0 = 0; w0 < m; w0 += 32) {
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = src.get(w0 + j);
+                uint32_t word = 0u;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    word |= (v[j] < 0.f ? 1u : 0u) << j;
+                    tk.push_scan(fabsf(v[j]), w0 + j);
+                }
+                F.hard(F.par, w0 >> 5, q) = word;
+                par ^= __popc(word);
+            }
+        } else if (active && sub == 0) {
             for (int w0 = 0; w0 < m; w0 += 32) {
                 const int cnt = m - w0 < 32 ? m - w0 : 32;
                 uint32_t word = 0u;
