@@ -44,15 +44,16 @@ class PbOp(ctypes.Structure):
                 ("side", ctypes.c_int32), ("spc_truncated", ctypes.c_int32)]
 
 
-def shapes() -> list[tuple[str, str, int, int, int]]:
-    """(tag, element type, mode, warps per frame, paths per warp) from csrc/shapes.def."""
+def shapes() -> list[tuple[str, str, int, int, int, int]]:
+    """(tag, element type, mode, warps per frame, paths per warp, channel in
+    global) from csrc/shapes.def."""
     out = []
     with open(os.path.join(CSRC, "shapes.def")) as fh:
         for line in fh:
             line = line.strip()
             if line.startswith("PB_SHAPE("):
-                tag, t, mode, w, ppw = [x.strip() for x in line[9:-1].split(",")]
-                out.append((tag, t, int(mode), int(w), int(ppw)))
+                tag, t, mode, w, ppw, chg = [x.strip() for x in line[9:-1].split(",")]
+                out.append((tag, t, int(mode), int(w), int(ppw), int(chg)))
     return out
 
 
@@ -71,8 +72,12 @@ def build(verbose: bool = False, jobs: int | None = None, profile: bool = False)
     PB_ABLATE) into libpolar_b200_prof.so for tools/op_cycles.py."""
     from concurrent.futures import ThreadPoolExecutor
     BUILD_DIR = os.path.join(LIB_DIR, "obj_prof" if profile else "obj")
-    NVCC_FLAGS = globals()["NVCC_FLAGS"] + (["-DPB_PROFILE=1"] if profile else [])
+    NVCC_FLAGS = globals()["NVCC_FLAGS"] + (["-DPB_PROFILE=1"] if profile else []) + \
+        [f for f in os.environ.get("PB_NVCC_DEFS", "").split() if f.startswith("-D")]  # experiments
     LIB_PATH = os.path.join(LIB_DIR, "libpolar_b200_prof.so") if profile else globals()["LIB_PATH"]
+    if os.environ.get("PB_NVCC_DEFS"):
+        import hashlib
+        BUILD_DIR += "_" + hashlib.sha1(os.environ["PB_NVCC_DEFS"].encode()).hexdigest()[:8]
     os.makedirs(BUILD_DIR, exist_ok=True)
     hdrs = [os.path.join(CSRC, f) for f in ("decode_kernel.cuh", "decoder.cuh", "shapes.def")]
     hdrs.append(os.path.join(INCLUDE, "polar_b200.h"))
@@ -80,12 +85,12 @@ def build(verbose: bool = False, jobs: int | None = None, profile: bool = False)
     cmds = []
     objs = []
     inst = os.path.join(CSRC, "decode_inst.cu")
-    for tag, t, mode, w, ppw in shapes():
+    for tag, t, mode, w, ppw, chg in shapes():
         obj = os.path.join(BUILD_DIR, f"decode_{tag}.o")
         objs.append(obj)
         if _stale(obj, [inst, *hdrs]):
             cmds.append(["nvcc", *NVCC_FLAGS, *extra, "-I", INCLUDE, f"-DPB_T={t}", f"-DPB_W={w}",
-                         f"-DPB_PPW={ppw}", f"-DPB_TAG={tag}", "-c", inst, "-o", obj])
+                         f"-DPB_PPW={ppw}", f"-DPB_CHG={chg}", f"-DPB_TAG={tag}", "-c", inst, "-o", obj])
     for src in ("dispatch.cu", "runtime.cu"):
         obj = os.path.join(BUILD_DIR, src.replace(".cu", ".o"))
         objs.append(obj)

@@ -138,10 +138,11 @@ struct ChanSrc {
 };
 
 // ------------------------------------------------------- configuration
-// Code / layout constants.  RtCfg reads them from the launch parameters
-// (the interpreted kernel); generated kernels supply a type with the same
-// members returning literals, so every address folds at compile time.
+// Code / layout constants, read from the launch parameters; where the
+// channel lives (shared memory or global scratch) is compile-time.
+template <bool CHG>
 struct RtCfg {
+    static constexpr bool kChGlobal = CHG;  // channel in global scratch
     const Params *p;
     __device__ __forceinline__ int N() const { return p->N; }
     __device__ __forceinline__ int n() const { return p->n; }
@@ -172,7 +173,7 @@ struct RtCfg {
 
 // ------------------------------------------------------- frame state
 
-template <typename T, int W, int PPW, class CFG = RtCfg>
+template <typename T, int W, int PPW, class CFG>
 struct Dec {
     static constexpr int LP = ilog2(PPW);
     static constexpr int GSS = 32 / PPW;           // steady-state lanes per path
@@ -201,7 +202,9 @@ struct Dec {
     __device__ __forceinline__ uint32_t *beta_row(int s, int row) const {
         return reinterpret_cast<uint32_t *>(sm + cfg.b_off(s)) + row * cfg.b_stride(s);
     }
-    __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(sm + cfg.ch_off()); }
+    __device__ __forceinline__ T *channel() const {
+        return reinterpret_cast<T *>((CFG::kChGlobal ? gs : sm) + cfg.ch_off());
+    }
     __device__ __forceinline__ double *pm(int b) const {
         return reinterpret_cast<double *>(sm + cfg.pm_off()) + b * cfg.L();
     }
@@ -1243,24 +1246,26 @@ __device__ __forceinline__ void decode_frames(const Params &P, const CFG &cfg) {
     }
 }
 
-template <typename T, int W, int PPW>
+template <typename T, int W, int PPW, bool CHG>
 __global__ void __launch_bounds__(256, 1) k_decode(const __grid_constant__ Params P) {
-    decode_frames<T, W, PPW, RtCfg, RtOps>(P, RtCfg{&P});
+    decode_frames<T, W, PPW, RtCfg<CHG>, RtOps>(P, RtCfg<CHG>{&P});
 }
 
 #ifndef __CUDACC_RTC__
-template <typename T, int W, int PPW>
+template <typename T, int W, int PPW, bool CHG>
 cudaError_t launch_t(const Params *p, int grid, size_t smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_decode<T, W, PPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_decode<T, W, PPW, CHG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_decode<T, W, PPW><<<grid, 32 * W * p->fpc, smem, st>>>(*p);
+    k_decode<T, W, PPW, CHG><<<grid, 32 * W * p->fpc, smem, st>>>(*p);
     return cudaGetLastError();
 }
-template <typename T, int W, int PPW>
+template <typename T, int W, int PPW, bool CHG>
 cudaError_t occ_t(size_t smem, int fpc, int *bps) {
-    cudaError_t e = cudaFuncSetAttribute(k_decode<T, W, PPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_decode<T, W, PPW, CHG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_decode<T, W, PPW>, 32 * W * fpc, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_decode<T, W, PPW, CHG>, 32 * W * fpc, smem);
 }
 
 #endif

@@ -27,10 +27,10 @@
 #define PB_PROFILE 0
 #endif
 
-extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps, int ppw, int grid, size_t smem,
+extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps, int ppw, int chg, int grid, size_t smem,
                                         cudaStream_t stream);
-extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, size_t smem, int fpc, int *blocks_per_sm);
-extern "C" int pb_shape_supported(int mode, int warps, int ppw);
+extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, int chg, size_t smem, int fpc, int *blocks_per_sm);
+extern "C" int pb_shape_supported(int mode, int warps, int ppw, int chg);
 
 namespace {
 
@@ -93,6 +93,7 @@ struct pb_handle {
     uint32_t *d_xsyn4 = nullptr, *d_info = nullptr;
     int grid = 0, blocks_per_sm = 0, sms = 0, warps = 1, ppw = 1;
     int fpc = 1;  // frames per CTA
+    bool chg = false;  // channel in global scratch (not shared memory)
     size_t smem_frame = 0;
     unsigned char *d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -306,68 +307,89 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         while (p * wv < L) p <<= 1;
         return p;
     };
-    if (!pb_shape_supported(mode, warps, shape_ppw(warps))) warps = 1;
+    if (!pb_shape_supported(mode, warps, shape_ppw(warps), 0)) warps = 1;
     int ppw = shape_ppw(warps), lppw = 0;
     while ((1 << lppw) < ppw) ++lppw;
     const int rows = ppw * warps;  // alpha rows, padded to whole interleave blocks
     h->ppw = ppw;
     h->warps = warps;
-    pb::FrameLayout &lay = h->base.lay;
-    int off = 0;
-    lay.ch_off = off;
-    off = align_up(off + N * es, 16);
-    for (int s = 0; s < n; ++s) {
-        int words = std::max(1, (1 << s) / 32);
-        lay.b_stride[s] = words > 1 ? words + 1 : 1;
-        lay.b_off[s] = off;
-        off = align_up(off + L * lay.b_stride[s] * 4, 16);
-    }
-    lay.pm_off = off;
-    off = align_up(off + 2 * L * 8, 16);
-    lay.idx_stride = std::max(1, (n + 3) / 4);  // index words per path (4 stages per word)
-    lay.ia_off = off;
-    off = align_up(off + 2 * L * lay.idx_stride * 4, 16);
-    lay.ib_off = off;
-    off = align_up(off + 2 * L * lay.idx_stride * 4, 16);
-    const int nbuf = warps > 1 ? 2 : 1;  // candidate buffers (by leaf parity across warps)
-    lay.cd_off = off;
-    off = align_up(off + nbuf * L * pb::kMaxCand * 8, 16);
-    lay.clrb_off = off;
-    off = align_up(off + nbuf * L * 4 * 2, 16);
-    lay.cflag_off = off;
-    off = align_up(off + nbuf * L, 16);
-    lay.asg_off = off;
-    off = align_up(off + nbuf * 2 * L, 16);
-    lay.hard_words = std::max(1, max_hard / 32);
-    lay.hard_off = off;
-    off = align_up(off + nbuf * L * lay.hard_words * 4, 16);
-    lay.root_words = std::max(1, N / 32);
-    lay.root_off = off;
-    off = align_up(off + lay.root_words * 4, 16);
-
     const int smem_cap = 227 * 1024;
-    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", mode == PB_MODE_F32 ? 3 : 8));
-    const int budget = std::max(off, env_int("PB_SMEM_BUDGET", smem_cap / target_fps - 1024));
-    // alpha stages s = 0 .. n-2 (n-1 is recomputed), lowest stages first into
-    // shared memory, the rest into per-CTA global scratch (L2-resident)
-    int s_global = n - 1;
-    for (int s = 0; s <= n - 2; ++s) {
-        int bytes = align_up(rows * (1 << s) * es, 16);
-        if (off + bytes > budget) {
-            s_global = s;
-            break;
+    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", 8));
+    // Per-frame layout for a channel in shared memory or in global scratch.
+    auto plan_layout = [&](bool chg, pb::FrameLayout &lay) {
+        lay = pb::FrameLayout{};
+        int off = 0, goff = 0;
+        lay.ch_off = 0;
+        if (chg)
+            goff = align_up(N * es, 256);  // global scratch, before the global alpha stages
+        else
+            off = align_up(N * es, 16);
+        for (int s = 0; s < n; ++s) {
+            int words = std::max(1, (1 << s) / 32);
+            lay.b_stride[s] = words > 1 ? words + 1 : 1;
+            lay.b_off[s] = off;
+            off = align_up(off + L * lay.b_stride[s] * 4, 16);
         }
-        lay.a_off[s] = off;
-        off += bytes;
+        lay.pm_off = off;
+        off = align_up(off + 2 * L * 8, 16);
+        lay.idx_stride = std::max(1, (n + 3) / 4);  // index words per path (4 stages per word)
+        lay.ia_off = off;
+        off = align_up(off + 2 * L * lay.idx_stride * 4, 16);
+        lay.ib_off = off;
+        off = align_up(off + 2 * L * lay.idx_stride * 4, 16);
+        const int nbuf = warps > 1 ? 2 : 1;  // candidate buffers (by leaf parity across warps)
+        lay.cd_off = off;
+        off = align_up(off + nbuf * L * pb::kMaxCand * 8, 16);
+        lay.clrb_off = off;
+        off = align_up(off + nbuf * L * 4 * 2, 16);
+        lay.cflag_off = off;
+        off = align_up(off + nbuf * L, 16);
+        lay.asg_off = off;
+        off = align_up(off + nbuf * 2 * L, 16);
+        lay.hard_words = std::max(1, max_hard / 32);
+        lay.hard_off = off;
+        off = align_up(off + nbuf * L * lay.hard_words * 4, 16);
+        lay.root_words = std::max(1, N / 32);
+        lay.root_off = off;
+        off = align_up(off + lay.root_words * 4, 16);
+
+        const int budget = std::max(off, env_int("PB_SMEM_BUDGET", smem_cap / target_fps - 1024));
+        // alpha stages s = 0 .. n-2 (n-1 is recomputed), lowest stages first into
+        // shared memory, the rest into per-frame global scratch (L2-resident)
+        int s_global = n - 1;
+        for (int s = 0; s <= n - 2; ++s) {
+            int bytes = align_up(rows * (1 << s) * es, 16);
+            if (off + bytes > budget) {
+                s_global = s;
+                break;
+            }
+            lay.a_off[s] = off;
+            off += bytes;
+        }
+        lay.a_gfrom = s_global;
+        for (int s = s_global; s <= n - 2; ++s) {
+            lay.a_off[s] = goff;
+            goff = align_up(goff + rows * (1 << s) * es, 256);
+        }
+        lay.gbytes = goff;
+        lay.smem_bytes = align_up(off, 16);
+    };
+    // The channel moves to global scratch (L1/L2; it is read only by the
+    // stage n-1 ops) when that buys more frames per SM or keeps more alpha
+    // stages in shared memory; int8 channels are small and stay.
+    pb::FrameLayout &lay = h->base.lay;
+    {
+        pb::FrameLayout ls, lg;
+        plan_layout(false, ls);
+        plan_layout(true, lg);
+        auto fps_of = [&](const pb::FrameLayout &l) { return std::min(target_fps, smem_cap / std::max(1, l.smem_bytes)); };
+        const int chg_env = env_int("PB_CH_GLOBAL", -1);
+        bool chg = fps_of(lg) > fps_of(ls) || (fps_of(lg) == fps_of(ls) && lg.a_gfrom > ls.a_gfrom);
+        if (chg_env >= 0) chg = chg_env != 0;
+        chg = chg && pb_shape_supported(mode, warps, ppw, 1);
+        h->chg = chg;
+        lay = chg ? lg : ls;
     }
-    lay.a_gfrom = s_global;
-    int goff = 0;
-    for (int s = s_global; s <= n - 2; ++s) {
-        lay.a_off[s] = goff;
-        goff = align_up(goff + rows * (1 << s) * es, 256);
-    }
-    lay.gbytes = goff;
-    lay.smem_bytes = align_up(off, 16);
     if (lay.smem_bytes > smem_cap) {
         delete h;
         return fail(PB_EINVAL, "code too large for the per-frame shared-memory plan (" +
@@ -397,7 +419,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     }
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
     if (env_int("PB_GRID_SMS", 0) > 0) h->sms = std::min(h->sms, env_int("PB_GRID_SMS", 0));  // experiments
-    e = pb_occupancy(mode, h->warps, h->ppw, h->smem_frame, 1, &h->blocks_per_sm);
+    e = pb_occupancy(mode, h->warps, h->ppw, h->chg, h->smem_frame, 1, &h->blocks_per_sm);
     if (e != cudaSuccess || h->blocks_per_sm < 1) {
         delete h;
         return cuda_fail(e == cudaSuccess ? cudaErrorInvalidConfiguration : e, "occupancy");
@@ -414,7 +436,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         while (fpc > 1 && (size_t)fpc * h->smem_frame > (size_t)smem_cap) --fpc;
         int bps = 0;
         while (fpc > 1) {
-            e = pb_occupancy(mode, h->warps, h->ppw, fpc * h->smem_frame, fpc, &bps);
+            e = pb_occupancy(mode, h->warps, h->ppw, h->chg, fpc * h->smem_frame, fpc, &bps);
             if (e == cudaSuccess && bps >= 1) break;
             --fpc;
         }
@@ -487,10 +509,10 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
              "{\"N\": %d, \"k\": %d, \"L\": %d, \"mode\": \"%s\", \"ops\": %d, \"device_ops\": %d, "
              "\"smem_per_frame\": %d, \"alpha_global_from_stage\": %d, \"global_scratch_per_frame\": %d, "
              "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": %d, \"warps_per_frame\": %d, "
-             "\"paths_per_warp\": %d, \"frames_per_cta\": %d}",
+             "\"paths_per_warp\": %d, \"frames_per_cta\": %d, \"channel_in_global\": %d}",
              N, code->k, L, mode == PB_MODE_F32 ? "f32" : "int8", n_ops, (int)h->prog.size(),
              lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm * h->fpc, h->sms, h->grid,
-             32 * h->warps * h->fpc, h->warps, h->ppw, h->fpc);
+             32 * h->warps * h->fpc, h->warps, h->ppw, h->fpc, (int)h->chg);
     h->plan_json = buf;
     *out = h;
     return PB_OK;
@@ -542,7 +564,7 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
     int grid = (int)std::min<long long>(h->grid, (pr.batch + h->fpc - 1) / h->fpc);
     if (grid < 1) return PB_OK;
     PB_CUDA(cudaEventRecord(h->ev0, st));
-    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, grid, h->smem_frame * h->fpc, st);
+    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc, st);
     if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
     PB_CUDA(cudaEventRecord(h->ev1, st));
     h->timed = true;
