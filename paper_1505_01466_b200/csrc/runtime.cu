@@ -103,6 +103,9 @@ struct pb_handle {
     unsigned char *d_out = nullptr;
     size_t d_out_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // pipelined host-buffer calls: two internal streams + join events
+    cudaStream_t aux[2] = {nullptr, nullptr};
+    cudaEvent_t evs = nullptr, evj[2] = {nullptr, nullptr};
     bool timed = false;
     long long launches = 0;
     std::string plan_json;
@@ -528,6 +531,11 @@ int pb_destroy(pb_handle *h) {
     cudaFree(h->d_out);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
+    for (int j = 0; j < 2; ++j) {
+        if (h->aux[j]) cudaStreamDestroy(h->aux[j]);
+        if (h->evj[j]) cudaEventDestroy(h->evj[j]);
+    }
+    if (h->evs) cudaEventDestroy(h->evs);
     delete h;
     return PB_OK;
 }
@@ -557,6 +565,68 @@ int ensure(void **p, size_t *cap, size_t need) {
     cudaError_t e = cudaMalloc(p, sz);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc staging");
     *cap = sz;
+    return PB_OK;
+}
+
+// Host-buffer decode of a large batch in chunks over two internal streams:
+// chunk i's copy-in overlaps chunk i-1's kernel and copy-out (the copies
+// only overlap when the host buffers are pinned).  The user stream orders
+// the whole call; last_kernel_ms spans it.
+int decode_pipelined(pb_handle *h, const pb::Params &base, const void *llr, size_t in_es, int64_t batch,
+                     long long chunk, uint8_t *info_out, uint8_t *crc_ok, double *pm_out, int32_t *paths_used,
+                     cudaStream_t st) {
+    const size_t in_bytes = (size_t)batch * h->N * in_es;
+    int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
+    if (rc) return rc;
+    const size_t big_info = (size_t)batch * h->k;
+    const size_t o_ok = (big_info + 255) / 256 * 256;
+    const size_t o_pm = o_ok + ((size_t)batch + 255) / 256 * 256;
+    const size_t o_pu = o_pm + (size_t)batch * 8;
+    rc = ensure((void **)&h->d_out, &h->d_out_cap, o_pu + (size_t)batch * 4);
+    if (rc) return rc;
+    for (int j = 0; j < 2; ++j) {
+        if (!h->aux[j]) PB_CUDA(cudaStreamCreateWithFlags(&h->aux[j], cudaStreamNonBlocking));
+        if (!h->evj[j]) PB_CUDA(cudaEventCreateWithFlags(&h->evj[j], cudaEventDisableTiming));
+    }
+    if (!h->evs) PB_CUDA(cudaEventCreateWithFlags(&h->evs, cudaEventDisableTiming));
+    PB_CUDA(cudaEventRecord(h->evs, st));
+    for (int j = 0; j < 2; ++j) PB_CUDA(cudaStreamWaitEvent(h->aux[j], h->evs, 0));
+    PB_CUDA(cudaEventRecord(h->ev0, h->aux[0]));
+    unsigned char *din = static_cast<unsigned char *>(h->d_in);
+    const unsigned char *hin = static_cast<const unsigned char *>(llr);
+    int i = 0;
+    for (long long f0 = 0; f0 < batch; f0 += chunk, ++i) {
+        cudaStream_t sa = h->aux[i & 1];
+        const long long nb = std::min<long long>(chunk, batch - f0);
+        const size_t io = (size_t)f0 * h->N * in_es, ib = (size_t)nb * h->N * in_es;
+        PB_CUDA(cudaMemcpyAsync(din + io, hin + io, ib, cudaMemcpyHostToDevice, sa));
+        pb::Params pc = base;
+        pc.llr = din + io;
+        pc.batch = nb;
+        pc.info_out = info_out ? h->d_out + (size_t)f0 * h->k : nullptr;
+        pc.crc_ok = crc_ok ? h->d_out + o_ok + f0 : nullptr;
+        pc.pm_out = pm_out ? reinterpret_cast<double *>(h->d_out + o_pm) + f0 : nullptr;
+        pc.paths_used = paths_used ? reinterpret_cast<int32_t *>(h->d_out + o_pu) + f0 : nullptr;
+        const int grid = (int)std::min<long long>(h->grid, (nb + h->fpc - 1) / h->fpc);
+        cudaError_t e = pb_launch_decode(&pc, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc, sa);
+        if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
+        h->launches += 1;
+        if (info_out)
+            PB_CUDA(cudaMemcpyAsync(info_out + (size_t)f0 * h->k, pc.info_out, (size_t)nb * h->k,
+                                    cudaMemcpyDeviceToHost, sa));
+        if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok + f0, pc.crc_ok, (size_t)nb, cudaMemcpyDeviceToHost, sa));
+        if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out + f0, pc.pm_out, (size_t)nb * 8, cudaMemcpyDeviceToHost, sa));
+        if (paths_used)
+            PB_CUDA(cudaMemcpyAsync(paths_used + f0, pc.paths_used, (size_t)nb * 4, cudaMemcpyDeviceToHost, sa));
+    }
+    for (int j = 0; j < 2; ++j) {
+        PB_CUDA(cudaEventRecord(h->evj[j], h->aux[j]));
+        PB_CUDA(cudaStreamWaitEvent(st, h->evj[j], 0));
+    }
+    PB_CUDA(cudaEventRecord(h->ev1, st));
+    h->timed = true;
+    PB_CUDA(cudaStreamSynchronize(st));
+    PB_CUDA(cudaGetLastError());
     return PB_OK;
 }
 
@@ -608,6 +678,9 @@ extern "C" int pb_decode(pb_handle *h, const void *llr, int in_type, int64_t bat
         return launch(h, pr, st);
     }
     // staged path: host buffers in and/or out
+    const long long chunk = std::max<long long>(1, env_int("PB_CHUNK_FRAMES", std::max(4096, 6 * h->grid * h->fpc)));
+    if (!dev_in && batch > chunk) return decode_pipelined(h, pr, llr, in_es, batch, chunk, info_out, crc_ok, pm_out,
+                                                          paths_used, st);
     if (!dev_in) {
         int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
         if (rc) return rc;

@@ -137,3 +137,21 @@ def test_warp_shapes_agree(c1, warps, monkeypatch):
         o = oracle.decode_batch(sch, L, fb.llrs[:96])
         assert np.array_equal(r.info_bits, o.info_bits)
         assert np.array_equal(r.chosen_pm, o.chosen_pm)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_chunked_host_pipeline_matches_device_call(c1, monkeypatch, pinned):
+    """Host-buffer batches above PB_CHUNK_FRAMES run chunked over two streams;
+    results must equal the single-launch call, ragged tail included."""
+    import torch
+    spec, sch, fb = c1
+    dec = pb.ListDecoder(sch, 4)
+    ref = dec.decode_batch(fb.llrs)                 # below the chunk size: one launch
+    monkeypatch.setenv("PB_CHUNK_FRAMES", "70")   # 300 frames -> 5 chunks, last one ragged
+    llr = torch.from_numpy(fb.llrs).pin_memory() if pinned else fb.llrs
+    launches = dec.launches
+    got = dec.decode_batch(llr)
+    assert dec.launches - launches == 5
+    for a, b in zip((got.info_bits, got.crc_ok, got.chosen_pm, got.paths_used),
+                    (ref.info_bits, ref.crc_ok, ref.chosen_pm, ref.paths_used)):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
