@@ -1199,7 +1199,10 @@ struct RtOps {
                     np = o.pout;
                     break;
             }
-            __syncwarp();
+            if (P.sync_mask >= 0 && (oi & P.sync_mask) == 0)
+                __syncthreads();  // regroup the CTA's frames (shared instruction fetch)
+            else
+                __syncwarp();
             if (prof) {
                 const long long t1 = clock64();
                 long long *oc = P.op_cycles + oi * 12;

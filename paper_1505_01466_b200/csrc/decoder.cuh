@@ -83,6 +83,7 @@ struct Params {
     long long *op_cycles;       // debug: per-op clock64 deltas of CTA 0's first frame, or null
     int ablate;                 // timing experiments only (PB_ABLATE): skip parts, wrong results
     int fpc;                    // frames per CTA (W warps each)
+    int sync_mask;              // CTA barrier after ops with (index & mask) == 0; -1: none
     FrameLayout lay;
 };
 
