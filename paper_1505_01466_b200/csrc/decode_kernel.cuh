@@ -564,14 +564,13 @@ __device__ __forceinline__ void bitonic_merge_desc(long long &v, int Wd, int lan
         v = (((lane & j) == 0) == (o > v)) ? o : v;
     }
 }
-__device__ __forceinline__ int excl_scan(int v, int lane) {
-    int incl = v;
+// exclusive warp prefix sum of v in [0, 15]: one ballot per bit, independent
+__device__ __forceinline__ int excl_scan4(int v, int lane) {
+    const unsigned below = (1u << lane) - 1u;
+    int r = 0;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(FULL_MASK, incl, d);
-        if (lane >= d) incl += t;
-    }
-    return incl - v;
+    for (int b = 0; b < 4; ++b) r += __popc(__ballot_sync(FULL_MASK, (v >> b) & 1) & below) << b;
+    return r;
 }
 
 // SPC flip sets relative to the ML word over the four LRB slots, emission
@@ -625,35 +624,38 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const
         for (int c = 0; c < kMaxCand; ++c) srt[c] = key[c];
         // best-first column per lane (Rate-1 columns already are:
         // 0 >= -m1 >= -m2 >= -(m1+m2), monotone under rounding)
+        auto cswap = [&](int a, int b) {
+            const long long x = srt[a], y = srt[b];
+            srt[a] = x > y ? x : y;
+            srt[b] = x > y ? y : x;
+        };
         if (C == 2) {
-            const long long x = srt[0], y = srt[1];
-            srt[0] = x > y ? x : y;
-            srt[1] = x > y ? y : x;
-        } else if (C == 8) {
-#pragma unroll
-            for (int pass = 0; pass < 8; ++pass)
-#pragma unroll
-                for (int c = pass & 1; c + 1 < 8; c += 2) {
-                    const long long x = srt[c], y = srt[c + 1];
-                    srt[c] = x > y ? x : y;
-                    srt[c + 1] = x > y ? y : x;
-                }
+            cswap(0, 1);
+        } else if (C == 8) {  // Batcher odd-even merge sort, 19 comparators, depth 6
+            cswap(0, 1); cswap(2, 3); cswap(4, 5); cswap(6, 7);
+            cswap(0, 2); cswap(1, 3); cswap(4, 6); cswap(5, 7);
+            cswap(1, 2); cswap(5, 6);
+            cswap(0, 4); cswap(1, 5); cswap(2, 6); cswap(3, 7);
+            cswap(2, 4); cswap(3, 5);
+            cswap(1, 2); cswap(3, 4); cswap(5, 6);
         }
         F.mark(4);
-        // kept set: slot = lane (< L); start from every source's best
+        // kept set: slot = lane (< L); start from every source's best.  The
+        // lane's exposed candidate is srt[0] of its shifted column.
         long long kept = lane < L ? srt[0] : LLONG_MAX;
-        int ptr = 1;
-        for (;;) {
-            long long cand = LLONG_MIN;
 #pragma unroll
-            for (int c = 1; c < kMaxCand; ++c)
-                if (c == ptr && c < C) cand = srt[c];
+        for (int c = 0; c < kMaxCand; ++c) srt[c] = c + 1 < C ? srt[c + 1 < kMaxCand ? c + 1 : c] : LLONG_MIN;
+        for (;;) {
+            const long long cand = srt[0];
             const long long best = warp_max_ll(cand);
             const long long worst = warp_min_ll(kept);
             if (best <= worst) break;
             const int from = __ffs(__ballot_sync(FULL_MASK, cand == best)) - 1;
             const int into = __ffs(__ballot_sync(FULL_MASK, kept == worst)) - 1;
-            if (lane == from) ++ptr;
+            if (lane == from) {
+#pragma unroll
+                for (int c = 0; c < kMaxCand; ++c) srt[c] = c + 1 < kMaxCand ? srt[c + 1] : LLONG_MIN;
+            }
             if (lane == into) kept = best;
         }
         const long long Tk = warp_min_ll(kept);
@@ -666,7 +668,10 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const
             eq += key[c] == Tk;
         }
         const int need = L - (int)__reduce_add_sync(FULL_MASK, (unsigned)gt);
-        int r = excl_scan(eq, lane);
+        // ties at Tk: the earliest `need` in (source, cand) order; with no
+        // surplus tie (the usual case) every tie survives and no scan is needed
+        const int eqt = (int)__reduce_add_sync(FULL_MASK, (unsigned)eq);
+        int r = eqt <= need ? 0 : excl_scan4(eq, lane);
         mask = 0u;
 #pragma unroll
         for (int c = 0; c < kMaxCand; ++c) {
@@ -679,7 +684,7 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const
         }
     }
     F.mark(6);
-    int k = excl_scan(__popc(mask), lane);
+    int k = excl_scan4(__popc(mask), lane);
     uint8_t *asg = F.asg(F.par);
     while (mask) {
         const int c = __ffs(mask) - 1;
