@@ -109,6 +109,7 @@ def build(verbose: bool = False, jobs: int | None = None, profile: bool = False)
     if verbose:
         for lg in logs:
             print(lg)
+    LIB_PATH = os.environ.get("PB_LIB_OUT") or LIB_PATH  # experiments: build a variant elsewhere
     tmp = LIB_PATH + ".tmp"
     subprocess.run(["nvcc", *ARCH, "-shared", "-o", tmp, *objs], check=True, cwd=CSRC)
     os.replace(tmp, LIB_PATH)

@@ -11,6 +11,13 @@ constexpr int kMaxLog = 16;     // N <= 65536
 constexpr int kMaxL = 32;       // selection runs on one warp: one lane per source path
 constexpr int kMaxCand = 8;
 
+// threads per CTA the kernels are compiled for (__launch_bounds__): the
+// register budget per thread is 65536 / PB_MAXT
+#ifndef PB_MAXT
+#define PB_MAXT 256
+#endif
+constexpr int kMaxThreads = PB_MAXT;
+
 // Device op kinds.  Combines never appear: each leaf carries its chain of
 // combines.
 enum : int8_t { DK_F = 0, DK_G = 1, DK_R0 = 2, DK_REP = 3, DK_R1 = 4, DK_SPC = 5, DK_NOP = 6 };

@@ -436,7 +436,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     // (A CTA barrier after every op to force lockstep measured slower.)
     {
         const int fpc_env = env_int("PB_FPC", 0);
-        int fpc = std::min(fpc_env > 0 ? fpc_env : h->blocks_per_sm, 8 / h->warps);  // 256-thread bound
+        int fpc = std::min(fpc_env > 0 ? fpc_env : h->blocks_per_sm, pb::kMaxThreads / 32 / h->warps);  // launch bound
         while (fpc > 1 && (size_t)fpc * h->smem_frame > (size_t)smem_cap) --fpc;
         int bps = 0;
         while (fpc > 1) {
