@@ -80,7 +80,9 @@ typedef struct pb_handle pb_handle;
  * (ValueError "list size X must be >= 1"), re-validates the op list against
  * the schedule grammar (schedule.py:159-201), and uploads the lowered device
  * program, CRC syndrome tables and payload positions.
- * list_size: 1..32 (PB_EINVAL above 32 in this version). */
+ * list_size: 1..32 (PB_EINVAL above 32 in this version).  At list size 1,
+ * pb_decode runs the single-path kernel with the list decoder's leaf rules
+ * (identical results, ~30x faster than a one-path list decode). */
 int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
               int device, pb_handle **out);
 
@@ -104,6 +106,24 @@ int pb_decode(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t
 int pb_decode_paths(pb_handle *h, const void *llr, int in_type, int64_t batch,
                     uint8_t *codewords, double *path_pm, uint8_t *path_crc,
                     int32_t *paths_used, void *stream);
+
+/* Adaptive decoding: AdaptiveDecoder.decode (listdec.py:437-459), batched.
+ * A single-path Fast-SSC pass (fastssc.py:20-83) decodes every frame; frames
+ * whose CRC passes keep that result (paths_used 1, invoked_list 0), the rest
+ * are re-decoded by the list decoder of this handle (invoked_list 1).  The
+ * failing frames are queued on the device: no host round trip between the
+ * two kernels.  Outputs as pb_decode plus invoked_list uint8 [batch] (may be
+ * NULL).  PB_EINVAL "adaptive decoding needs a CRC in the code spec" for a
+ * code without CRC (the reference raises ValueError in the constructor). */
+int pb_decode_adaptive(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *info_out,
+                       uint8_t *crc_ok, double *pm_out, int32_t *paths_used, uint8_t *invoked_list,
+                       void *stream);
+
+/* The single-path pass alone: polaris.fastssc.execute_schedule
+ * (fastssc.py:20-83).  codewords uint8 [batch][N] (one byte per bit),
+ * pm_out double [batch].  Host buffers only; synchronous. */
+int pb_fastssc(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *codewords,
+               double *pm_out, void *stream);
 
 /* Release the handle and its device memory. */
 int pb_destroy(pb_handle *h);

@@ -577,6 +577,111 @@ static int decode_frame(dec_t *d, const float *llr) {
     return P;
 }
 
+
+/* ------------------------------------------------ single-path fast path */
+
+/* polaris.fastssc.execute_schedule (fastssc.py:20-83) for one frame: every
+ * leaf takes its most likely decision directly (Rate-0 zeros, Rate-1 hard
+ * decisions, repetition by the sign of the pairwise sum, SPC by the Wagner
+ * rule on the first least reliable position).  x: [N] codeword estimate;
+ * returns the path metric.  The adaptive decoder (listdec.py:437-459) runs
+ * this first and keeps its result when the CRC passes. */
+static double fastssc_frame(const oc_code *code, const int32_t *ops, int n_ops, int int8_mode,
+                            const float *llr, unsigned char *x, float *work) {
+    const int N = code->N;
+    int n = 0;
+    while ((1 << n) < N) n++;
+    float *ch = work, *alpha = work + N;                 /* alpha[s] at offset 2^s */
+    unsigned char *beta = (unsigned char *)(work + 2 * N); /* beta[s][side] at (2s+side)*N */
+    for (int i = 0; i < N; i++) {
+        float v = llr[i];
+        ch[i] = v > 1048576.0f ? 1048576.0f : (v < -1048576.0f ? -1048576.0f : v);
+    }
+    double pm = 0.0;
+    for (int o = 0; o < n_ops; o++) {
+        const int32_t *op = ops + 5 * o;
+        int kind = op[0], m = op[1], s = op[2], side = op[3], h = m >> 1;
+        const float *src = m == N ? ch : alpha + (1 << s);
+        if (kind == K_F) {                                      /* 59-61 */
+            float *d = alpha + (1 << (s - 1));
+            for (int i = 0; i < h; i++) d[i] = f_fn(src[i], src[i + h]);
+            continue;
+        }
+        if (kind == K_G) {                                      /* 62-64 */
+            float *d = alpha + (1 << (s - 1));
+            const unsigned char *bl = beta + (size_t)(2 * (s - 1)) * N;
+            for (int i = 0; i < h; i++) {
+                float v = src[i + h] + (1.0f - 2.0f * (float)bl[i]) * src[i];
+                if (int8_mode) v = v > 127.0f ? 127.0f : (v < -127.0f ? -127.0f : v);
+                d[i] = v;
+            }
+            continue;
+        }
+        unsigned char *dst = m == N ? x : beta + (size_t)(2 * s + side) * N;
+        if (kind == K_COMB) {                                   /* 66-69 */
+            const unsigned char *l = beta + (size_t)(2 * (s - 1)) * N, *r = l + N;
+            for (int i = 0; i < h; i++) { dst[i] = l[i] ^ r[i]; dst[i + h] = r[i]; }
+        } else if (kind == K_R0) {                              /* 70-72 */
+            float *mn = (float *)malloc(sizeof(float) * m);
+            for (int i = 0; i < m; i++) { mn[i] = src[i] < 0.0f ? src[i] : 0.0f; dst[i] = 0; }
+            pm += (double)pw_sum(mn, m);
+            free(mn);
+        } else if (kind == K_R1) {                              /* 73-74 */
+            for (int i = 0; i < m; i++) dst[i] = src[i] < 0.0f;
+        } else if (kind == K_REP) {                             /* 75-80 */
+            float *a = (float *)malloc(sizeof(float) * 2 * m);
+            for (int i = 0; i < m; i++) { a[i] = src[i] < 0.0f ? src[i] : 0.0f; a[m + i] = src[i] > 0.0f ? src[i] : 0.0f; }
+            float neg = pw_sum(a, m), pos = pw_sum(a + m, m), tot = pw_sum(src, m);
+            int ones = tot < 0.0f;
+            for (int i = 0; i < m; i++) dst[i] = (unsigned char)ones;
+            pm += ones ? (double)(-pos) : (double)neg;
+            free(a);
+        } else if (kind == K_SPC) {                             /* 81-88 */
+            int par = 0, weak = 0;
+            float wm = INFINITY;
+            for (int i = 0; i < m; i++) {
+                dst[i] = src[i] < 0.0f;
+                par ^= dst[i];
+                float mg = fabsf(src[i]);
+                if (mg < wm) { wm = mg; weak = i; }             /* argmin: first minimum */
+            }
+            if (par) { dst[weak] ^= 1; pm -= (double)wm; }
+        } else {
+            return NAN;
+        }
+    }
+    return pm;
+}
+
+int oracle_fastssc_batch(const oc_code *code, const int32_t *ops, int n_ops, int int8_mode,
+                         const float *llr, int64_t batch, uint8_t *codewords, double *pm,
+                         uint8_t *info, uint8_t *crc_ok) {
+    const int N = code->N;
+    if (N < 2 || (N & (N - 1))) return -11;
+    float *work = (float *)malloc(sizeof(float) * 2 * N + (size_t)2 * 17 * N);
+    unsigned char *x = (unsigned char *)malloc(N), *u = (unsigned char *)malloc(N);
+    dec_t d;
+    memset(&d, 0, sizeof d);
+    d.code = code;
+    int *ipos = (int *)malloc(sizeof(int) * N);
+    int ni = 0;
+    for (int i = 0; i < N; i++)
+        if (!code->frozen[i]) ipos[ni++] = i;
+    d.info_pos = ipos;
+    for (int64_t b = 0; b < batch; b++) {
+        double p = fastssc_frame(code, ops, n_ops, int8_mode, llr + (size_t)b * N, x, work);
+        if (codewords) memcpy(codewords + (size_t)b * N, x, N);
+        if (pm) pm[b] = p;
+        memcpy(u, x, N);
+        polar_transform(u, N);
+        if (info)
+            for (int i = 0; i < code->k; i++) info[(size_t)b * code->k + i] = u[ipos[i]];
+        if (crc_ok) crc_ok[b] = (uint8_t)crc_ok_of(&d, u);
+    }
+    free(work); free(x); free(u); free(ipos);
+    return 0;
+}
+
 /* --------------------------------------------------------- batch entry */
 
 typedef struct {

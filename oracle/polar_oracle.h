@@ -24,6 +24,13 @@ int oracle_decode_batch(const oc_code *code, const int32_t *ops, int n_ops, int 
                         uint8_t *crc_ok, double *pm, int32_t *paths_used, uint8_t *all_cw,
                         double *all_pm, uint8_t *all_crc, int nthreads);
 
+/* polaris.fastssc.execute_schedule (fastssc.py:20-83) per frame: codeword
+ * estimates [batch][N] (may be NULL), path metric, and the payload / CRC
+ * flag extract_payload gives for it (encode.py:76-87; may be NULL). */
+int oracle_fastssc_batch(const oc_code *code, const int32_t *ops, int n_ops, int int8_mode,
+                         const float *llr, int64_t batch, uint8_t *codewords, double *pm,
+                         uint8_t *info, uint8_t *crc_ok);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,8 +15,9 @@ from .schedule import (NodeKind, NodeOp, Schedule, ScheduleConfig, build_schedul
                        classify, emit_source)
 from .channel import (LLR_CLAMP, ChannelConfig, clamp_llr, frame_rng, generate_frames,
                       quantize_int8, transmit)
-from .listdec import (BatchResult, DecodeResult, ListDecoder, PathOutcome, decode,
-                      select_candidates)
+from .listdec import (AdaptiveBatchResult, AdaptiveDecoder, BatchResult, DecodeResult,
+                      ListDecoder, PathOutcome, decode, select_candidates)
+from .fastssc import execute_schedule
 
 __version__ = "0.1.0"
 
@@ -29,6 +30,7 @@ __all__ = [
     "emit_source",
     "LLR_CLAMP", "ChannelConfig", "clamp_llr", "frame_rng", "generate_frames",
     "quantize_int8", "transmit",
-    "BatchResult", "DecodeResult", "ListDecoder", "PathOutcome", "decode",
+    "AdaptiveBatchResult", "AdaptiveDecoder", "BatchResult", "DecodeResult", "ListDecoder",
+    "PathOutcome", "decode", "execute_schedule",
     "select_candidates", "__version__",
 ]

@@ -27,7 +27,8 @@ PB_OK, PB_EINVAL, PB_ECUDA, PB_EINTERNAL, PB_ENOMEM = 0, -1, -2, -3, -4
 PB_MODE_F32, PB_MODE_INT8 = 0, 1
 PB_IN_F32, PB_IN_I8 = 0, 1
 
-EXPORTS = ("pb_create", "pb_decode", "pb_decode_paths", "pb_destroy", "pb_last_error",
+EXPORTS = ("pb_create", "pb_decode", "pb_decode_paths", "pb_decode_adaptive", "pb_fastssc",
+           "pb_destroy", "pb_last_error",
            "pb_plan_json", "pb_launch_count", "pb_last_kernel_ms", "pb_version")
 
 
@@ -91,7 +92,7 @@ def build(verbose: bool = False, jobs: int | None = None, profile: bool = False)
         if _stale(obj, [inst, *hdrs]):
             cmds.append(["nvcc", *NVCC_FLAGS, *extra, "-I", INCLUDE, f"-DPB_T={t}", f"-DPB_W={w}",
                          f"-DPB_PPW={ppw}", f"-DPB_CHG={chg}", f"-DPB_TAG={tag}", "-c", inst, "-o", obj])
-    for src in ("dispatch.cu", "runtime.cu"):
+    for src in ("dispatch.cu", "runtime.cu", "ssc_kernel.cu"):
         obj = os.path.join(BUILD_DIR, src.replace(".cu", ".o"))
         objs.append(obj)
         if _stale(obj, [os.path.join(CSRC, src), *hdrs]):
@@ -137,6 +138,10 @@ def lib():
     L.pb_decode.argtypes = [vp, vp, i32, i64, vp, vp, vp, vp, vp]
     L.pb_decode_paths.restype = i32
     L.pb_decode_paths.argtypes = [vp, vp, i32, i64, vp, vp, vp, vp, vp]
+    L.pb_decode_adaptive.restype = i32
+    L.pb_decode_adaptive.argtypes = [vp, vp, i32, i64, vp, vp, vp, vp, vp, vp]
+    L.pb_fastssc.restype = i32
+    L.pb_fastssc.argtypes = [vp, vp, i32, i64, vp, vp, vp]
     L.pb_destroy.restype = i32
     L.pb_destroy.argtypes = [vp]
     L.pb_last_error.restype = ctypes.c_char_p

@@ -1232,10 +1232,14 @@ __device__ __forceinline__ void decode_frames(const Params &P, const CFG &cfg) {
     unsigned char *gs = P.gscratch ? P.gscratch + (size_t)slot * cfg.gbytes() : nullptr;
     unsigned char *sm = g_smem + (size_t)grp * cfg.smem_bytes();
     const long long stride = (long long)gridDim.x * P.fpc;
-    for (long long f0 = (long long)blockIdx.x * P.fpc; f0 < P.batch; f0 += stride) {
+    // adaptive pass: the frames the single-path pass could not settle
+    // (count and row map on the device, written by k_ssc)
+    const long long batch = P.batch_dev ? (long long)*P.batch_dev : P.batch;
+    for (long long f0 = (long long)blockIdx.x * P.fpc; f0 < batch; f0 += stride) {
         // tail: idle slots decode the last frame again and write nothing
-        const long long f = f0 + grp < P.batch ? f0 + grp : P.batch - 1;
-        const bool own = f0 + grp < P.batch;
+        const long long fi = f0 + grp < batch ? f0 + grp : batch - 1;
+        const long long f = P.frame_map ? (long long)P.frame_map[fi] : fi;
+        const bool own = f0 + grp < batch;
         Dec<T, W, PPW, CFG> F(P, cfg, sm, gs);
         load_channel(F, f);
         if ((threadIdx.x & (32 * W - 1)) == 0) F.pm(0)[0] = 0.0;

@@ -89,9 +89,51 @@ struct Params {
     unsigned char *gscratch;    // [CTA slots][gbytes]
     long long *op_cycles;       // debug: per-op clock64 deltas of CTA 0's first frame, or null
     int ablate;                 // timing experiments only (PB_ABLATE): skip parts, wrong results
+    const int32_t *frame_map;   // adaptive pass: frame f reads / writes row frame_map[f], or null
+    const int32_t *batch_dev;   // adaptive pass: frame count on the device (<= batch), or null
     int fpc;                    // frames per CTA (W warps each)
     int sync_mask;              // CTA barrier after ops with (index & mask) == 0; -1: none
     FrameLayout lay;
+};
+
+// ---------------------------------------------------------------------
+// Single-path (L = 1) pass: polaris.fastssc.execute_schedule
+// (fastssc.py:20-83) and the first stage of AdaptiveDecoder
+// (listdec.py:437-459).  One warp per frame, lanes over elements; the frame
+// keeps one alpha row per stage and one beta word row per slot in shared
+// memory.
+struct SscLayout {
+    int ch_off;                 // channel LLRs, N elements of T
+    int a_off[kMaxLog];         // alpha stage s (s <= n-2), 2^s elements, contiguous
+    int b_off[kMaxLog];         // beta slot s (s <= n-1), max(1, 2^s / 32) words
+    int root_off;               // codeword x, max(1, N / 32) words
+    int smem_bytes;             // per frame (16-byte multiple)
+};
+
+enum : int { SSC_LIST_L1 = 0, SSC_FAST = 1, SSC_ADAPTIVE = 2 };
+
+struct SscParams {
+    const DOp *prog;
+    int n_ops;
+    const uint32_t *xsyn4;      // codeword-domain CRC syndrome nibble tables
+    const uint32_t *info_pos;   // [k]
+    int N, n, k;
+    int has_crc;
+    uint32_t crc_const;
+    int semantics;              // SSC_*: leaf decisions of the L = 1 list decoder or of fastssc
+    const void *llr;
+    int in_type;
+    long long batch;
+    uint8_t *info_out;          // [B][k] or null
+    uint8_t *crc_ok;            // [B] or null
+    double *pm_out;             // [B] or null
+    int32_t *paths_used;        // [B] or null
+    uint8_t *invoked;           // [B] or null (adaptive: 1 = the list decoder takes the frame)
+    int32_t *fail_idx;          // adaptive: frames whose CRC failed (unordered)
+    int32_t *fail_count;        // adaptive: their number
+    uint32_t *cw_out;           // [B][N/32] packed codeword, or null
+    int fpc;                    // frames (warps) per CTA
+    SscLayout lay;
 };
 
 }  // namespace pb

@@ -31,6 +31,8 @@ extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps
                                         cudaStream_t stream);
 extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, int chg, size_t smem, int fpc, int *blocks_per_sm);
 extern "C" int pb_shape_supported(int mode, int warps, int ppw, int chg);
+extern "C" cudaError_t pb_launch_ssc(const pb::SscParams *p, int mode, int grid, cudaStream_t st);
+extern "C" cudaError_t pb_occupancy_ssc(int mode, int fpc, size_t smem_frame, int *bps);
 
 namespace {
 
@@ -109,6 +111,13 @@ struct pb_handle {
     bool timed = false;
     long long launches = 0;
     std::string plan_json;
+    // single-path pass (L = 1 decodes, adaptive decoding): k_ssc
+    bool ssc_ok = false;
+    pb::SscParams ssc{};
+    int ssc_grid = 0;
+    bool l1_ssc = false;         // route L = 1 decodes through k_ssc
+    int32_t *d_fail = nullptr;   // adaptive: failing frame indices + per-chunk counts
+    size_t d_fail_cap = 0;
 };
 
 namespace {
@@ -450,6 +459,39 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     }
     h->grid = h->sms * h->blocks_per_sm;
 
+    // ---- single-path pass plan (k_ssc): one warp per frame, everything in
+    // shared memory; up to 16 frames per CTA
+    {
+        pb::SscLayout &sl = h->ssc.lay;
+        int off = 0;
+        sl.ch_off = 0;
+        off = align_up(N * es, 16);
+        for (int s = 0; s <= n - 2; ++s) {
+            sl.a_off[s] = off;
+            off = align_up(off + (1 << s) * es, 16);
+        }
+        for (int s = 0; s < n; ++s) {
+            sl.b_off[s] = off;
+            off = align_up(off + std::max(1, (1 << s) / 32) * 4, 16);
+        }
+        sl.root_off = off;
+        off = align_up(off + std::max(1, N / 32) * 4, 16);
+        sl.smem_bytes = off;
+        int sfpc = std::min(16, smem_cap / std::max(1, off));
+        int bps = 0;
+        while (sfpc >= 1) {
+            if (pb_occupancy_ssc(mode, sfpc, off, &bps) == cudaSuccess && bps >= 1) break;
+            --sfpc;
+        }
+        cudaGetLastError();
+        if (sfpc >= 1 && bps >= 1) {
+            h->ssc_ok = true;
+            h->ssc.fpc = sfpc;
+            h->ssc_grid = h->sms * bps;
+        }
+        h->l1_ssc = h->ssc_ok && L == 1 && env_int("PB_L1_LIST", 0) == 0;
+    }
+
     // ---- device tables
     if ((e = cudaMalloc(&h->d_prog, sizeof(pb::DOp) * h->prog.size())) != cudaSuccess ||
         (e = cudaMalloc(&h->d_xsyn4, sizeof(uint32_t) * 128 * std::max(1, N / 32))) != cudaSuccess ||
@@ -514,15 +556,30 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     // slight loss for the short per-op code of L <= 8.
     pr.sync_mask = h->fpc > 1 ? env_int("PB_SYNC_MASK", h->ppw * h->warps >= 16 ? 31 : -1) : -1;
 
+    {
+        pb::SscParams &sp = h->ssc;
+        sp.prog = h->d_prog;
+        sp.n_ops = (int)h->prog.size();
+        sp.xsyn4 = h->d_xsyn4;
+        sp.info_pos = h->d_info;
+        sp.N = N;
+        sp.n = n;
+        sp.k = code->k;
+        sp.has_crc = w != 0;
+        sp.crc_const = crc_const;
+    }
+
     char buf[1024];
     snprintf(buf, sizeof buf,
              "{\"N\": %d, \"k\": %d, \"L\": %d, \"mode\": \"%s\", \"ops\": %d, \"device_ops\": %d, "
              "\"smem_per_frame\": %d, \"alpha_global_from_stage\": %d, \"global_scratch_per_frame\": %d, "
              "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": %d, \"warps_per_frame\": %d, "
-             "\"paths_per_warp\": %d, \"frames_per_cta\": %d, \"channel_in_global\": %d}",
+             "\"paths_per_warp\": %d, \"frames_per_cta\": %d, \"channel_in_global\": %d, "
+             "\"ssc\": {\"smem_per_frame\": %d, \"frames_per_cta\": %d, \"grid\": %d, \"l1_decodes\": %d}}",
              N, code->k, L, mode == PB_MODE_F32 ? "f32" : "int8", n_ops, (int)h->prog.size(),
              lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm * h->fpc, h->sms, h->grid,
-             32 * h->warps * h->fpc, h->warps, h->ppw, h->fpc, (int)h->chg);
+             32 * h->warps * h->fpc, h->warps, h->ppw, h->fpc, (int)h->chg, h->ssc.lay.smem_bytes,
+             h->ssc_ok ? h->ssc.fpc : 0, h->ssc_grid, (int)h->l1_ssc);
     h->plan_json = buf;
     *out = h;
     return PB_OK;
@@ -536,6 +593,7 @@ int pb_destroy(pb_handle *h) {
     cudaFree(h->d_scratch);
     cudaFree(h->d_in);
     cudaFree(h->d_out);
+    cudaFree(h->d_fail);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     for (int j = 0; j < 2; ++j) {
@@ -575,22 +633,99 @@ int ensure(void **p, size_t *cap, size_t need) {
     return PB_OK;
 }
 
+// Output staging regions of a batch in h->d_out: info [B][k], crc_ok [B],
+// pm [B] doubles, paths_used [B] int32, invoked [B].
+struct OutLayout {
+    size_t ok, pm, pu, inv, total;
+    explicit OutLayout(int64_t batch, int k) {
+        const size_t big_info = (size_t)batch * k;
+        ok = (big_info + 255) / 256 * 256;
+        pm = ok + ((size_t)batch + 255) / 256 * 256;
+        pu = pm + (size_t)batch * 8;
+        inv = pu + ((size_t)batch * 4 + 255) / 256 * 256;
+        total = inv + (size_t)batch;
+    }
+};
+
+// Device buffers of one decode call (one chunk of a pipelined call).
+struct Job {
+    const void *llr;
+    int64_t batch;
+    uint8_t *info, *ok, *inv;
+    double *pm;
+    int32_t *pu;
+    int32_t *fail_idx, *fail_count;  // adaptive only
+};
+
+// Launch the kernels of one decode on `st`:
+//   list decode (L >= 2)  k_decode
+//   L = 1                 k_ssc with the list decoder's leaf semantics
+//   adaptive              k_ssc (fastssc semantics) settles the frames whose
+//                         CRC passes and queues the rest; k_decode then takes
+//                         the queued frames (count and rows read on the device)
+int run_kernels(pb_handle *h, const pb::Params &base, int in_type, const Job &j, bool adaptive, cudaStream_t st) {
+    if (j.batch <= 0) return PB_OK;
+    const bool use_ssc = adaptive || h->l1_ssc;
+    if (use_ssc) {
+        if (adaptive) PB_CUDA(cudaMemsetAsync(j.fail_count, 0, sizeof(int32_t), st));
+        pb::SscParams sp = h->ssc;
+        sp.semantics = adaptive ? pb::SSC_ADAPTIVE : pb::SSC_LIST_L1;
+        sp.llr = j.llr;
+        sp.in_type = in_type;
+        sp.batch = j.batch;
+        sp.info_out = j.info;
+        sp.crc_ok = j.ok;
+        sp.pm_out = j.pm;
+        sp.paths_used = j.pu;
+        sp.invoked = j.inv;
+        sp.fail_idx = j.fail_idx;
+        sp.fail_count = j.fail_count;
+        sp.cw_out = nullptr;
+        const int grid = (int)std::min<long long>(h->ssc_grid, (j.batch + sp.fpc - 1) / sp.fpc);
+        cudaError_t e = pb_launch_ssc(&sp, h->mode, grid, st);
+        if (e != cudaSuccess) return cuda_fail(e, "single-path kernel launch");
+        h->launches += 1;
+        if (!adaptive) return PB_OK;
+    }
+    pb::Params pr = base;
+    pr.llr = j.llr;
+    pr.in_type = in_type;
+    pr.batch = j.batch;
+    pr.info_out = j.info;
+    pr.crc_ok = j.ok;
+    pr.pm_out = j.pm;
+    pr.paths_used = j.pu;
+    pr.path_cw = nullptr;
+    pr.path_pm = nullptr;
+    pr.path_crc = nullptr;
+    pr.frame_map = adaptive ? j.fail_idx : nullptr;
+    pr.batch_dev = adaptive ? j.fail_count : nullptr;
+    const int grid = (int)std::min<long long>(h->grid, (j.batch + h->fpc - 1) / h->fpc);
+    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc, st);
+    if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
+    h->launches += 1;
+    return PB_OK;
+}
+
+int ensure_fail(pb_handle *h, int64_t batch, int chunks) {
+    return ensure((void **)&h->d_fail, &h->d_fail_cap, ((size_t)batch + 64 + (size_t)chunks) * sizeof(int32_t));
+}
+
 // Host-buffer decode of a large batch in chunks over two internal streams:
-// chunk i's copy-in overlaps chunk i-1's kernel and copy-out (the copies
+// chunk i's copy-in overlaps chunk i-1's kernels and copy-out (the copies
 // only overlap when the host buffers are pinned).  The user stream orders
 // the whole call; last_kernel_ms spans it.
-int decode_pipelined(pb_handle *h, const pb::Params &base, const void *llr, size_t in_es, int64_t batch,
+int decode_pipelined(pb_handle *h, const pb::Params &base, const void *llr, int in_type, size_t in_es, int64_t batch,
                      long long chunk, uint8_t *info_out, uint8_t *crc_ok, double *pm_out, int32_t *paths_used,
-                     cudaStream_t st) {
+                     uint8_t *invoked, bool adaptive, cudaStream_t st) {
     const size_t in_bytes = (size_t)batch * h->N * in_es;
     int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
     if (rc) return rc;
-    const size_t big_info = (size_t)batch * h->k;
-    const size_t o_ok = (big_info + 255) / 256 * 256;
-    const size_t o_pm = o_ok + ((size_t)batch + 255) / 256 * 256;
-    const size_t o_pu = o_pm + (size_t)batch * 8;
-    rc = ensure((void **)&h->d_out, &h->d_out_cap, o_pu + (size_t)batch * 4);
+    const OutLayout ol(batch, h->k);
+    rc = ensure((void **)&h->d_out, &h->d_out_cap, ol.total);
     if (rc) return rc;
+    const int nchunks = (int)((batch + chunk - 1) / chunk);
+    if (adaptive && (rc = ensure_fail(h, batch, nchunks))) return rc;
     for (int j = 0; j < 2; ++j) {
         if (!h->aux[j]) PB_CUDA(cudaStreamCreateWithFlags(&h->aux[j], cudaStreamNonBlocking));
         if (!h->evj[j]) PB_CUDA(cudaEventCreateWithFlags(&h->evj[j], cudaEventDisableTiming));
@@ -607,24 +742,23 @@ int decode_pipelined(pb_handle *h, const pb::Params &base, const void *llr, size
         const long long nb = std::min<long long>(chunk, batch - f0);
         const size_t io = (size_t)f0 * h->N * in_es, ib = (size_t)nb * h->N * in_es;
         PB_CUDA(cudaMemcpyAsync(din + io, hin + io, ib, cudaMemcpyHostToDevice, sa));
-        pb::Params pc = base;
-        pc.llr = din + io;
-        pc.batch = nb;
-        pc.info_out = info_out ? h->d_out + (size_t)f0 * h->k : nullptr;
-        pc.crc_ok = crc_ok ? h->d_out + o_ok + f0 : nullptr;
-        pc.pm_out = pm_out ? reinterpret_cast<double *>(h->d_out + o_pm) + f0 : nullptr;
-        pc.paths_used = paths_used ? reinterpret_cast<int32_t *>(h->d_out + o_pu) + f0 : nullptr;
-        const int grid = (int)std::min<long long>(h->grid, (nb + h->fpc - 1) / h->fpc);
-        cudaError_t e = pb_launch_decode(&pc, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc, sa);
-        if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
-        h->launches += 1;
+        Job jb{};
+        jb.llr = din + io;
+        jb.batch = nb;
+        jb.info = info_out ? h->d_out + (size_t)f0 * h->k : nullptr;
+        jb.ok = crc_ok ? h->d_out + ol.ok + f0 : nullptr;
+        jb.pm = pm_out ? reinterpret_cast<double *>(h->d_out + ol.pm) + f0 : nullptr;
+        jb.pu = paths_used ? reinterpret_cast<int32_t *>(h->d_out + ol.pu) + f0 : nullptr;
+        jb.inv = invoked ? h->d_out + ol.inv + f0 : nullptr;
+        jb.fail_idx = adaptive ? h->d_fail + f0 : nullptr;
+        jb.fail_count = adaptive ? h->d_fail + batch + 64 + i : nullptr;
+        if ((rc = run_kernels(h, base, in_type, jb, adaptive, sa))) return rc;
         if (info_out)
-            PB_CUDA(cudaMemcpyAsync(info_out + (size_t)f0 * h->k, pc.info_out, (size_t)nb * h->k,
-                                    cudaMemcpyDeviceToHost, sa));
-        if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok + f0, pc.crc_ok, (size_t)nb, cudaMemcpyDeviceToHost, sa));
-        if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out + f0, pc.pm_out, (size_t)nb * 8, cudaMemcpyDeviceToHost, sa));
-        if (paths_used)
-            PB_CUDA(cudaMemcpyAsync(paths_used + f0, pc.paths_used, (size_t)nb * 4, cudaMemcpyDeviceToHost, sa));
+            PB_CUDA(cudaMemcpyAsync(info_out + (size_t)f0 * h->k, jb.info, (size_t)nb * h->k, cudaMemcpyDeviceToHost, sa));
+        if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok + f0, jb.ok, (size_t)nb, cudaMemcpyDeviceToHost, sa));
+        if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out + f0, jb.pm, (size_t)nb * 8, cudaMemcpyDeviceToHost, sa));
+        if (paths_used) PB_CUDA(cudaMemcpyAsync(paths_used + f0, jb.pu, (size_t)nb * 4, cudaMemcpyDeviceToHost, sa));
+        if (invoked) PB_CUDA(cudaMemcpyAsync(invoked + f0, jb.inv, (size_t)nb, cudaMemcpyDeviceToHost, sa));
     }
     for (int j = 0; j < 2; ++j) {
         PB_CUDA(cudaEventRecord(h->evj[j], h->aux[j]));
@@ -634,6 +768,16 @@ int decode_pipelined(pb_handle *h, const pb::Params &base, const void *llr, size
     h->timed = true;
     PB_CUDA(cudaStreamSynchronize(st));
     PB_CUDA(cudaGetLastError());
+    return PB_OK;
+}
+
+int launch_timed(pb_handle *h, const pb::Params &base, int in_type, const Job &j, bool adaptive, cudaStream_t st) {
+    if (j.batch <= 0) return PB_OK;
+    PB_CUDA(cudaEventRecord(h->ev0, st));
+    int rc = run_kernels(h, base, in_type, j, adaptive, st);
+    if (rc) return rc;
+    PB_CUDA(cudaEventRecord(h->ev1, st));
+    h->timed = true;
     return PB_OK;
 }
 
@@ -649,75 +793,84 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
     return PB_OK;
 }
 
-}  // namespace
-
-
-extern "C" int pb_decode(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *info_out,
-                         uint8_t *crc_ok, double *pm_out, int32_t *paths_used, void *stream) {
+int decode_impl(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *info_out, uint8_t *crc_ok,
+                double *pm_out, int32_t *paths_used, uint8_t *invoked, bool adaptive, void *stream) {
     g_err.clear();
     if (!h) return fail(PB_EINVAL, "null handle");
     if (batch < 0) return fail(PB_EINVAL, "negative batch");
     if (in_type != PB_IN_F32 && in_type != PB_IN_I8) return fail(PB_EINVAL, "unknown input type");
     if (in_type == PB_IN_I8 && h->mode != PB_MODE_INT8)
         return fail(PB_EINVAL, "int8 LLR input needs an int8-mode decoder");
+    if (adaptive && !h->base.has_crc) return fail(PB_EINVAL, "adaptive decoding needs a CRC in the code spec");
+    if (adaptive && !h->ssc_ok)
+        return fail(PB_EINVAL, "code too large for the single-path pass's shared-memory plan");
     if (batch == 0) return PB_OK;
     if (!llr) return fail(PB_EINVAL, "null LLR pointer");
     PB_CUDA(cudaSetDevice(h->device));
     cudaStream_t st = (cudaStream_t)stream;
     const size_t in_es = in_type == PB_IN_F32 ? 4 : 1;
     const size_t in_bytes = (size_t)batch * h->N * in_es;
-    pb::Params pr = h->base;
-    pr.in_type = in_type;
-    pr.batch = batch;
-    pr.path_cw = nullptr;
-    pr.path_pm = nullptr;
-    pr.path_crc = nullptr;
 
     const bool dev_in = is_device_ptr(llr);
     const bool all_dev = dev_in && (!info_out || is_device_ptr(info_out)) && (!crc_ok || is_device_ptr(crc_ok)) &&
-                         (!pm_out || is_device_ptr(pm_out)) && (!paths_used || is_device_ptr(paths_used));
+                         (!pm_out || is_device_ptr(pm_out)) && (!paths_used || is_device_ptr(paths_used)) &&
+                         (!invoked || is_device_ptr(invoked));
     if (all_dev) {
-        pr.llr = llr;
-        pr.info_out = info_out;
-        pr.crc_ok = crc_ok;
-        pr.pm_out = pm_out;
-        pr.paths_used = paths_used;
-        return launch(h, pr, st);
+        int rc = adaptive ? ensure_fail(h, batch, 1) : PB_OK;
+        if (rc) return rc;
+        Job jb{llr, batch, info_out, crc_ok, invoked, pm_out, paths_used,
+               adaptive ? h->d_fail : nullptr, adaptive ? h->d_fail + batch + 64 : nullptr};
+        return launch_timed(h, h->base, in_type, jb, adaptive, st);
     }
     // staged path: host buffers in and/or out
     const long long chunk = std::max<long long>(1, env_int("PB_CHUNK_FRAMES", std::max(4096, 6 * h->grid * h->fpc)));
-    if (!dev_in && batch > chunk) return decode_pipelined(h, pr, llr, in_es, batch, chunk, info_out, crc_ok, pm_out,
-                                                          paths_used, st);
+    if (!dev_in && batch > chunk)
+        return decode_pipelined(h, h->base, llr, in_type, in_es, batch, chunk, info_out, crc_ok, pm_out, paths_used,
+                                invoked, adaptive, st);
+    const void *dllr = llr;
     if (!dev_in) {
         int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
         if (rc) return rc;
         PB_CUDA(cudaMemcpyAsync(h->d_in, llr, in_bytes, cudaMemcpyHostToDevice, st));
-        pr.llr = h->d_in;
-    } else {
-        pr.llr = llr;
+        dllr = h->d_in;
     }
-    const size_t big_info = (size_t)batch * h->k;
-    const size_t o_info = 0;
-    const size_t o_ok = (big_info + 255) / 256 * 256;
-    const size_t o_pm = o_ok + ((size_t)batch + 255) / 256 * 256;
-    const size_t o_pu = o_pm + (size_t)batch * 8;
-    const size_t total = o_pu + (size_t)batch * 4;
-    int rc = ensure((void **)&h->d_out, &h->d_out_cap, total);
+    const OutLayout ol(batch, h->k);
+    int rc = ensure((void **)&h->d_out, &h->d_out_cap, ol.total);
     if (rc) return rc;
-    pr.info_out = info_out ? h->d_out + o_info : nullptr;
-    pr.crc_ok = crc_ok ? h->d_out + o_ok : nullptr;
-    pr.pm_out = pm_out ? reinterpret_cast<double *>(h->d_out + o_pm) : nullptr;
-    pr.paths_used = paths_used ? reinterpret_cast<int32_t *>(h->d_out + o_pu) : nullptr;
-    rc = launch(h, pr, st);
+    if (adaptive && (rc = ensure_fail(h, batch, 1))) return rc;
+    Job jb{};
+    jb.llr = dllr;
+    jb.batch = batch;
+    jb.info = info_out ? h->d_out : nullptr;
+    jb.ok = crc_ok ? h->d_out + ol.ok : nullptr;
+    jb.pm = pm_out ? reinterpret_cast<double *>(h->d_out + ol.pm) : nullptr;
+    jb.pu = paths_used ? reinterpret_cast<int32_t *>(h->d_out + ol.pu) : nullptr;
+    jb.inv = invoked ? h->d_out + ol.inv : nullptr;
+    jb.fail_idx = adaptive ? h->d_fail : nullptr;
+    jb.fail_count = adaptive ? h->d_fail + batch + 64 : nullptr;
+    rc = launch_timed(h, h->base, in_type, jb, adaptive, st);
     if (rc) return rc;
-    if (info_out) PB_CUDA(cudaMemcpyAsync(info_out, pr.info_out, big_info, cudaMemcpyDeviceToHost, st));
-    if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok, pr.crc_ok, (size_t)batch, cudaMemcpyDeviceToHost, st));
-    if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out, pr.pm_out, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
-    if (paths_used)
-        PB_CUDA(cudaMemcpyAsync(paths_used, pr.paths_used, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+    if (info_out) PB_CUDA(cudaMemcpyAsync(info_out, jb.info, (size_t)batch * h->k, cudaMemcpyDeviceToHost, st));
+    if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok, jb.ok, (size_t)batch, cudaMemcpyDeviceToHost, st));
+    if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out, jb.pm, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
+    if (paths_used) PB_CUDA(cudaMemcpyAsync(paths_used, jb.pu, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+    if (invoked) PB_CUDA(cudaMemcpyAsync(invoked, jb.inv, (size_t)batch, cudaMemcpyDeviceToHost, st));
     PB_CUDA(cudaStreamSynchronize(st));
     PB_CUDA(cudaGetLastError());
     return PB_OK;
+}
+
+}  // namespace
+
+extern "C" int pb_decode(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *info_out,
+                         uint8_t *crc_ok, double *pm_out, int32_t *paths_used, void *stream) {
+    return decode_impl(h, llr, in_type, batch, info_out, crc_ok, pm_out, paths_used, nullptr, false, stream);
+}
+
+extern "C" int pb_decode_adaptive(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *info_out,
+                                  uint8_t *crc_ok, double *pm_out, int32_t *paths_used, uint8_t *invoked_list,
+                                  void *stream) {
+    return decode_impl(h, llr, in_type, batch, info_out, crc_ok, pm_out, paths_used, invoked_list, true, stream);
 }
 
 // Debug: decode `batch` host frames and return the clock64 cycles each device
@@ -808,5 +961,54 @@ extern "C" int pb_decode_paths(pb_handle *h, const void *llr, int in_type, int64
     const int N = h->N;
     for (size_t r = 0; r < (size_t)batch * L; ++r)
         for (int i = 0; i < N; ++i) codewords[r * N + i] = (uint8_t)((cw[r * rw + (i >> 5)] >> (i & 31)) & 1u);
+    return PB_OK;
+}
+
+// polaris.fastssc.execute_schedule (fastssc.py:20-83): the single-path
+// pass alone.  Host buffers only; synchronous.
+extern "C" int pb_fastssc(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *codewords,
+                          double *pm_out, void *stream) {
+    g_err.clear();
+    if (!h) return fail(PB_EINVAL, "null handle");
+    if (batch < 0) return fail(PB_EINVAL, "negative batch");
+    if (in_type != PB_IN_F32 && in_type != PB_IN_I8) return fail(PB_EINVAL, "unknown input type");
+    if (in_type == PB_IN_I8 && h->mode != PB_MODE_INT8)
+        return fail(PB_EINVAL, "int8 LLR input needs an int8-mode decoder");
+    if (!h->ssc_ok) return fail(PB_EINVAL, "code too large for the single-path pass's shared-memory plan");
+    if (batch == 0) return PB_OK;
+    if (!llr || !codewords || !pm_out) return fail(PB_EINVAL, "null pointer");
+    PB_CUDA(cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = h->N, nwd = std::max(1, N / 32);
+    const size_t in_bytes = (size_t)batch * N * (in_type == PB_IN_F32 ? 4 : 1);
+    int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
+    if (rc) return rc;
+    const size_t n_cw = (size_t)batch * nwd * 4, o_pm = (n_cw + 255) / 256 * 256;
+    rc = ensure((void **)&h->d_out, &h->d_out_cap, o_pm + (size_t)batch * 8);
+    if (rc) return rc;
+    PB_CUDA(cudaMemcpyAsync(h->d_in, llr, in_bytes, cudaMemcpyHostToDevice, st));
+    pb::SscParams sp = h->ssc;
+    sp.semantics = pb::SSC_FAST;
+    sp.llr = h->d_in;
+    sp.in_type = in_type;
+    sp.batch = batch;
+    sp.info_out = nullptr;
+    sp.crc_ok = nullptr;
+    sp.pm_out = reinterpret_cast<double *>(h->d_out + o_pm);
+    sp.paths_used = nullptr;
+    sp.invoked = nullptr;
+    sp.fail_idx = nullptr;
+    sp.fail_count = nullptr;
+    sp.cw_out = reinterpret_cast<uint32_t *>(h->d_out);
+    const int grid = (int)std::min<long long>(h->ssc_grid, (batch + sp.fpc - 1) / sp.fpc);
+    cudaError_t e = pb_launch_ssc(&sp, h->mode, grid, st);
+    if (e != cudaSuccess) return cuda_fail(e, "single-path kernel launch");
+    h->launches += 1;
+    std::vector<uint32_t> cw((size_t)batch * nwd);
+    PB_CUDA(cudaMemcpyAsync(cw.data(), sp.cw_out, n_cw, cudaMemcpyDeviceToHost, st));
+    PB_CUDA(cudaMemcpyAsync(pm_out, sp.pm_out, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
+    PB_CUDA(cudaStreamSynchronize(st));
+    for (size_t r = 0; r < (size_t)batch; ++r)
+        for (int i = 0; i < N; ++i) codewords[r * N + i] = (uint8_t)((cw[r * nwd + (i >> 5)] >> (i & 31)) & 1u);
     return PB_OK;
 }

@@ -21,8 +21,8 @@ from .channel import clamp_llr
 from .encode import extract_payload, polar_encode
 from .schedule import Schedule
 
-__all__ = ["DecodeResult", "PathOutcome", "BatchResult", "select_candidates",
-           "ListDecoder", "decode"]
+__all__ = ["DecodeResult", "PathOutcome", "BatchResult", "AdaptiveBatchResult",
+           "select_candidates", "ListDecoder", "AdaptiveDecoder", "decode"]
 
 
 @dataclass(eq=False)
@@ -55,6 +55,14 @@ class BatchResult:
     crc_ok: np.ndarray      # [B] bool
     chosen_pm: np.ndarray   # [B] float64
     paths_used: np.ndarray  # [B] int32
+
+
+@dataclass(eq=False)
+class AdaptiveBatchResult(BatchResult):
+    """``AdaptiveDecoder.decode_batch`` output: ``BatchResult`` plus, per
+    frame, whether the list decoder was invoked."""
+
+    invoked_list: np.ndarray = None  # [B] bool
 
 
 def select_candidates(pools, list_size: int):
@@ -289,6 +297,83 @@ class ListDecoder:
             out.append(PathOutcome(codeword=codeword, u=u, info_bits=payload,
                                    pm=float(pm[0, t]), crc_ok=crc_ok))
         return out
+
+
+class AdaptiveDecoder:
+    """Single-path pass first; the full list only on CRC failure
+    (reference ``listdec.py:437-459``).
+
+    On the GPU both stages run back to back on one stream: the single-path
+    kernel settles every frame whose CRC passes and queues the others on the
+    device, and the list kernel decodes the queued frames.  Results equal the
+    reference's per frame: the Fast-SSC result (``paths_used`` 1,
+    ``invoked_list`` False) when its CRC passes, else the list decoder's.
+    """
+
+    def __init__(self, schedule: Schedule, list_size: int, *, mode: str = "f32",
+                 device: int = 0):
+        if schedule.spec.crc is None:
+            raise ValueError("adaptive decoding needs a CRC in the code spec")
+        self.schedule = schedule
+        self.list_size = list_size
+        self._list = ListDecoder(schedule, list_size, mode=mode, device=device)
+        self.spec = schedule.spec
+
+    @property
+    def launches(self) -> int:
+        return self._list.launches
+
+    def last_kernel_ms(self) -> float:
+        return self._list.last_kernel_ms()
+
+    def decode_batch(self, llrs, stream=None,
+                     out: "AdaptiveBatchResult | None" = None) -> AdaptiveBatchResult:
+        """Decode a [B, N] batch of host frames; one result row per frame."""
+        keep, ptr, in_type, B = self._list._frames(llrs)
+        k = self.spec.k
+        if out is None:
+            out = AdaptiveBatchResult(np.empty((B, k), np.uint8), np.empty(B, np.bool_),
+                                      np.empty(B, np.float64), np.empty(B, np.int32),
+                                      np.empty(B, np.bool_))
+        rc = _native.lib().pb_decode_adaptive(
+            self._list._h, ctypes.c_void_p(ptr), in_type, B, _addr(out.info_bits),
+            _addr(out.crc_ok), _addr(out.chosen_pm), _addr(out.paths_used),
+            _addr(out.invoked_list), ctypes.c_void_p(stream) if stream else None)
+        _native.check(rc, "pb_decode_adaptive")
+        del keep
+        return out
+
+    def decode_device(self, llrs, info_out=None, crc_ok=None, pm_out=None, paths_used=None,
+                      invoked_list=None, stream=None) -> None:
+        """Device-resident torch tensors, asynchronous on ``stream``."""
+        import torch
+        if llrs.dim() != 2 or llrs.shape[1] != self.spec.N:
+            raise ValueError(f"LLR frame has {llrs.shape[-1]} values, spec wants {self.spec.N}")
+        if not llrs.is_cuda or not llrs.is_contiguous():
+            raise ValueError("decode_device needs a contiguous CUDA tensor")
+        in_type = _native.PB_IN_I8 if llrs.dtype == torch.int8 else _native.PB_IN_F32
+        if llrs.dtype not in (torch.int8, torch.float32):
+            raise ValueError(f"unsupported LLR dtype {llrs.dtype}")
+        if stream is None:
+            stream = torch.cuda.current_stream(llrs.device).cuda_stream
+
+        def p(t):
+            return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+        rc = _native.lib().pb_decode_adaptive(self._list._h, p(llrs), in_type, llrs.shape[0],
+                                              p(info_out), p(crc_ok), p(pm_out), p(paths_used),
+                                              p(invoked_list),
+                                              ctypes.c_void_p(stream) if stream else None)
+        _native.check(rc, "pb_decode_adaptive")
+
+    def decode(self, llr) -> DecodeResult:
+        a = np.asarray(llr).ravel()
+        if a.size != self.spec.N:
+            raise ValueError(f"LLR frame has {a.size} values, spec wants {self.spec.N}")
+        r = self.decode_batch(a[None, :])
+        return DecodeResult(info_bits=r.info_bits[0], crc_ok=bool(r.crc_ok[0]),
+                            chosen_pm=float(r.chosen_pm[0]), paths_used=int(r.paths_used[0]),
+                            invoked_list=bool(r.invoked_list[0]))
 
 
 def decode(llr, schedule: Schedule, list_size: int) -> DecodeResult:

@@ -49,3 +49,21 @@ def expected(case, arrays):
         out["path_pm"] = arrays[f"{key}.path_pm"]
         out["path_crc"] = arrays[f"{key}.path_crc"].astype(bool)
     return out
+
+
+def load_adaptive():
+    """Reference fastssc.execute_schedule + AdaptiveDecoder fixtures
+    (tests/golden/make_golden_adaptive.py)."""
+    with open(os.path.join(HERE, "reference_adaptive.json")) as fh:
+        cases = json.load(fh)["cases"]
+    return cases, np.load(os.path.join(HERE, "reference_adaptive.npz"))
+
+
+def expected_adaptive(case, arrays):
+    key, k, N = case["name"], case["k"], case["N"]
+    return dict(ssc_cw=np.unpackbits(arrays[f"{key}.ssc_codeword"], axis=1)[:, :N],
+                ssc_pm=arrays[f"{key}.ssc_pm"],
+                info=np.unpackbits(arrays[f"{key}.info"], axis=1)[:, :k],
+                crc_ok=arrays[f"{key}.crc_ok"].astype(bool), pm=arrays[f"{key}.pm"],
+                paths_used=arrays[f"{key}.paths_used"],
+                invoked=arrays[f"{key}.invoked_list"].astype(bool))
