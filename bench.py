@@ -37,12 +37,18 @@ CONFIGS = {
     # name: (N, K incl. CRC, crc, design Eb/N0, L, Eb/N0, mode, label)
     "c1_L4": (1024, 512, "crc8_d5", 2.0, 4, 2.5, "f32", "c1"),
     "c2_L8": (1024, 860, "crc32", 4.0, 8, 4.0, "f32", "c2"),
+    "c3_L1": (2048, 1723, "crc32", 4.0, 1, 4.0, "f32", "c3"),  # single-path pass (k_ssc)
     "c3_L2": (2048, 1723, "crc32", 4.0, 2, 4.0, "f32", "c3"),
     "c3_L8": (2048, 1723, "crc32", 4.0, 8, 4.0, "f32", "c3"),
     "c3_L32": (2048, 1723, "crc32", 4.0, 32, 4.0, "f32", "c3"),
     "c4_int8_L32": (2048, 1723, "crc32", 4.0, 32, 4.0, "int8", "c4"),
     "c5_L16": (8192, 6144, "crc32", 3.0, 16, 3.0, "f32", "c5"),
 }
+# adaptive decoding (reference AdaptiveDecoder listdec.py:437-459):
+# the single-path pass first, the list only for CRC failures -- the decoder
+# behind the paper's headline throughput table; not the north-star metric
+for _base in ("c1_L4", "c2_L8", "c3_L8", "c3_L32", "c4_int8_L32", "c5_L16"):
+    CONFIGS[_base + "_adaptive"] = CONFIGS[_base]
 DEFAULT_CONFIG = "c3_L32"
 METRIC = "decoded info Gbit/s, Fast-SSC list-CRC (2048,1723) L=32; FER parity vs oracle"
 
@@ -157,20 +163,21 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def oracle_rate(schedule, L, llrs, mode, seconds: float):
+def oracle_rate(schedule, L, llrs, mode, seconds: float, adaptive: bool = False):
     """Info bits/s of the CPU oracle port on all host threads over a bounded
     sample (calibrated to ~`seconds` of work)."""
     from oracle import oracle
     threads = cpu_threads()
     int8 = mode == "int8"
     feed = pb.quantize_int8(llrs).astype(np.float32) if int8 else llrs
-    probe = min(len(feed), max(threads, 2 * threads))
+    run = oracle.adaptive_batch if adaptive else oracle.decode_batch
+    probe = min(len(feed), max(threads, 2 * threads) * (16 if adaptive else 1))
     t0 = time.perf_counter()
-    oracle.decode_batch(schedule, L, feed[:probe], int8=int8, threads=threads)
+    run(schedule, L, feed[:probe], int8=int8, threads=threads)
     dt = time.perf_counter() - t0
     n = int(min(len(feed), max(probe, probe * seconds / max(dt, 1e-6))))
     t0 = time.perf_counter()
-    oracle.decode_batch(schedule, L, feed[:n], int8=int8, threads=threads)
+    run(schedule, L, feed[:n], int8=int8, threads=threads)
     dt = time.perf_counter() - t0
     return n * schedule.spec.k / dt, n, threads, dt
 
@@ -191,7 +198,8 @@ def run_reference(args):
     # per-step sample: ~args.ref_step_s seconds of oracle work on all threads
     pool = pb.generate_frames(spec, ebn0, seed=args.seed, start=0,
                               count=max(4 * threads, 256))
-    rate, n, threads, _ = oracle_rate(sch, L, pool.llrs, mode, 2.0)
+    adaptive = args.config.endswith("_adaptive")
+    rate, n, threads, _ = oracle_rate(sch, L, pool.llrs, mode, 2.0, adaptive)
     per_step = int(max(threads, min(len(pool.llrs) * 64, rate / spec.k * args.ref_step_s)))
     if per_step > len(pool.llrs):
         pool = pb.generate_frames(spec, ebn0, seed=args.seed, start=0, count=per_step)
@@ -201,7 +209,8 @@ def run_reference(args):
     times = []
     for step in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.decode_batch(sch, L, feed[:per_step], int8=int8, threads=threads)
+        (oracle.adaptive_batch if adaptive else oracle.decode_batch)(
+            sch, L, feed[:per_step], int8=int8, threads=threads)
         if step >= args.warmup:
             times.append(time.perf_counter() - t0)
     total = sum(times)
@@ -223,9 +232,16 @@ def run_reference(args):
     return 0
 
 
+def metric_of(cfg):
+    if cfg.endswith("_adaptive"):
+        return "decoded info Gbit/s, adaptive Fast-SSC + list-CRC (SSC pass, list on CRC failure)"
+    return METRIC
+
+
 def config_dict(args, spec, L, ebn0, mode, label, batch):
+    dec = "adaptive (single-path pass, list on CRC failure), " if args.config.endswith("_adaptive") else ""
     return {"workload": f"{label}: polar ({spec.N},{spec.k_total}) incl. CRC-{spec.crc_width}"
-                        f" (payload {spec.k}), L={L}, {mode}, Eb/N0={ebn0} dB",
+                        f" (payload {spec.k}), {dec}L={L}, {mode}, Eb/N0={ebn0} dB",
             "config_key": args.config, "N": spec.N, "K": spec.k_total, "k_payload": spec.k,
             "list_size": L, "mode": mode, "ebn0_db": ebn0, "batch_frames": batch,
             "l2": "inputs larger than L2 (batch LLRs > 126 MB)"}
@@ -266,11 +282,19 @@ def main():
     okd = torch.empty(B, dtype=torch.uint8, device=dev)
     pmd = torch.empty(B, dtype=torch.float64, device=dev)
     pud = torch.empty(B, dtype=torch.int32, device=dev)
-    dec = pb.ListDecoder(sch, L, mode=mode, device=local)
+    invd = torch.empty(B, dtype=torch.uint8, device=dev)
+    adaptive = args.config.endswith("_adaptive")
+    if adaptive:
+        dec = pb.AdaptiveDecoder(sch, L, mode=mode, device=local)
+    else:
+        dec = pb.ListDecoder(sch, L, mode=mode, device=local)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        dec.decode_device(llr_dev, info, okd, pmd, pud)
+        if adaptive:
+            dec.decode_device(llr_dev, info, okd, pmd, pud, invd)
+        else:
+            dec.decode_device(llr_dev, info, okd, pmd, pud)
 
     for _ in range(args.warmup):
         step()
@@ -309,7 +333,8 @@ def main():
     ok_h = torch.empty(B, dtype=torch.uint8).pin_memory()
     pm_h = torch.empty(B, dtype=torch.float64).pin_memory()
     pu_h = torch.empty(B, dtype=torch.int32).pin_memory()
-    out_h = pb.BatchResult(info_h, ok_h, pm_h, pu_h)
+    out_h = (pb.AdaptiveBatchResult(info_h, ok_h, pm_h, pu_h, torch.empty(B, dtype=torch.uint8).pin_memory())
+             if adaptive else pb.BatchResult(info_h, ok_h, pm_h, pu_h))
     e2e_steps = max(1, min(args.steps, 5))
     dec.decode_batch(llr_host, out=out_h)
     if world > 1:
@@ -330,7 +355,11 @@ def main():
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         W = lane_ops_per_frame(sch, L)
-        kernel_ms = total_ms / max(1, launches) if world == 1 else float(np.mean(step_ms))
+        inv_frac = float(invd.float().mean()) if adaptive else 1.0
+        if adaptive:  # single-path work for every frame + list work for the invoked ones
+            W = lane_ops_per_frame(sch, 1) + inv_frac * W
+        kernel_ms = (total_ms / max(1, launches) if world == 1 and not adaptive
+                     else total_ms / args.steps)
         achieved = W * B / (kernel_ms * 1e-3) / 1e9           # G lane-ops/s, one GPU
         peak = sms * 128 * sm_mhz * 1e6 / 1e9
         hbm_bytes = B * (spec.N * 4 + spec.k + 13)
@@ -345,7 +374,7 @@ def main():
             except Exception:
                 traffic = None
         line = {
-            "metric": METRIC, "value": value, "unit": "Gbit/s", "n_gpus": world,
+            "metric": metric_of(args.config), "value": value, "unit": "Gbit/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if mode == "f32" else "int8",
@@ -358,7 +387,7 @@ def main():
             "gpu_launches": int(launches),
             "e2e": {"value": frames_all * e2e_steps * spec.k / e2e_s / 1e9, "unit": "Gbit/s",
                     "h2d_bytes_per_step": B * spec.N * 4,
-                    "d2h_bytes_per_step": B * (spec.k + 1 + 8 + 4)},
+                    "d2h_bytes_per_step": B * (spec.k + 1 + 8 + 4 + (1 if adaptive else 0))},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Glane-op/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "work_per_frame_lane_ops": W,
@@ -366,15 +395,17 @@ def main():
                                       f"(sm_max_mhz, {peak_kind}); SURVEY 8(d) ALU-issue roofline",
                          "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / float(peaks.get("hbm_gbs", 6650.0))},
             "clocks": clocks.summary(),
-            "plan": json.loads(dec.plan),
+            "plan": json.loads((dec._list if adaptive else dec).plan),
         }
         if not args.no_cpu_baseline:
-            rate, n, threads, dt = oracle_rate(sch, L, frames.llrs, mode, args.cpu_seconds)
+            rate, n, threads, dt = oracle_rate(sch, L, frames.llrs, mode, args.cpu_seconds, adaptive)
             line["cpu_baseline"] = {"value": rate / 1e9, "unit": "Gbit/s", "cores": threads,
                                     "kind": "port",
                                     "sample": f"{n} frames of the same batch through "
                                               f"oracle/libpolar_oracle.so ({dt:.1f} s, "
                                               f"{threads} threads)"}
+        if adaptive:
+            line["list_invoked_frac"] = inv_frac
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
