@@ -125,6 +125,25 @@ int pb_decode_adaptive(pb_handle *h, const void *llr, int in_type, int64_t batch
 int pb_fastssc(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *codewords,
                double *pm_out, void *stream);
 
+/* On-device frame generation for throughput sweeps: frames
+ * first_frame .. first_frame+count-1 of the (seed, Eb/N0) stream for this
+ * handle's code -- payload bits, CRC attach (encode.py:56-73), polar encode
+ * (encode.py:29-53), BPSK-AWGN LLRs 2y/sigma^2 clamped (sim.py:79-91).
+ * Counter-based Philox4x32-10 per frame: shard- and batch-split invariant,
+ * statistically equivalent to (not bit-identical with) the reference's numpy
+ * stream.  llr_out [count][N] float32 (out_type PB_IN_F32) or int8
+ * (PB_IN_I8, clip(rint(4 llr), +-127)); payload_out [count][ceil(k/32)]
+ * packed bits or NULL.  Device buffers; asynchronous on `stream`. */
+int pb_generate_frames(pb_handle *h, uint64_t seed, double ebn0_db, int64_t first_frame, int64_t count,
+                       int out_type, void *llr_out, uint32_t *payload_out, void *stream);
+
+/* Frame / bit error counters (sim.py:_chunk_counts) of decoded payload bytes
+ * info [batch][k] against packed payloads [batch][ceil(k/32)], ADDED per
+ * chunk of `chunk` frames into counts [ceil(batch/chunk)][3] uint64 =
+ * (frames, frame errors, bit errors).  Device buffers; async on `stream`. */
+int pb_count_errors(pb_handle *h, const uint8_t *info, const uint32_t *payload, int64_t batch, int chunk,
+                    uint64_t *counts, void *stream);
+
 /* Release the handle and its device memory. */
 int pb_destroy(pb_handle *h);
 

@@ -18,6 +18,7 @@ from .channel import (LLR_CLAMP, ChannelConfig, clamp_llr, frame_rng, generate_f
 from .listdec import (AdaptiveBatchResult, AdaptiveDecoder, BatchResult, DecodeResult,
                       ListDecoder, PathOutcome, decode, select_candidates)
 from .fastssc import execute_schedule
+from .sim import CSV_FIELDS, DeviceFrames, SimRecord, run_sweep, write_csv
 
 __version__ = "0.1.0"
 
@@ -32,5 +33,6 @@ __all__ = [
     "quantize_int8", "transmit",
     "AdaptiveBatchResult", "AdaptiveDecoder", "BatchResult", "DecodeResult", "ListDecoder",
     "PathOutcome", "decode", "execute_schedule",
+    "CSV_FIELDS", "DeviceFrames", "SimRecord", "run_sweep", "write_csv",
     "select_candidates", "__version__",
 ]

@@ -28,6 +28,7 @@ PB_MODE_F32, PB_MODE_INT8 = 0, 1
 PB_IN_F32, PB_IN_I8 = 0, 1
 
 EXPORTS = ("pb_create", "pb_decode", "pb_decode_paths", "pb_decode_adaptive", "pb_fastssc",
+           "pb_generate_frames", "pb_count_errors",
            "pb_destroy", "pb_last_error",
            "pb_plan_json", "pb_launch_count", "pb_last_kernel_ms", "pb_version")
 
@@ -92,7 +93,7 @@ def build(verbose: bool = False, jobs: int | None = None, profile: bool = False)
         if _stale(obj, [inst, *hdrs]):
             cmds.append(["nvcc", *NVCC_FLAGS, *extra, "-I", INCLUDE, f"-DPB_T={t}", f"-DPB_W={w}",
                          f"-DPB_PPW={ppw}", f"-DPB_CHG={chg}", f"-DPB_TAG={tag}", "-c", inst, "-o", obj])
-    for src in ("dispatch.cu", "runtime.cu", "ssc_kernel.cu"):
+    for src in ("dispatch.cu", "runtime.cu", "ssc_kernel.cu", "frame_gen.cu"):
         obj = os.path.join(BUILD_DIR, src.replace(".cu", ".o"))
         objs.append(obj)
         if _stale(obj, [os.path.join(CSRC, src), *hdrs]):
@@ -142,6 +143,10 @@ def lib():
     L.pb_decode_adaptive.argtypes = [vp, vp, i32, i64, vp, vp, vp, vp, vp, vp]
     L.pb_fastssc.restype = i32
     L.pb_fastssc.argtypes = [vp, vp, i32, i64, vp, vp, vp]
+    L.pb_generate_frames.restype = i32
+    L.pb_generate_frames.argtypes = [vp, ctypes.c_uint64, ctypes.c_double, i64, i64, i32, vp, vp, vp]
+    L.pb_count_errors.restype = i32
+    L.pb_count_errors.argtypes = [vp, vp, vp, i64, i32, vp, vp]
     L.pb_destroy.restype = i32
     L.pb_destroy.argtypes = [vp]
     L.pb_last_error.restype = ctypes.c_char_p

@@ -136,4 +136,21 @@ struct SscParams {
     SscLayout lay;
 };
 
+// On-device frame generation (frame_gen.cu)
+namespace gen {
+struct GenParams {
+    int N, n, k, crc_w;
+    const uint32_t *info_pos;   // [k + crc_w] u positions (payload, then CRC)
+    const uint32_t *hu;         // [k] CRC syndrome row of payload bit j
+    uint32_t crc_const;
+    unsigned long long seed;
+    long long first, count;
+    float sigma, scale;         // noise std, LLR scale 2 / sigma^2
+    int out_type;               // 0 float32, 1 int8
+    void *llr;                  // [count][N]
+    uint32_t *payload;          // [count][kw] packed bits (bit i of word i/32), or null
+    int kw;
+};
+}  // namespace gen
+
 }  // namespace pb

@@ -33,6 +33,10 @@ extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, int chg, size_
 extern "C" int pb_shape_supported(int mode, int warps, int ppw, int chg);
 extern "C" cudaError_t pb_launch_ssc(const pb::SscParams *p, int mode, int grid, cudaStream_t st);
 extern "C" cudaError_t pb_occupancy_ssc(int mode, int fpc, size_t smem_frame, int *bps);
+extern "C" cudaError_t pb_launch_gen(const pb::gen::GenParams *p, int sms, cudaStream_t st);
+extern "C" cudaError_t pb_launch_errcount(const uint8_t *info, const uint32_t *payload, long long batch, int k, int kw,
+                                       int chunk, unsigned long long *counts, int sms, cudaStream_t st);
+#include <cmath>
 
 namespace {
 
@@ -118,6 +122,10 @@ struct pb_handle {
     bool l1_ssc = false;         // route L = 1 decodes through k_ssc
     int32_t *d_fail = nullptr;   // adaptive: failing frame indices + per-chunk counts
     size_t d_fail_cap = 0;
+    // on-device frame generation: all K info positions, payload syndrome rows
+    uint32_t *d_info_all = nullptr, *d_hu = nullptr;
+    int crc_w = 0;
+    uint32_t gen_crc_const = 0;
 };
 
 namespace {
@@ -500,6 +508,19 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         return cuda_fail(e, "cudaMalloc tables");
     }
     std::vector<uint32_t> info_k(info.begin(), info.begin() + code->k);
+    {
+        std::vector<uint32_t> all(info.begin(), info.end()), hu(code->k);
+        for (int j = 0; j < code->k; ++j) hu[j] = Hu[info[j]];
+        if ((e = cudaMalloc(&h->d_info_all, sizeof(uint32_t) * all.size())) != cudaSuccess ||
+            (e = cudaMalloc(&h->d_hu, sizeof(uint32_t) * std::max<size_t>(1, hu.size()))) != cudaSuccess) {
+            pb_destroy(h);
+            return cuda_fail(e, "cudaMalloc generator tables");
+        }
+        cudaMemcpy(h->d_info_all, all.data(), sizeof(uint32_t) * all.size(), cudaMemcpyHostToDevice);
+        cudaMemcpy(h->d_hu, hu.data(), sizeof(uint32_t) * hu.size(), cudaMemcpyHostToDevice);
+        h->crc_w = w;
+        h->gen_crc_const = crc_const;
+    }
     cudaMemcpy(h->d_prog, h->prog.data(), sizeof(pb::DOp) * h->prog.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(h->d_info, info_k.data(), sizeof(uint32_t) * code->k, cudaMemcpyHostToDevice);
     {
@@ -594,6 +615,8 @@ int pb_destroy(pb_handle *h) {
     cudaFree(h->d_in);
     cudaFree(h->d_out);
     cudaFree(h->d_fail);
+    cudaFree(h->d_info_all);
+    cudaFree(h->d_hu);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     for (int j = 0; j < 2; ++j) {
@@ -1010,5 +1033,63 @@ extern "C" int pb_fastssc(pb_handle *h, const void *llr, int in_type, int64_t ba
     PB_CUDA(cudaStreamSynchronize(st));
     for (size_t r = 0; r < (size_t)batch; ++r)
         for (int i = 0; i < N; ++i) codewords[r * N + i] = (uint8_t)((cw[r * nwd + (i >> 5)] >> (i & 31)) & 1u);
+    return PB_OK;
+}
+
+// On-device frames (frame_gen.cu): `count` frames first_frame.. of the
+// (seed, Eb/N0) stream of this handle's code, LLRs float32 (out_type
+// PB_IN_F32) or int8 (PB_IN_I8) into llr_out [count][N], packed payload bits
+// into payload_out [count][ceil(k/32)] (may be NULL).  Device buffers only;
+// asynchronous on `stream`.
+extern "C" int pb_generate_frames(pb_handle *h, uint64_t seed, double ebn0_db, int64_t first_frame, int64_t count,
+                                  int out_type, void *llr_out, uint32_t *payload_out, void *stream) {
+    g_err.clear();
+    if (!h) return fail(PB_EINVAL, "null handle");
+    if (count < 0 || first_frame < 0) return fail(PB_EINVAL, "negative frame range");
+    if (out_type != PB_IN_F32 && out_type != PB_IN_I8) return fail(PB_EINVAL, "unknown output type");
+    if (count == 0) return PB_OK;
+    if (!llr_out) return fail(PB_EINVAL, "null LLR pointer");
+    PB_CUDA(cudaSetDevice(h->device));
+    pb::gen::GenParams g{};
+    g.N = h->N;
+    g.n = h->n;
+    g.k = h->k;
+    g.crc_w = h->crc_w;
+    g.info_pos = h->d_info_all;
+    g.hu = h->d_hu;
+    g.crc_const = h->gen_crc_const;
+    g.seed = seed;
+    g.first = first_frame;
+    g.count = count;
+    const double rate = (double)h->k / h->N;  // payload rate, sim.py:70,166
+    const double sigma = std::sqrt(1.0 / (2.0 * rate * std::pow(10.0, ebn0_db / 10.0)));
+    g.sigma = (float)sigma;
+    g.scale = (float)(2.0 / (sigma * sigma));
+    g.out_type = out_type == PB_IN_F32 ? 0 : 1;
+    g.llr = llr_out;
+    g.payload = payload_out;
+    g.kw = (h->k + 31) / 32;
+    cudaError_t e = pb_launch_gen(&g, h->sms, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "frame generator launch");
+    h->launches += 1;
+    return PB_OK;
+}
+
+// Error counters of decoded payload bytes info [batch][k] against packed
+// payload bits [batch][ceil(k/32)], accumulated (added) per chunk of `chunk`
+// frames into counts [ceil(batch/chunk)][3] uint64 = (frames, frame errors,
+// bit errors).  Device buffers only; asynchronous on `stream`.
+extern "C" int pb_count_errors(pb_handle *h, const uint8_t *info, const uint32_t *payload, int64_t batch, int chunk,
+                               uint64_t *counts, void *stream) {
+    g_err.clear();
+    if (!h) return fail(PB_EINVAL, "null handle");
+    if (batch < 0 || chunk < 1) return fail(PB_EINVAL, "bad batch / chunk");
+    if (batch == 0) return PB_OK;
+    if (!info || !payload || !counts) return fail(PB_EINVAL, "null pointer");
+    PB_CUDA(cudaSetDevice(h->device));
+    cudaError_t e = pb_launch_errcount(info, payload, batch, h->k, (h->k + 31) / 32, chunk,
+                                    reinterpret_cast<unsigned long long *>(counts), h->sms, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "error counter launch");
+    h->launches += 1;
     return PB_OK;
 }

@@ -58,6 +58,16 @@ CASES = [
 ]
 
 
+SWEEPS = [
+    dict(name="sw_s256_L8", N=256, k=120, crc=CRC32, eps=0.5, L=8, snrs=[1.0, 1.5, 2.0],
+         adaptive=False, min_errors=12, max_frames=640, seed=77, chunk_size=64),
+    dict(name="sw_s256_L8_adaptive", N=256, k=120, crc=CRC32, eps=0.5, L=8, snrs=[1.0, 2.0, 3.0],
+         adaptive=True, min_errors=12, max_frames=640, seed=78, chunk_size=64),
+    dict(name="sw_s128_L4_min0", N=128, k=56, crc=CRC8_07, eps=0.5, L=4, snrs=[0.5, 2.5],
+         adaptive=False, min_errors=0, max_frames=300, seed=79, chunk_size=48),
+]
+
+
 def _sched_cfg(ref, name):
     return {"spc4": ref.ScheduleConfig(), "spc_none": ref.ScheduleConfig(spc_cap=None),
             "unspecialized": ref.ScheduleConfig.unspecialized()}[name]
@@ -120,9 +130,27 @@ def main():
         manifest.append(case)
         print(f"{key}: {B} frames, list invoked on {int(inv.sum())}", flush=True)
 
+    # polaris.sim.run_sweep points (sim.py:200-302): counts under the
+    # chunked stop rule, list and adaptive, for the GPU sweep harness
+    from polaris.sim import run_sweep
+    sweeps = []
+    for sw in SWEEPS:
+        crc = ref.CrcConfig(**sw["crc"])
+        spec = ref.CodeSpec.construct(sw["N"], sw["k"], crc, sw["eps"])
+        sch = ref.build_schedule(spec)
+        recs = run_sweep(sch, sw["L"], sw["snrs"], adaptive=sw["adaptive"], min_errors=sw["min_errors"],
+                         max_frames=sw["max_frames"], seed=sw["seed"], workers=8,
+                         chunk_size=sw["chunk_size"])
+        sw = dict(sw, records=[dict(snr_db=r.snr_db, frames=r.frames, frame_errors=r.frame_errors,
+                                    bit_errors=r.bit_errors, invoked_list_fraction=r.invoked_list_fraction,
+                                    hit_max_frames=r.hit_max_frames) for r in recs])
+        sweeps.append(sw)
+        print("sweep", sw["name"], [(r["frames"], r["frame_errors"]) for r in sw["records"]], flush=True)
+
     with open(os.path.join(HERE, "reference_adaptive.json"), "w") as fh:
         json.dump({"generator": "tests/golden/make_golden_adaptive.py",
-                   "reference": "polaris (/root/reference/pkg/src)", "cases": manifest}, fh, indent=1)
+                   "reference": "polaris (/root/reference/pkg/src)", "cases": manifest,
+                   "sweeps": sweeps}, fh, indent=1)
     np.savez_compressed(os.path.join(HERE, "reference_adaptive.npz"), **arrays)
 
 

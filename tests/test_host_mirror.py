@@ -142,3 +142,15 @@ def test_mask_file_round_trip(tmp_path):
     back = pb.CodeSpec.load(path)
     assert back.N == 64 and back.k == 28 and back.crc == pb.CRC8
     assert np.array_equal(back.frozen_mask, spec.frozen_mask)
+
+
+def test_write_csv_matches_reference_format(tmp_path):
+    """9-column CSV of polaris.sim.write_csv (sim.py:40-50,120-145)."""
+    r = pb.SimRecord(snr_db=3.5, frames=1000, frame_errors=12, bit_errors=345, fer=0.012,
+                     ber=345 / (1000 * 828), mean_latency_us=1.23456, info_throughput_mbps=670.7,
+                     invoked_list_fraction=1.0)
+    p = tmp_path / "s.csv"
+    pb.write_csv([r], str(p))
+    lines = p.read_text().splitlines()
+    assert lines[0] == "snr_db,frames,frame_errors,bit_errors,FER,BER,mean_latency_us,info_throughput_mbps,invoked_list_fraction"
+    assert lines[1] == "3.5,1000,12,345,0.012,0.000416667,1.235,670.7000,1"
