@@ -77,9 +77,10 @@ def build(verbose: bool = False, jobs: int | None = None, profile: bool = False)
     NVCC_FLAGS = globals()["NVCC_FLAGS"] + (["-DPB_PROFILE=1"] if profile else []) + \
         [f for f in os.environ.get("PB_NVCC_DEFS", "").split() if f.startswith("-D")]  # experiments
     LIB_PATH = os.path.join(LIB_DIR, "libpolar_b200_prof.so") if profile else globals()["LIB_PATH"]
-    if os.environ.get("PB_NVCC_DEFS"):
+    if os.environ.get("PB_NVCC_DEFS") or os.environ.get("PB_SHAPES"):
         import hashlib
-        BUILD_DIR += "_" + hashlib.sha1(os.environ["PB_NVCC_DEFS"].encode()).hexdigest()[:8]
+        key = os.environ.get("PB_NVCC_DEFS", "") + "|" + os.environ.get("PB_SHAPES", "")
+        BUILD_DIR += "_" + hashlib.sha1(key.encode()).hexdigest()[:8]
     os.makedirs(BUILD_DIR, exist_ok=True)
     hdrs = [os.path.join(CSRC, f) for f in ("decode_kernel.cuh", "decoder.cuh", "shapes.def")]
     hdrs.append(os.path.join(INCLUDE, "polar_b200.h"))
@@ -87,7 +88,18 @@ def build(verbose: bool = False, jobs: int | None = None, profile: bool = False)
     cmds = []
     objs = []
     inst = os.path.join(CSRC, "decode_inst.cu")
+    only = [x for x in os.environ.get("PB_SHAPES", "").split(",") if x]  # experiments: a subset
+    dispatch_defs = []
+    if only:
+        sub = os.path.join(BUILD_DIR, "shapes_subset.def")
+        with open(sub, "w") as fh:
+            for tag, t, mode, w, ppw, chg in shapes():
+                if tag in only:
+                    fh.write(f"PB_SHAPE({tag}, {t}, {mode}, {w}, {ppw}, {chg})\n")
+        dispatch_defs = [f'-DPB_SHAPES_DEF="{sub}"']
     for tag, t, mode, w, ppw, chg in shapes():
+        if only and tag not in only:
+            continue
         obj = os.path.join(BUILD_DIR, f"decode_{tag}.o")
         objs.append(obj)
         if _stale(obj, [inst, *hdrs]):
@@ -96,8 +108,9 @@ def build(verbose: bool = False, jobs: int | None = None, profile: bool = False)
     for src in ("dispatch.cu", "runtime.cu", "ssc_kernel.cu", "frame_gen.cu"):
         obj = os.path.join(BUILD_DIR, src.replace(".cu", ".o"))
         objs.append(obj)
-        if _stale(obj, [os.path.join(CSRC, src), *hdrs]):
-            cmds.append(["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj])
+        if _stale(obj, [os.path.join(CSRC, src), *hdrs]) or (only and src == "dispatch.cu"):
+            cmds.append(["nvcc", *NVCC_FLAGS, "-I", INCLUDE, *(dispatch_defs if src == "dispatch.cu" else []),
+                         "-c", os.path.join(CSRC, src), "-o", obj])
     jobs = jobs or max(1, min(len(cmds), os.cpu_count() or 1))
 
     def run(cmd):

@@ -99,42 +99,124 @@ __device__ __forceinline__ float g_op(float a, float b, unsigned bit) {
 
 __device__ __forceinline__ int log2ceil(int x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
+// four consecutive elements (one 128-bit / 32-bit access)
+template <typename T>
+struct V4;
+template <>
+struct V4<float> {
+    static __device__ __forceinline__ void ld(const float *p, float (&v)[4]) {
+        const float4 x = *reinterpret_cast<const float4 *>(p);
+        v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+    }
+    static __device__ __forceinline__ void st(float *p, const float (&v)[4]) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <>
+struct V4<int8_t> {
+    static __device__ __forceinline__ void ld(const int8_t *p, float (&v)[4]) {
+        const int x = *reinterpret_cast<const int *>(p);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = (float)((x << (24 - 8 * j)) >> 24);
+    }
+    static __device__ __forceinline__ void st(int8_t *p, const float (&v)[4]) {
+        unsigned x = 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x |= ((unsigned)__float2int_rn(v[j]) & 0xffu) << (8 * j);
+        *reinterpret_cast<unsigned *>(p) = x;
+    }
+};
+
 // ------------------------------------------------------------- sources
-// stored alpha row: block-interleaved, element i at p[i * PPW]
+// Stored alpha rows (FrameLayout).  PPW >= 16 (one or two lanes per path in
+// the steady state): quad-interleaved -- a block of PPW rows stores quad x
+// (elements 4x .. 4x+3) of local row rl at quad index
+// x * PPW + ((rl + c(x)) mod PPW), c(x) = x (PPW = 32) or x * PPW / 4, so the
+// steady-state lanes read their quads with 128-bit accesses from 512
+// contiguous bytes, bank-conflict free.  PPW <= 8 (four or more lanes per
+// path): element-interleaved, element i of local row rl at i * PPW + rl, the
+// lanes of a path taking consecutive elements (conflict free).
+template <int PPW>
+struct Lay {
+    static constexpr bool kQuad = PPW >= 16;
+    static __device__ __forceinline__ int q(int x, int rl) {
+        const int c = PPW == 32 ? x : x * (PPW / 4);
+        return (x * PPW + ((rl + c) & (PPW - 1))) * 4;
+    }
+    static __device__ __forceinline__ int e(int i, int rl) { return kQuad ? q(i >> 2, rl) + (i & 3) : i * PPW + rl; }
+};
 template <typename T, int PPW>
 struct RowSrc {
-    const T *p;
-    __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(p + i * PPW); }
+    static constexpr bool kQuad = Lay<PPW>::kQuad;
+    const T *blk;
+    int rl;
+    __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(blk + Lay<PPW>::e(i, rl)); }
+    __device__ __forceinline__ void get4(int x, float (&v)[4]) const {
+        if (kQuad) {
+            V4<T>::ld(blk + Lay<PPW>::q(x, rl), v);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = get(4 * x + j);
+        }
+    }
 };
 template <typename T, int PPW>
 struct RowDst {
-    T *p;
-    __device__ __forceinline__ void put(int i, float v) const { Elem<T>::st(p + i * PPW, v); }
+    T *blk;
+    int rl;
+    __device__ __forceinline__ void put(int i, float v) const { Elem<T>::st(blk + Lay<PPW>::e(i, rl), v); }
+    __device__ __forceinline__ void put4(int x, const float (&v)[4]) const {
+        if (Lay<PPW>::kQuad) {
+            V4<T>::st(blk + Lay<PPW>::q(x, rl), v);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) put(4 * x + j, v[j]);
+        }
+    }
 };
 // stage n-1 in the left half of the tree: f(channel halves)
 template <typename T>
 struct VirtF {
+    static constexpr bool kQuad = true;
     const T *ch;
     int half;
     __device__ __forceinline__ float get(int i) const {
         return f_op(Elem<T>::ld(ch + i), Elem<T>::ld(ch + i + half));
     }
+    __device__ __forceinline__ void get4(int x, float (&v)[4]) const {
+        float a[4], b[4];
+        V4<T>::ld(ch + 4 * x, a);
+        V4<T>::ld(ch + 4 * x + half, b);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = f_op(a[j], b[j]);
+    }
 };
 // stage n-1 in the right half: g(channel halves, the path's left-half bits)
 template <typename T>
 struct VirtG {
+    static constexpr bool kQuad = true;
     const T *ch;
     const uint32_t *bw;
     int half;
     __device__ __forceinline__ float get(int i) const {
         return g_op<T>(Elem<T>::ld(ch + i), Elem<T>::ld(ch + i + half), (bw[i >> 5] >> (i & 31)) & 1u);
     }
+    __device__ __forceinline__ void get4(int x, float (&v)[4]) const {
+        float a[4], b[4];
+        V4<T>::ld(ch + 4 * x, a);
+        V4<T>::ld(ch + 4 * x + half, b);
+        const unsigned bits = bw[x >> 3] >> ((x & 7) * 4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = g_op<T>(a[j], b[j], (bits >> j) & 1u);
+    }
 };
 // the channel itself (a root leaf)
 template <typename T>
 struct ChanSrc {
+    static constexpr bool kQuad = true;
     const T *ch;
     __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(ch + i); }
+    __device__ __forceinline__ void get4(int x, float (&v)[4]) const { V4<T>::ld(ch + 4 * x, v); }
 };
 
 // ------------------------------------------------------- configuration
@@ -154,6 +236,7 @@ struct RtCfg {
     __device__ __forceinline__ int a_off(int s) const { return p->lay.a_off[s]; }
     __device__ __forceinline__ int a_gfrom() const { return p->lay.a_gfrom; }
     __device__ __forceinline__ int b_off(int s) const { return p->lay.b_off[s]; }
+    __device__ __forceinline__ int b_gfrom() const { return p->lay.b_gfrom; }
     __device__ __forceinline__ int b_stride(int s) const { return p->lay.b_stride[s]; }
     __device__ __forceinline__ int pm_off() const { return p->lay.pm_off; }
     __device__ __forceinline__ int ia_off() const { return p->lay.ia_off; }
@@ -195,12 +278,13 @@ struct Dec {
         if (PB_PROFILE && ph && lane == 0) ph[i] = clock64();
     }
 
-    // row r, element 0 of a block-interleaved stage s
-    __device__ __forceinline__ int rowoff(int s, int r) const { return ((r >> LP) << (LP + s)) + (r & (PPW - 1)); }
+    // row r of stage s: its PPW-row block (quad-interleaved, FrameLayout)
+    // and its local row index
+    __device__ __forceinline__ int blkoff(int s, int r) const { return (r >> LP) * (PPW << (s < 2 ? 2 : s)); }
     __device__ __forceinline__ T *a_sm(int s) const { return reinterpret_cast<T *>(sm + cfg.a_off(s)); }
     __device__ __forceinline__ T *a_gl(int s) const { return reinterpret_cast<T *>(gs + cfg.a_off(s)); }
     __device__ __forceinline__ uint32_t *beta_row(int s, int row) const {
-        return reinterpret_cast<uint32_t *>(sm + cfg.b_off(s)) + row * cfg.b_stride(s);
+        return reinterpret_cast<uint32_t *>((s >= cfg.b_gfrom() ? gs : sm) + cfg.b_off(s)) + row * cfg.b_stride(s);
     }
     __device__ __forceinline__ T *channel() const {
         return reinterpret_cast<T *>((CFG::kChGlobal ? gs : sm) + cfg.ch_off());
@@ -266,7 +350,61 @@ struct Dec {
 
 // ---------------------------------------------------------------- F / G
 
-// G lanes per path; GC > 0: G known at compile time (steady state)
+// One path's F / G: h outputs, G lanes per path (GC > 0: known at compile
+// time, the steady state), this lane = sub.  h >= 4: the lane's quads
+// x = sub, sub + G, ... in unrolled blocks of UQ whose loads all issue before
+// the stores (UQ = 8 for L2-latency global sources); h < 4: scalar.
+template <typename T, bool IS_G, int GC, int UQ, class S, class D>
+__device__ __forceinline__ void fg_row(const S &src, const D &dst, const uint32_t *bw, int h, int Grt, int sub) {
+    const int G = GC > 0 ? GC : Grt;
+    if (h < 4) {
+        for (int i = sub; i < h; i += G)
+            dst.put(i, IS_G ? g_op<T>(src.get(i), src.get(i + h), (bw[0] >> i) & 1u) : f_op(src.get(i), src.get(i + h)));
+        return;
+    }
+    const int nq = h >> 2;
+    int x0 = sub;
+    for (; x0 + (UQ - 1) * G < nq; x0 += G * UQ) {  // whole blocks: no guards
+        float a[UQ][4], b[UQ][4];
+        unsigned bits[UQ];
+#pragma unroll
+        for (int u = 0; u < UQ; ++u) {
+            const int x = x0 + u * G;
+            src.get4(x, a[u]);
+            src.get4(x + nq, b[u]);
+            bits[u] = IS_G ? bw[x >> 3] >> ((x & 7) * 4) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < UQ; ++u) {
+            float o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op<T>(a[u][j], b[u][j], (bits[u] >> j) & 1u) : f_op(a[u][j], b[u][j]);
+            dst.put4(x0 + u * G, o);
+        }
+    }
+    for (; x0 < nq; x0 += G) {  // the rest, one quad at a time
+        float a[4], b[4], o[4];
+        src.get4(x0, a);
+        src.get4(x0 + nq, b);
+        const unsigned bits = IS_G ? bw[x0 >> 3] >> ((x0 & 7) * 4) : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op<T>(a[j], b[j], (bits >> j) & 1u) : f_op(a[j], b[j]);
+        dst.put4(x0, o);
+    }
+}
+
+// quads in flight per lane (global-scratch / shared-memory sources)
+#ifndef PB_UQ_GL
+#define PB_UQ_GL 8
+#endif
+#ifndef PB_UQ_SM
+#define PB_UQ_SM 4
+#endif
+
+// Element-interleaved layout (PPW <= 8): the G lanes of a path take
+// consecutive elements.  fg_loop: any G (GC > 0: compile-time); fg_chunks:
+// steady state with h >= 32, 32-element chunks whose loads all issue before
+// the stores (immediate offsets, beta word loaded once).
 template <typename T, bool IS_G, int GC, class S, class D>
 __device__ __forceinline__ void fg_loop(const S &src, const D &dst, const uint32_t *bw, int h, int Grt, int sub) {
     const int G = GC > 0 ? GC : Grt;
@@ -283,13 +421,9 @@ __device__ __forceinline__ void fg_loop(const S &src, const D &dst, const uint32
         }
     }
 }
-
-// Steady state (G = GC lanes per path, compile-time) with h >= 32: 32-element
-// chunks, the lane's elements of a chunk in unrolled blocks of U whose loads
-// all issue before the stores (immediate offsets, beta word loaded once).
 template <typename T, bool IS_G, int GC, int PPW, int UMAX, class S>
 __device__ __forceinline__ void fg_chunks(const S &src, T *dst, const uint32_t *bw, int h, int sub) {
-    constexpr int PER = 32 / GC;              // this lane's elements per chunk
+    constexpr int PER = 32 / GC;                // this lane's elements per chunk
     constexpr int U = PER < UMAX ? PER : UMAX;  // unrolled block (loads in flight)
     for (int c0 = 0; c0 < h; c0 += 32) {
         const uint32_t wsh = IS_G ? (bw[c0 >> 5] >> sub) : 0u;
@@ -317,44 +451,71 @@ template <typename T, int W, int PPW, class CFG, bool IS_G, bool SRC_GL = false,
 __device__ __forceinline__ void fg_to_dst(const Dec<T, W, PPW, CFG> &F, const S &src, int s, int q, const uint32_t *bw,
                                           int h, int G, int sub) {
     constexpr int GS = Dec<T, W, PPW, CFG>::GSS;
-    constexpr int UM = SRC_GL ? 32 : 8;
-    const int off = F.rowoff(s - 1, q);
-    if (s - 1 < F.cfg.a_gfrom()) {
-        T *d = F.a_sm(s - 1) + off;
-        if (G == GS && h >= 32)
-            fg_chunks<T, IS_G, GS, PPW, UM>(src, d, bw, h, sub);
+    const int off = F.blkoff(s - 1, q), rl = q & (PPW - 1);
+    T *d = (s - 1 < F.cfg.a_gfrom() ? F.a_sm(s - 1) : F.a_gl(s - 1)) + off;
+    if (Lay<PPW>::kQuad) {
+        constexpr int UQ = SRC_GL ? PB_UQ_GL : PB_UQ_SM;
+        if (G == GS)
+            fg_row<T, IS_G, GS, UQ>(src, RowDst<T, PPW>{d, rl}, bw, h, G, sub);
         else
-            fg_loop<T, IS_G, 0>(src, RowDst<T, PPW>{d}, bw, h, G, sub);
+            fg_row<T, IS_G, 0, UQ>(src, RowDst<T, PPW>{d, rl}, bw, h, G, sub);
     } else {
-        T *d = F.a_gl(s - 1) + off;
+        constexpr int UM = SRC_GL ? 32 : 8;
         if (G == GS && h >= 32)
-            fg_chunks<T, IS_G, GS, PPW, UM>(src, d, bw, h, sub);
+            fg_chunks<T, IS_G, GS, PPW, UM>(src, d + rl, bw, h, sub);
         else
-            fg_loop<T, IS_G, 0>(src, RowDst<T, PPW>{d}, bw, h, G, sub);
+            fg_loop<T, IS_G, 0>(src, RowDst<T, PPW>{d, rl}, bw, h, G, sub);
     }
+}
+
+// F / G whose source is the never-stored stage n-1 (recomputed from the
+// channel) or a global-scratch stage: few ops per frame, each long
+// (PB_FAR=1 keeps them out of line; measured slower, so inlined by default)
+#ifndef PB_FAR
+#define PB_FAR 0
+#endif
+template <typename T, int W, int PPW, class CFG, bool IS_G>
+__device__ __forceinline__ void fg_far_body(Dec<T, W, PPW, CFG> &F, const DOp &o, int q, int G, int sub) {
+    const CFG &cfg = F.cfg;
+    const int s = o.stage, h = 1 << (s - 1);
+    const uint32_t *bw = IS_G ? F.beta_row(s - 1, F.ib(F.cur, s - 1, q)) : nullptr;
+    if (s == cfg.n() - 1) {
+        if (o.vmode == VM_F)
+            fg_to_dst<T, W, PPW, CFG, IS_G>(F, VirtF<T>{F.channel(), cfg.N() >> 1}, s, q, bw, h, G, sub);
+        else
+            fg_to_dst<T, W, PPW, CFG, IS_G>(
+                F, VirtG<T>{F.channel(), F.beta_row(cfg.n() - 1, F.ib(F.cur, cfg.n() - 1, q)), cfg.N() >> 1}, s, q, bw, h,
+                G, sub);
+    } else {
+        const int r = F.ia(F.cur, s, q);
+        fg_to_dst<T, W, PPW, CFG, IS_G, true>(F, RowSrc<T, PPW>{F.a_gl(s) + F.blkoff(s, r), r & (PPW - 1)}, s, q, bw,
+                                             h, G, sub);
+    }
+}
+template <typename T, int W, int PPW, class CFG, bool IS_G>
+__device__ __noinline__ void fg_far(const Params &P, unsigned char *sm, unsigned char *gs, int cur, DOp o, int q, int G,
+                                    int sub) {
+    Dec<T, W, PPW, CFG> F(P, CFG{&P}, sm, gs);
+    F.cur = cur;
+    fg_far_body<T, W, PPW, CFG, IS_G>(F, o, q, G, sub);
 }
 
 template <typename T, int W, int PPW, class CFG, bool IS_G>
 __device__ __forceinline__ void fg_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
     const auto mp = F.map(o.pin);
     if (!mp.active || PB_ABL(F.P, 8)) return;
-    const Params &P = F.P;
     const CFG &cfg = F.cfg;
     const int s = o.stage, h = 1 << (s - 1), q = mp.q;
-    const uint32_t *bw = IS_G ? F.beta_row(s - 1, F.ib(F.cur, s - 1, q)) : nullptr;
-    if (s == cfg.n() - 1) {
-        if (o.vmode == VM_F)
-            fg_to_dst<T, W, PPW, CFG, IS_G>(F, VirtF<T>{F.channel(), cfg.N() >> 1}, s, q, bw, h, mp.G, mp.sub);
+    if (s == cfg.n() - 1 || s >= cfg.a_gfrom()) {
+        if (PB_FAR)
+            fg_far<T, W, PPW, CFG, IS_G>(F.P, F.sm, F.gs, F.cur, o, q, mp.G, mp.sub);
         else
-            fg_to_dst<T, W, PPW, CFG, IS_G>(
-                F, VirtG<T>{F.channel(), F.beta_row(cfg.n() - 1, F.ib(F.cur, cfg.n() - 1, q)), cfg.N() >> 1}, s, q, bw, h, mp.G,
-                mp.sub);
+            fg_far_body<T, W, PPW, CFG, IS_G>(F, o, q, mp.G, mp.sub);
     } else {
-        const int off = F.rowoff(s, F.ia(F.cur, s, q));
-        if (s < cfg.a_gfrom())
-            fg_to_dst<T, W, PPW, CFG, IS_G>(F, RowSrc<T, PPW>{F.a_sm(s) + off}, s, q, bw, h, mp.G, mp.sub);
-        else
-            fg_to_dst<T, W, PPW, CFG, IS_G, true>(F, RowSrc<T, PPW>{F.a_gl(s) + off}, s, q, bw, h, mp.G, mp.sub);
+        const uint32_t *bw = IS_G ? F.beta_row(s - 1, F.ib(F.cur, s - 1, q)) : nullptr;
+        const int r = F.ia(F.cur, s, q);
+        fg_to_dst<T, W, PPW, CFG, IS_G>(F, RowSrc<T, PPW>{F.a_sm(s) + F.blkoff(s, r), r & (PPW - 1)}, s, q, bw, h,
+                                        mp.G, mp.sub);
     }
     if (mp.sub == 0) F.ia(F.cur, s - 1, q) = (uint8_t)q;
 }
@@ -365,8 +526,10 @@ __device__ __forceinline__ void fg_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
 // ((0+1)+(2+3))+((4+5)+(6+7)); larger n halves recursively.  For power-of-
 // two node sizes that is a perfect binary tree over 8*nb accumulators
 // (nb = max(1, n/128)), each a sequential sum of min(n,128)/8 elements.
-// GS lanes of a group share the 8 accumulator columns (lane sub owns columns
-// j = sub + a*GS); tree levels on lane bits shuffle, the rest stay in registers.
+// GS lanes of a group share the 8 accumulator columns, lane sub owning the
+// contiguous columns [sub*NA, sub*NA + NA) (NA = 8/GS): the low tree levels
+// add in registers, the rest shuffle; the columns of a row of 8 elements are
+// one or two quads (128-bit loads) for NA >= 4.
 
 template <int NS>
 __device__ __forceinline__ void acc_add(float *acc, float a) {
@@ -385,6 +548,29 @@ __device__ __forceinline__ void acc_init(float *acc, float a) {
     }
 }
 
+// the NA elements e0 .. e0+NA-1 (e0 a multiple of NA)
+template <int NA, class S>
+__device__ __forceinline__ void load_cols(const S &src, int e0, float (&v)[NA]) {
+    if (NA == 8) {
+        float q0[4], q1[4];
+        src.get4(e0 >> 2, q0);
+        src.get4((e0 >> 2) + 1, q1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v[j] = q0[j];
+            v[(j + 4) & (NA - 1)] = q1[j];
+        }
+    } else if (NA == 4) {
+        float q0[4];
+        src.get4(e0 >> 2, q0);
+#pragma unroll
+        for (int j = 0; j < NA; ++j) v[j] = q0[j];
+    } else {
+#pragma unroll
+        for (int j = 0; j < NA; ++j) v[j] = src.get(e0 + j);
+    }
+}
+
 // NS = 1: sum min(a,0); NS = 3: (sum min(a,0), sum max(a,0), sum a).
 // Valid in the group leader lane.
 template <int NS, int GS, class S>
@@ -400,7 +586,11 @@ __device__ __forceinline__ void pw_sums(const S &src, int m, bool active, int su
         return;
     }
     constexpr int NA = 8 / GS;  // accumulator columns per lane
+    constexpr int LNA = ilog2(NA);
     constexpr int LG = ilog2(GS);
+    // quad-readable sources: lane sub owns the contiguous columns
+    // [sub*NA, sub*NA + NA); element-interleaved rows: columns sub + a*GS
+    constexpr bool CONTIG = S::kQuad;
     const int blk = m < 128 ? m : 128;
     const int nb = m / blk;
     const int per = blk >> 3;
@@ -410,35 +600,51 @@ __device__ __forceinline__ void pw_sums(const S &src, int m, bool active, int su
     for (int b = 0; b < nb; ++b) {
         float acc[NA][NS];
         // the NA column chains are independent: interleave them (ILP)
-        const int base = b * blk + sub;
+        const int base = b * blk + (CONTIG ? sub * NA : sub);
         if (act) {
+            float v[NA];
+            if (CONTIG) {
+                load_cols<NA>(src, base, v);
+            } else {
 #pragma unroll
-            for (int a = 0; a < NA; ++a) acc_init<NS>(acc[a], src.get(base + a * GS));
-            for (int r = 1; r < per; ++r)
+                for (int a = 0; a < NA; ++a) v[a] = src.get(base + a * GS);
+            }
 #pragma unroll
-                for (int a = 0; a < NA; ++a) acc_add<NS>(acc[a], src.get(base + a * GS + 8 * r));
+            for (int a = 0; a < NA; ++a) acc_init<NS>(acc[a], v[a]);
+            for (int r = 1; r < per; ++r) {
+                if (CONTIG) {
+                    load_cols<NA>(src, base + 8 * r, v);
+                } else {
+#pragma unroll
+                    for (int a = 0; a < NA; ++a) v[a] = src.get(base + a * GS + 8 * r);
+                }
+#pragma unroll
+                for (int a = 0; a < NA; ++a) acc_add<NS>(acc[a], v[a]);
+            }
         } else {
 #pragma unroll
             for (int a = 0; a < NA; ++a)
 #pragma unroll
                 for (int t = 0; t < NS; ++t) acc[a][t] = 0.f;
         }
-        // levels 0..2 of the column tree: lane bits shuffle, register bits add
+        // levels 0..2 of the column tree (column index bits: register bits
+        // add in registers, lane bits shuffle)
 #pragma unroll
         for (int lv = 0; lv < 3; ++lv) {
-            if (lv < LG) {
+            const bool reg = CONTIG ? lv < LNA : lv >= LG;
+            if (reg) {
+                const int step = CONTIG ? 1 << lv : 1 << (lv - LG);
 #pragma unroll
-                for (int a = 0; a < NA; ++a)
+                for (int a = 0; a < NA; a += 2 * step)
+#pragma unroll
+                    for (int t = 0; t < NS; ++t) acc[a][t] = __fadd_rn(acc[a][t], acc[a + step][t]);
+            } else {
+                const int d = CONTIG ? 1 << (lv - LNA) : 1 << lv;
+#pragma unroll
+                for (int a = 0; a < (CONTIG ? 1 : NA); ++a)
 #pragma unroll
                     for (int t = 0; t < NS; ++t)
-                        acc[a][t] = __fadd_rn(acc[a][t], __shfl_xor_sync(FULL_MASK, acc[a][t], 1 << lv));
-            } else {
-                const int step = 1 << (lv - LG);
-#pragma unroll
-                for (int a = 0; a < NA; ++a)
-                    if ((a & step) == 0 && a + step < NA)
-#pragma unroll
-                        for (int t = 0; t < NS; ++t) acc[a][t] = __fadd_rn(acc[a][t], acc[a + step][t]);
+                        acc[a][t] = __fadd_rn(acc[a][t], __shfl_xor_sync(FULL_MASK, acc[a][t], d));
             }
         }
         // combine block sums in numpy's halving order: registers for the
@@ -803,11 +1009,16 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW, CFG> &F, const DOp &o, 
     int par = 0;
     if (Gl == 1) {
         if (active && sub == 0 && m >= 32) {
-            // whole 32-element blocks: all loads in flight before the serial scan
+            // whole 32-element blocks: all (quad) loads in flight before the serial scan
             for (int w0 = 0; w0 < m; w0 += 32) {
                 float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = src.get(w0 + j);
+                for (int j = 0; j < 8; ++j) {
+                    float qv[4];
+                    src.get4((w0 >> 2) + j, qv);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) v[4 * j + e] = qv[e];
+                }
                 uint32_t word = 0u;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
@@ -817,19 +1028,35 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW, CFG> &F, const DOp &o, 
                 F.hard(F.par, w0 >> 5, q) = word;
                 par ^= __popc(word);
             }
-        } else if (active && sub == 0) {
-            for (int w0 = 0; w0 < m; w0 += 32) {
-                const int cnt = m - w0 < 32 ? m - w0 : 32;
-                uint32_t word = 0u;
-#pragma unroll 4
-                for (int j = 0; j < cnt; ++j) {
-                    const float a = src.get(w0 + j);
-                    word |= (a < 0.f ? 1u : 0u) << j;
-                    tk.push_scan(fabsf(a), w0 + j);
+        } else if (S::kQuad && active && sub == 0 && m >= 4) {
+            // m = 4, 8, 16: quads, loads first
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (4 * j < m) {
+                    float qv[4];
+                    src.get4(j, qv);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) v[4 * j + e] = qv[e];
                 }
-                F.hard(F.par, w0 >> 5, q) = word;
-                par ^= __popc(word);
+            uint32_t word = 0u;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < m) {
+                    word |= (v[j] < 0.f ? 1u : 0u) << j;
+                    tk.push_scan(fabsf(v[j]), j);
+                }
+            F.hard(F.par, 0, q) = word;
+            par ^= __popc(word);
+        } else if (active && sub == 0) {
+            uint32_t word = 0u;
+            for (int j = 0; j < m; ++j) {
+                const float a = src.get(j);
+                word |= (a < 0.f ? 1u : 0u) << j;
+                tk.push_scan(fabsf(a), j);
             }
+            F.hard(F.par, 0, q) = word;
+            par ^= __popc(word);
         }
         F.mark(2);
     } else {
@@ -930,11 +1157,11 @@ __device__ __forceinline__ void leaf_phase_a(Dec<T, W, PPW, CFG> &F, const DOp &
         leaf_scan<T, W, PPW, CFG, 4>(F, o, kind, src, q, active, G, sub);
 }
 
-// dispatch on where the node's LLRs live
+// leaves reading the channel, the recomputed stage n-1 or a global-scratch
+// stage: rare, kept out of line (see fg_far)
 template <typename T, int W, int PPW, class CFG>
-__device__ __forceinline__ void leaf_read(Dec<T, W, PPW, CFG> &F, const DOp &o, int kind, int q, bool active, int G,
-                                          int sub) {
-    const Params &P = F.P;
+__device__ __forceinline__ void leaf_read_far_body(Dec<T, W, PPW, CFG> &F, const DOp &o, int kind, int q, bool active,
+                                                   int G, int sub) {
     const CFG &cfg = F.cfg;
     const int t = o.stage;
     const int qq = active ? q : F.warp * PPW;
@@ -947,11 +1174,34 @@ __device__ __forceinline__ void leaf_read(Dec<T, W, PPW, CFG> &F, const DOp &o, 
             leaf_phase_a(F, o, kind, VirtG<T>{F.channel(), F.beta_row(cfg.n() - 1, F.ib(F.cur, cfg.n() - 1, qq)), cfg.N() >> 1}, q,
                          active, G, sub);
     } else {
-        const int off = F.rowoff(t, F.ia(F.cur, t, qq));
-        if (t < cfg.a_gfrom())
-            leaf_phase_a(F, o, kind, RowSrc<T, PPW>{F.a_sm(t) + off}, q, active, G, sub);
+        const int r = F.ia(F.cur, t, qq);
+        leaf_phase_a(F, o, kind, RowSrc<T, PPW>{F.a_gl(t) + F.blkoff(t, r), r & (PPW - 1)}, q, active, G, sub);
+    }
+}
+template <typename T, int W, int PPW, class CFG>
+__device__ __noinline__ void leaf_read_far(const Params &P, unsigned char *sm, unsigned char *gs, int cur, int par,
+                                           DOp o, int kind, int q, bool active, int G, int sub) {
+    Dec<T, W, PPW, CFG> F(P, CFG{&P}, sm, gs);
+    F.cur = cur;
+    F.par = par;
+    leaf_read_far_body(F, o, kind, q, active, G, sub);
+}
+
+// dispatch on where the node's LLRs live
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ void leaf_read(Dec<T, W, PPW, CFG> &F, const DOp &o, int kind, int q, bool active, int G,
+                                          int sub) {
+    const CFG &cfg = F.cfg;
+    const int t = o.stage;
+    if (t >= cfg.n() - 1 || t >= cfg.a_gfrom()) {
+        if (PB_FAR && !PB_PROFILE)
+            leaf_read_far<T, W, PPW, CFG>(F.P, F.sm, F.gs, F.cur, F.par, o, kind, q, active, G, sub);
         else
-            leaf_phase_a(F, o, kind, RowSrc<T, PPW>{F.a_gl(t) + off}, q, active, G, sub);
+            leaf_read_far_body(F, o, kind, q, active, G, sub);
+    } else {
+        const int qq = active ? q : F.warp * PPW;
+        const int r = F.ia(F.cur, t, qq);
+        leaf_phase_a(F, o, kind, RowSrc<T, PPW>{F.a_sm(t) + F.blkoff(t, r), r & (PPW - 1)}, q, active, G, sub);
     }
 }
 

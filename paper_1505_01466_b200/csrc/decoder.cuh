@@ -12,9 +12,12 @@ constexpr int kMaxL = 32;       // selection runs on one warp: one lane per sour
 constexpr int kMaxCand = 8;
 
 // threads per CTA the kernels are compiled for (__launch_bounds__): the
-// register budget per thread is 65536 / PB_MAXT
+// register budget per thread is 65536 / PB_MAXT.  512 = 16 single-warp frames
+// per SM at 128 registers: the decode is latency-bound, and 16 resident
+// frames beat 8 frames at 255 registers by 30-45 % (c3 L=32 1.86 -> 2.41,
+// c5 L=16 1.96 -> 2.93 Gbit/s) despite ~0.9 KB of spills (to L1).
 #ifndef PB_MAXT
-#define PB_MAXT 256
+#define PB_MAXT 512
 #endif
 constexpr int kMaxThreads = PB_MAXT;
 
@@ -39,15 +42,18 @@ struct __align__(16) DOp {
 
 // Per-frame storage plan.  Offsets in bytes from the frame's shared-memory
 // block, or from its global scratch block for alpha stages >= a_gfrom.
-// Alpha rows are block-interleaved: the PPW rows a warp owns are interleaved
-// element by element, row r element i at
-//   a_off[s] + ((r / PPW) * 2^s * PPW + i * PPW + r % PPW) * sizeof(T)
-// so a warp's (path, element) lanes hit 32 distinct banks / one 128-B line.
+// Alpha rows are quad-interleaved: the PPW rows a warp owns are interleaved
+// four elements (one quad) at a time with an XOR swizzle; with E = max(4, 2^s)
+// elements per row, quad x of row r starts at element
+//   (r / PPW) * PPW * E + (x * PPW + ((r % PPW) ^ (x & min(PPW, 8) - 1))) * 4
+// so a warp whose lanes are paths reads 32 quads of 512 contiguous bytes with
+// one 128-bit access each, and the lanes of one path spread over the banks.
 struct FrameLayout {
     int ch_off;                 // channel LLRs, N elements of T
     int a_off[kMaxLog];         // alpha stage s (s <= n-2)
     int a_gfrom;                // stages >= a_gfrom live in global scratch
     int b_off[kMaxLog];         // beta slot s (s <= n-1): L rows, uint32 words
+    int b_gfrom;                // beta slots >= b_gfrom live in global scratch
     int b_stride[kMaxLog];      // row stride, words
     int pm_off;                 // double [2][L]    path metrics (double-buffered)
     int ia_off;                 // uint32 [2][idx_stride][L] alpha row per stage, 4 per word

@@ -334,7 +334,8 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     h->ppw = ppw;
     h->warps = warps;
     const int smem_cap = 227 * 1024;
-    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", 8));
+    // resident frames per SM: one warp each, up to the launch bound
+    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", pb::kMaxThreads / 32));
     // Per-frame layout for a channel in shared memory or in global scratch.
     auto plan_layout = [&](bool chg, pb::FrameLayout &lay) {
         lay = pb::FrameLayout{};
@@ -344,11 +345,21 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
             goff = align_up(N * es, 256);  // global scratch, before the global alpha stages
         else
             off = align_up(N * es, 16);
+        // beta slots: the top ones (largest) may go to global scratch
+        // (PB_BETA_GLOBAL_FROM) to leave shared memory to more frames
+        // (measured: slots >= 6 global for c3 / c5 / int8 at 16 frames per SM;
+        // the freed shared memory also grows the L1 that caches the global rows)
+        lay.b_gfrom = std::min(n, std::max(1, env_int("PB_BETA_GLOBAL_FROM", 6)));
         for (int s = 0; s < n; ++s) {
             int words = std::max(1, (1 << s) / 32);
             lay.b_stride[s] = words > 1 ? words + 1 : 1;
-            lay.b_off[s] = off;
-            off = align_up(off + L * lay.b_stride[s] * 4, 16);
+            if (s >= lay.b_gfrom) {
+                lay.b_off[s] = goff;
+                goff = align_up(goff + L * lay.b_stride[s] * 4, 256);
+            } else {
+                lay.b_off[s] = off;
+                off = align_up(off + L * lay.b_stride[s] * 4, 16);
+            }
         }
         lay.pm_off = off;
         off = align_up(off + 2 * L * 8, 16);
@@ -377,8 +388,9 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         // alpha stages s = 0 .. n-2 (n-1 is recomputed), lowest stages first into
         // shared memory, the rest into per-frame global scratch (L2-resident)
         int s_global = n - 1;
+        // quad-interleaved rows: at least one quad (4 elements) per row
         for (int s = 0; s <= n - 2; ++s) {
-            int bytes = align_up(rows * (1 << s) * es, 16);
+            int bytes = align_up(rows * std::max(4, 1 << s) * es, 16);
             if (off + bytes > budget) {
                 s_global = s;
                 break;
@@ -389,7 +401,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         lay.a_gfrom = s_global;
         for (int s = s_global; s <= n - 2; ++s) {
             lay.a_off[s] = goff;
-            goff = align_up(goff + rows * (1 << s) * es, 256);
+            goff = align_up(goff + rows * std::max(4, 1 << s) * es, 256);
         }
         lay.gbytes = goff;
         lay.smem_bytes = align_up(off, 16);
