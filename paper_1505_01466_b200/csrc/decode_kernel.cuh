@@ -159,6 +159,8 @@ struct RowSrc {
             for (int j = 0; j < 4; ++j) v[j] = get(4 * x + j);
         }
     }
+    __device__ __forceinline__ unsigned bits_word(int) const { return 0u; }
+    __device__ __forceinline__ void get4w(int x, float (&v)[4], unsigned) const { get4(x, v); }
 };
 template <typename T, int PPW>
 struct RowDst {
@@ -190,6 +192,8 @@ struct VirtF {
 #pragma unroll
         for (int j = 0; j < 4; ++j) v[j] = f_op(a[j], b[j]);
     }
+    __device__ __forceinline__ unsigned bits_word(int) const { return 0u; }
+    __device__ __forceinline__ void get4w(int x, float (&v)[4], unsigned) const { get4(x, v); }
 };
 // stage n-1 in the right half: g(channel halves, the path's left-half bits)
 template <typename T>
@@ -209,6 +213,16 @@ struct VirtG {
 #pragma unroll
         for (int j = 0; j < 4; ++j) v[j] = g_op<T>(a[j], b[j], (bits >> j) & 1u);
     }
+    // the beta word of quad x, and get4 with it preloaded (x in that word)
+    __device__ __forceinline__ unsigned bits_word(int x) const { return bw[x >> 3]; }
+    __device__ __forceinline__ void get4w(int x, float (&v)[4], unsigned wd) const {
+        float a[4], b[4];
+        V4<T>::ld(ch + 4 * x, a);
+        V4<T>::ld(ch + 4 * x + half, b);
+        const unsigned bits = wd >> ((x & 7) * 4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = g_op<T>(a[j], b[j], (bits >> j) & 1u);
+    }
 };
 // the channel itself (a root leaf)
 template <typename T>
@@ -217,6 +231,8 @@ struct ChanSrc {
     const T *ch;
     __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(ch + i); }
     __device__ __forceinline__ void get4(int x, float (&v)[4]) const { V4<T>::ld(ch + 4 * x, v); }
+    __device__ __forceinline__ unsigned bits_word(int) const { return 0u; }
+    __device__ __forceinline__ void get4w(int x, float (&v)[4], unsigned) const { get4(x, v); }
 };
 
 // ------------------------------------------------------- configuration
@@ -364,15 +380,25 @@ __device__ __forceinline__ void fg_row(const S &src, const D &dst, const uint32_
     }
     const int nq = h >> 2;
     int x0 = sub;
+    // G lanes x UQ quads of a block within one 32-element beta word (the
+    // steady state): that word is loaded once per block
+    constexpr bool ONE_WORD = GC > 0 && GC * UQ <= 8;
     for (; x0 + (UQ - 1) * G < nq; x0 += G * UQ) {  // whole blocks: no guards
         float a[UQ][4], b[UQ][4];
         unsigned bits[UQ];
+        const unsigned wd = IS_G && ONE_WORD ? bw[x0 >> 3] : 0u;
+        const unsigned swa = ONE_WORD ? src.bits_word(x0) : 0u, swb = ONE_WORD ? src.bits_word(x0 + nq) : 0u;
 #pragma unroll
         for (int u = 0; u < UQ; ++u) {
             const int x = x0 + u * G;
-            src.get4(x, a[u]);
-            src.get4(x + nq, b[u]);
-            bits[u] = IS_G ? bw[x >> 3] >> ((x & 7) * 4) : 0u;
+            if (ONE_WORD) {
+                src.get4w(x, a[u], swa);
+                src.get4w(x + nq, b[u], swb);
+            } else {
+                src.get4(x, a[u]);
+                src.get4(x + nq, b[u]);
+            }
+            bits[u] = IS_G ? (ONE_WORD ? wd : bw[x >> 3]) >> ((x & 7) * 4) : 0u;
         }
 #pragma unroll
         for (int u = 0; u < UQ; ++u) {
@@ -938,7 +964,9 @@ __device__ __forceinline__ void bits_put(uint32_t *row, int off, int len, uint32
 // chain of Combines t .. sE-1 in place:
 //   dst[E - 2^(s+1), E - 2^s) = slot_s[row_s] ^ dst[E - 2^s, E)
 // (listdec.py:327-332 with the right child's bits kept where they are).
-// Called by all lanes of a warp (synchronises the warp between steps).
+// The levels below 32 bits all land in the node's last word: they run in a
+// register from prefetched slot words, one store; wider levels go word-
+// parallel over the group's lanes.  Called by all lanes of a warp.
 template <typename T, int W, int PPW, class CFG>
 __device__ __forceinline__ void word_and_chain(const Dec<T, W, PPW, CFG> &F, int b, const DOp &o, int kind, bool active,
                                                int G, int sub, int p, int c, int ibuf, int ipath, uint32_t *dst,
@@ -948,21 +976,33 @@ __device__ __forceinline__ void word_and_chain(const Dec<T, W, PPW, CFG> &F, int
         if (m >= 32) {
             for (int w = sub; w < (m >> 5); w += G) dst[((E - m) >> 5) + w] = leaf_word(F, b, kind, m, p, c, w);
         } else if (sub == 0) {
-            bits_put(dst, E - m, m, leaf_word(F, b, kind, m, p, c, 0));
+            const int s_sub = sE < 5 ? sE : 5;
+            const int W0 = E >= 32 ? E - 32 : 0;
+            uint32_t slw[5];
+#pragma unroll
+            for (int s = 0; s < 5; ++s)
+                slw[s] = (s >= t && s < s_sub) ? F.beta_row(s, F.ib(ibuf, s, ipath))[0] : 0u;
+            uint32_t R = leaf_word(F, b, kind, m, p, c, 0) << (E - m - W0);
+#pragma unroll
+            for (int s = 0; s < 5; ++s)
+                if (s >= t && s < s_sub) {
+                    const int seg = 1 << s;
+                    const uint32_t msk = (1u << seg) - 1u;
+                    R |= ((slw[s] ^ (R >> (E - seg - W0))) & msk) << (E - 2 * seg - W0);
+                }
+            if (E >= 32)
+                dst[(E >> 5) - 1] = R;
+            else
+                bits_put(dst, 0, E, R);
         }
     }
     __syncwarp();
-    for (int s = t; s < sE; ++s) {
+    for (int s = t > 5 ? t : 5; s < sE; ++s) {
         const int seg = 1 << s;
         if (active) {
             const uint32_t *sl = F.beta_row(s, F.ib(ibuf, s, ipath));
-            if (seg >= 32) {
-                const int a = (E - 2 * seg) >> 5, bb = (E - seg) >> 5;
-                for (int w = sub; w < (seg >> 5); w += G) dst[a + w] = sl[w] ^ dst[bb + w];
-            } else if (sub == 0) {
-                const uint32_t v = (sl[0] & ((1u << seg) - 1u)) ^ bits_get(dst, E - seg, seg);
-                bits_put(dst, E - 2 * seg, seg, v);
-            }
+            const int a = (E - 2 * seg) >> 5, bb = (E - seg) >> 5;
+            for (int w = sub; w < (seg >> 5); w += G) dst[a + w] = sl[w] ^ dst[bb + w];
         }
         __syncwarp();
     }
@@ -1009,7 +1049,13 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW, CFG> &F, const DOp &o, 
     int par = 0;
     if (Gl == 1) {
         if (active && sub == 0 && m >= 32) {
-            // whole 32-element blocks: all (quad) loads in flight before the serial scan
+            // whole 32-element blocks: all (quad) loads in flight, then NCH
+            // independent scan chains (element j in chain j % NCH, ascending
+            // within a chain), merged by (magnitude, index) at the end
+            constexpr int NCH = K == 2 ? 4 : 2;
+            TopK<K> tc[NCH];
+#pragma unroll
+            for (int h = 0; h < NCH; ++h) tc[h].init();
             for (int w0 = 0; w0 < m; w0 += 32) {
                 float v[32];
 #pragma unroll
@@ -1023,11 +1069,16 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW, CFG> &F, const DOp &o, 
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     word |= (v[j] < 0.f ? 1u : 0u) << j;
-                    tk.push_scan(fabsf(v[j]), w0 + j);
+                    tc[j % NCH].push_scan(fabsf(v[j]), w0 + j);
                 }
                 F.hard(F.par, w0 >> 5, q) = word;
                 par ^= __popc(word);
             }
+            tk = tc[0];
+#pragma unroll
+            for (int h = 1; h < NCH; ++h)
+#pragma unroll
+                for (int e = 0; e < K; ++e) tk.insert(tc[h].m[e], tc[h].i[e]);
         } else if (S::kQuad && active && sub == 0 && m >= 4) {
             // m = 4, 8, 16: quads, loads first
             float v[16];
