@@ -131,16 +131,19 @@ struct V4<int8_t> {
 // Stored alpha rows (FrameLayout).  PPW >= 16 (one or two lanes per path in
 // the steady state): quad-interleaved -- a block of PPW rows stores quad x
 // (elements 4x .. 4x+3) of local row rl at quad index
-// x * PPW + ((rl + c(x)) mod PPW), c(x) = x (PPW = 32) or x * PPW / 4, so the
+// x * PPW + ((rl + c(x)) mod PPW), c(x) = (x mod GS) * 8 / GS (GS = 32 / PPW
+// steady-state lanes per path: 0 for PPW = 32, 4 (x odd) for PPW = 16), so the
 // steady-state lanes read their quads with 128-bit accesses from 512
-// contiguous bytes, bank-conflict free.  PPW <= 8 (four or more lanes per
-// path): element-interleaved, element i of local row rl at i * PPW + rl, the
-// lanes of a path taking consecutive elements (conflict free).
+// contiguous bytes, bank-conflict free, at addresses affine in x (immediate
+// offsets in the unrolled loops).  PPW <= 8 (four or more lanes per path):
+// element-interleaved, element i of local row rl at i * PPW + rl, the lanes
+// of a path taking consecutive elements (conflict free).
 template <int PPW>
 struct Lay {
     static constexpr bool kQuad = PPW >= 16;
+    static constexpr int GS = 32 / PPW;
     static __device__ __forceinline__ int q(int x, int rl) {
-        const int c = PPW == 32 ? x : x * (PPW / 4);
+        const int c = (x & (GS - 1)) * (8 / GS);
         return (x * PPW + ((rl + c) & (PPW - 1))) * 4;
     }
     static __device__ __forceinline__ int e(int i, int rl) { return kQuad ? q(i >> 2, rl) + (i & 3) : i * PPW + rl; }
