@@ -289,10 +289,11 @@ struct Dec {
     int par;            // candidate-buffer parity (toggles at forking leaves)
     int lpar;           // parity used by the last forking leaf
     long long *ph;      // debug: phase timestamps of the current op (or null)
+    const DOp *prog;    // the op program (shared-memory copy when staged)
 
     __device__ Dec(const Params &p, CFG c, unsigned char *s, unsigned char *g)
         : P(p), cfg(c), sm(s), gs(g), lane(threadIdx.x & 31), warp((threadIdx.x >> 5) & (W - 1)), cur(0), par(0),
-          lpar(0), ph(nullptr) {}
+          lpar(0), ph(nullptr), prog(p.prog) {}
     __device__ __forceinline__ void mark(int i) const {
         if (PB_PROFILE && ph && lane == 0) ph[i] = clock64();
     }
@@ -842,21 +843,22 @@ __device__ __forceinline__ long long warp_min_ll(long long v) {
 // candidate beats the worst kept key it replaces it (REDUX max / min).  Then
 // every key > Tk survives, plus the earliest ties == Tk in (source, cand)
 // order until L are kept.
-template <typename T, int W, int PPW, class CFG>
-__device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const DOp &o) {
-    const int lane = F.lane, np = o.pin, C = o.ncand, L = F.cfg.L();
+template <typename T, int W, int PPW, class CFG, int NC>
+__device__ __forceinline__ void select_phase_c(const Dec<T, W, PPW, CFG> &F, const DOp &o) {
+    const int lane = F.lane, np = o.pin, L = F.cfg.L();
+    constexpr int C = NC;  // candidates per source (compile-time: 2 / 4 / 8)
     const bool vl = lane < np;
     const double pm = vl ? F.pm(F.cur)[lane] : 0.0;
-    long long key[kMaxCand];
+    long long key[NC];
 #pragma unroll
-    for (int c = 0; c < kMaxCand; ++c) key[c] = (vl && c < C) ? okey(pm + F.cd(F.par, c, lane)) : LLONG_MIN;
+    for (int c = 0; c < NC; ++c) key[c] = (vl && c < C) ? okey(pm + F.cd(F.par, c, lane)) : LLONG_MIN;
     unsigned mask;
     if (!o.select) {
         mask = vl ? (1u << C) - 1u : 0u;
     } else {
-        long long srt[kMaxCand];
+        long long srt[NC];
 #pragma unroll
-        for (int c = 0; c < kMaxCand; ++c) srt[c] = key[c];
+        for (int c = 0; c < NC; ++c) srt[c] = key[c];
         // best-first column per lane (Rate-1 columns already are:
         // 0 >= -m1 >= -m2 >= -(m1+m2), monotone under rounding)
         auto cswap = [&](int a, int b) {
@@ -879,7 +881,7 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const
         // lane's exposed candidate is srt[0] of its shifted column.
         long long kept = lane < L ? srt[0] : LLONG_MAX;
 #pragma unroll
-        for (int c = 0; c < kMaxCand; ++c) srt[c] = c + 1 < C ? srt[c + 1 < kMaxCand ? c + 1 : c] : LLONG_MIN;
+        for (int c = 0; c < NC; ++c) srt[c] = c + 1 < C ? srt[c + 1 < NC ? c + 1 : c] : LLONG_MIN;
         for (;;) {
             const long long cand = srt[0];
             const long long best = warp_max_ll(cand);
@@ -889,7 +891,7 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const
             const int into = __ffs(__ballot_sync(FULL_MASK, kept == worst)) - 1;
             if (lane == from) {
 #pragma unroll
-                for (int c = 0; c < kMaxCand; ++c) srt[c] = c + 1 < kMaxCand ? srt[c + 1] : LLONG_MIN;
+                for (int c = 0; c < NC; ++c) srt[c] = c + 1 < NC ? srt[c + 1] : LLONG_MIN;
             }
             if (lane == into) kept = best;
         }
@@ -898,7 +900,7 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const
         // Tk = the L-th best key; keep all better, then the earliest ties
         int gt = 0, eq = 0;
 #pragma unroll
-        for (int c = 0; c < kMaxCand; ++c) {
+        for (int c = 0; c < NC; ++c) {
             gt += key[c] > Tk;
             eq += key[c] == Tk;
         }
@@ -909,7 +911,7 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const
         int r = eqt <= need ? 0 : excl_scan4(eq, lane);
         mask = 0u;
 #pragma unroll
-        for (int c = 0; c < kMaxCand; ++c) {
+        for (int c = 0; c < NC; ++c) {
             if (key[c] > Tk) {
                 mask |= 1u << c;
             } else if (key[c] == Tk) {
@@ -928,6 +930,16 @@ __device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const
         asg[2 * k + 1] = (uint8_t)c;
         ++k;
     }
+}
+
+template <typename T, int W, int PPW, class CFG>
+__device__ __forceinline__ void select_phase(const Dec<T, W, PPW, CFG> &F, const DOp &o) {
+    if (o.ncand == 2)
+        select_phase_c<T, W, PPW, CFG, 2>(F, o);
+    else if (o.ncand == 4)
+        select_phase_c<T, W, PPW, CFG, 4>(F, o);
+    else
+        select_phase_c<T, W, PPW, CFG, 8>(F, o);
 }
 
 // ----------------------------------------------------- leaf word + chain
@@ -1489,11 +1501,12 @@ struct RtOps {
     template <typename T, int W, int PPW, class CFG>
     __device__ __forceinline__ static void run(Dec<T, W, PPW, CFG> &F, int &np, bool prof) {
         const Params &P = F.P;
-        DOp onext = P.prog[0];
+        const DOp *prog = F.prog;
+        DOp onext = prog[0];
         for (int oi = 0; oi < P.n_ops; ++oi) {
             const long long t0 = prof ? clock64() : 0;
             const DOp o = onext;
-            if (oi + 1 < P.n_ops) onext = P.prog[oi + 1];
+            if (oi + 1 < P.n_ops) onext = prog[oi + 1];
             switch (o.kind) {
                 case DK_F:
                     fg_op<T, W, PPW, CFG, false>(F, o);
@@ -1536,6 +1549,14 @@ __device__ __forceinline__ void decode_frames(const Params &P, const CFG &cfg) {
     unsigned char *gs = P.gscratch ? P.gscratch + (size_t)slot * cfg.gbytes() : nullptr;
     unsigned char *sm = g_smem + (size_t)grp * cfg.smem_bytes();
     const long long stride = (long long)gridDim.x * P.fpc;
+    // the op program, read by every frame once per op: staged in shared memory
+    const DOp *prog = P.prog;
+    if (P.prog_smem) {
+        DOp *sp = reinterpret_cast<DOp *>(g_smem + (size_t)P.fpc * cfg.smem_bytes());
+        for (int i = threadIdx.x; i < P.n_ops; i += blockDim.x) sp[i] = P.prog[i];
+        __syncthreads();
+        prog = sp;
+    }
     // adaptive pass: the frames the single-path pass could not settle
     // (count and row map on the device, written by k_ssc)
     const long long batch = P.batch_dev ? (long long)*P.batch_dev : P.batch;
@@ -1545,6 +1566,7 @@ __device__ __forceinline__ void decode_frames(const Params &P, const CFG &cfg) {
         const long long f = P.frame_map ? (long long)P.frame_map[fi] : fi;
         const bool own = f0 + grp < batch;
         Dec<T, W, PPW, CFG> F(P, cfg, sm, gs);
+        F.prog = prog;
         load_channel(F, f);
         if ((threadIdx.x & (32 * W - 1)) == 0) F.pm(0)[0] = 0.0;
         F.sync();

@@ -98,6 +98,7 @@ struct Params {
     const int32_t *frame_map;   // adaptive pass: frame f reads / writes row frame_map[f], or null
     const int32_t *batch_dev;   // adaptive pass: frame count on the device (<= batch), or null
     int fpc;                    // frames per CTA (W warps each)
+    int prog_smem;              // stage the op program in shared memory (after the frames' blocks)
     int sync_mask;              // CTA barrier after ops with (index & mask) == 0; -1: none
     FrameLayout lay;
 };

@@ -101,6 +101,7 @@ struct pb_handle {
     int fpc = 1;  // frames per CTA
     bool chg = false;  // channel in global scratch (not shared memory)
     size_t smem_frame = 0;
+    size_t prog_smem = 0;  // bytes of the op program staged after the frames (0: read from global)
     unsigned char *d_scratch = nullptr;
     size_t scratch_bytes = 0;
     // staging (host-buffer calls)
@@ -444,6 +445,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         pr.n_ops = (int)h->prog.size();
         pr.fpc = 1;
         pr.sync_mask = -1;
+        pr.prog_smem = 0;
     }
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
@@ -478,6 +480,16 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         h->blocks_per_sm = bps;
     }
     h->grid = h->sms * h->blocks_per_sm;
+    // op program staged in shared memory (PB_PROG_SMEM=1): measured neutral at
+    // L=32 and -10 % at L=8 (less L1), so the program is read through L1 by default
+    if (env_int("PB_PROG_SMEM", 0) && h->blocks_per_sm == 1 &&
+        h->fpc * h->smem_frame + sizeof(pb::DOp) * h->prog.size() <= (size_t)smem_cap) {
+        int bps2 = 0;
+        const size_t tot = h->fpc * h->smem_frame + sizeof(pb::DOp) * h->prog.size();
+        if (pb_occupancy(mode, h->warps, h->ppw, h->chg, tot, h->fpc, &bps2) == cudaSuccess && bps2 >= 1)
+            h->prog_smem = sizeof(pb::DOp) * h->prog.size();
+        cudaGetLastError();
+    }
 
     // ---- single-path pass plan (k_ssc): one warp per frame, everything in
     // shared memory; up to 16 frames per CTA
@@ -582,6 +594,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     pr.op_cycles = nullptr;
     pr.ablate = env_int("PB_ABLATE", 0);
     pr.fpc = h->fpc;
+    pr.prog_smem = h->prog_smem ? 1 : 0;
     // The CTA's frames drift apart op by op (data-dependent selection and
     // memory latencies) and then miss in the instruction cache separately; a
     // CTA barrier every 32 ops regroups them.  Measured: +30% for L >= 16
@@ -736,7 +749,7 @@ int run_kernels(pb_handle *h, const pb::Params &base, int in_type, const Job &j,
     pr.frame_map = adaptive ? j.fail_idx : nullptr;
     pr.batch_dev = adaptive ? j.fail_count : nullptr;
     const int grid = (int)std::min<long long>(h->grid, (j.batch + h->fpc - 1) / h->fpc);
-    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc, st);
+    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc + h->prog_smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
     h->launches += 1;
     return PB_OK;
@@ -820,7 +833,7 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
     int grid = (int)std::min<long long>(h->grid, (pr.batch + h->fpc - 1) / h->fpc);
     if (grid < 1) return PB_OK;
     PB_CUDA(cudaEventRecord(h->ev0, st));
-    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc, st);
+    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc + h->prog_smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
     PB_CUDA(cudaEventRecord(h->ev1, st));
     h->timed = true;
