@@ -97,6 +97,13 @@ __device__ __forceinline__ float g_op(float a, float b, unsigned bit) {
     return v;
 }
 
+template <typename T>
+__device__ __forceinline__ float g_op_bits(float a, float b, unsigned bits, int j) {
+    float v = __fadd_rn(b, __uint_as_float(__float_as_uint(a) ^ ((bits << (31 - j)) & 0x80000000u)));
+    if (Elem<T>::kInt) v = fminf(fmaxf(v, -127.f), 127.f);
+    return v;
+}
+
 __device__ __forceinline__ int log2ceil(int x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
 
 // four consecutive elements (one 128-bit / 32-bit access)
@@ -214,7 +221,7 @@ struct VirtG {
         V4<T>::ld(ch + 4 * x + half, b);
         const unsigned bits = bw[x >> 3] >> ((x & 7) * 4);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = g_op<T>(a[j], b[j], (bits >> j) & 1u);
+        for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(a[j], b[j], bits, j);
     }
     // the beta word of quad x, and get4 with it preloaded (x in that word)
     __device__ __forceinline__ unsigned bits_word(int x) const { return bw[x >> 3]; }
@@ -224,7 +231,7 @@ struct VirtG {
         V4<T>::ld(ch + 4 * x + half, b);
         const unsigned bits = wd >> ((x & 7) * 4);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = g_op<T>(a[j], b[j], (bits >> j) & 1u);
+        for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(a[j], b[j], bits, j);
     }
 };
 // the channel itself (a root leaf)
@@ -408,7 +415,7 @@ __device__ __forceinline__ void fg_row(const S &src, const D &dst, const uint32_
         for (int u = 0; u < UQ; ++u) {
             float o[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op<T>(a[u][j], b[u][j], (bits[u] >> j) & 1u) : f_op(a[u][j], b[u][j]);
+            for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op_bits<T>(a[u][j], b[u][j], bits[u], j) : f_op(a[u][j], b[u][j]);
             dst.put4(x0 + u * G, o);
         }
     }
@@ -418,7 +425,7 @@ __device__ __forceinline__ void fg_row(const S &src, const D &dst, const uint32_
         src.get4(x0 + nq, b);
         const unsigned bits = IS_G ? bw[x0 >> 3] >> ((x0 & 7) * 4) : 0u;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op<T>(a[j], b[j], (bits >> j) & 1u) : f_op(a[j], b[j]);
+        for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op_bits<T>(a[j], b[j], bits, j) : f_op(a[j], b[j]);
         dst.put4(x0, o);
     }
 }
