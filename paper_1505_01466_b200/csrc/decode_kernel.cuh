@@ -72,12 +72,16 @@ template <>
 struct Elem<float> {
     static constexpr bool kInt = false;
     static __device__ __forceinline__ float ld(const float *p) { return *p; }
+    static __device__ __forceinline__ float ldcs(const float *p) { return __ldcs(p); }
     static __device__ __forceinline__ void st(float *p, float v) { *p = v; }
 };
 template <>
 struct Elem<int8_t> {
     static constexpr bool kInt = true;
     static __device__ __forceinline__ float ld(const int8_t *p) { return (float)*p; }
+    static __device__ __forceinline__ float ldcs(const int8_t *p) {
+        return (float)__ldcs(reinterpret_cast<const signed char *>(p));
+    }
     static __device__ __forceinline__ void st(int8_t *p, float v) { *p = (int8_t)__float2int_rn(v); }
 };
 
@@ -115,6 +119,10 @@ struct V4<float> {
         const float4 x = *reinterpret_cast<const float4 *>(p);
         v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
     }
+    static __device__ __forceinline__ void ldcs(const float *p, float (&v)[4]) {
+        const float4 x = __ldcs(reinterpret_cast<const float4 *>(p));
+        v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+    }
     static __device__ __forceinline__ void st(float *p, const float (&v)[4]) {
         *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
     }
@@ -123,6 +131,11 @@ template <>
 struct V4<int8_t> {
     static __device__ __forceinline__ void ld(const int8_t *p, float (&v)[4]) {
         const int x = *reinterpret_cast<const int *>(p);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = (float)((x << (24 - 8 * j)) >> 24);
+    }
+    static __device__ __forceinline__ void ldcs(const int8_t *p, float (&v)[4]) {
+        const int x = __ldcs(reinterpret_cast<const int *>(p));
 #pragma unroll
         for (int j = 0; j < 4; ++j) v[j] = (float)((x << (24 - 8 * j)) >> 24);
     }
@@ -155,15 +168,22 @@ struct Lay {
     }
     static __device__ __forceinline__ int e(int i, int rl) { return kQuad ? q(i >> 2, rl) + (i & 3) : i * PPW + rl; }
 };
-template <typename T, int PPW>
+// LAST: the row's last read (a G or a leaf; F reads first) from global
+// scratch -- evict-first loads, so the L2 keeps the rows still to be read
+template <typename T, int PPW, bool LAST = false>
 struct RowSrc {
     static constexpr bool kQuad = Lay<PPW>::kQuad;
     const T *blk;
     int rl;
-    __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(blk + Lay<PPW>::e(i, rl)); }
+    __device__ __forceinline__ float get(int i) const {
+        return LAST ? Elem<T>::ldcs(blk + Lay<PPW>::e(i, rl)) : Elem<T>::ld(blk + Lay<PPW>::e(i, rl));
+    }
     __device__ __forceinline__ void get4(int x, float (&v)[4]) const {
         if (kQuad) {
-            V4<T>::ld(blk + Lay<PPW>::q(x, rl), v);
+            if (LAST)
+                V4<T>::ldcs(blk + Lay<PPW>::q(x, rl), v);
+            else
+                V4<T>::ld(blk + Lay<PPW>::q(x, rl), v);
         } else {
 #pragma unroll
             for (int j = 0; j < 4; ++j) v[j] = get(4 * x + j);
@@ -430,6 +450,11 @@ __device__ __forceinline__ void fg_row(const S &src, const D &dst, const uint32_
     }
 }
 
+// evict-first loads for the last read of a global-scratch row (RowSrc LAST)
+#ifndef PB_LAST_CS
+#define PB_LAST_CS 1
+#endif
+
 // quads in flight per lane (global-scratch / shared-memory sources)
 #ifndef PB_UQ_GL
 #define PB_UQ_GL 8
@@ -525,7 +550,7 @@ __device__ __forceinline__ void fg_far_body(Dec<T, W, PPW, CFG> &F, const DOp &o
                 G, sub);
     } else {
         const int r = F.ia(F.cur, s, q);
-        fg_to_dst<T, W, PPW, CFG, IS_G, true>(F, RowSrc<T, PPW>{F.a_gl(s) + F.blkoff(s, r), r & (PPW - 1)}, s, q, bw,
+        fg_to_dst<T, W, PPW, CFG, IS_G, true>(F, RowSrc<T, PPW, IS_G && PB_LAST_CS>{F.a_gl(s) + F.blkoff(s, r), r & (PPW - 1)}, s, q, bw,
                                              h, G, sub);
     }
 }
@@ -1248,7 +1273,7 @@ __device__ __forceinline__ void leaf_read_far_body(Dec<T, W, PPW, CFG> &F, const
                          active, G, sub);
     } else {
         const int r = F.ia(F.cur, t, qq);
-        leaf_phase_a(F, o, kind, RowSrc<T, PPW>{F.a_gl(t) + F.blkoff(t, r), r & (PPW - 1)}, q, active, G, sub);
+        leaf_phase_a(F, o, kind, RowSrc<T, PPW, PB_LAST_CS>{F.a_gl(t) + F.blkoff(t, r), r & (PPW - 1)}, q, active, G, sub);
     }
 }
 template <typename T, int W, int PPW, class CFG>
