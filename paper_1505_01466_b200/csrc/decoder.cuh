@@ -119,6 +119,12 @@ struct SscLayout {
 
 enum : int { SSC_LIST_L1 = 0, SSC_FAST = 1, SSC_ADAPTIVE = 2 };
 
+// threads per CTA of k_ssc (__launch_bounds__): 1024 = 32 frames per SM at 64
+// registers, the channel in global scratch to fit them
+#ifndef PB_SSC_MAXT
+#define PB_SSC_MAXT 1024
+#endif
+
 struct SscParams {
     const DOp *prog;
     int n_ops;
@@ -139,6 +145,7 @@ struct SscParams {
     int32_t *fail_idx;          // adaptive: frames whose CRC failed (unordered)
     int32_t *fail_count;        // adaptive: their number
     uint32_t *cw_out;           // [B][N/32] packed codeword, or null
+    unsigned char *gch;         // channel in global scratch ([CTA slots][N] of T), or null: shared memory
     int fpc;                    // frames (warps) per CTA
     SscLayout lay;
 };

@@ -121,6 +121,8 @@ struct pb_handle {
     pb::SscParams ssc{};
     int ssc_grid = 0;
     bool l1_ssc = false;         // route L = 1 decodes through k_ssc
+    bool ssc_chg = false;        // k_ssc channel in global scratch
+    unsigned char *d_ssc_ch = nullptr;
     int32_t *d_fail = nullptr;   // adaptive: failing frame indices + per-chunk counts
     size_t d_fail_cap = 0;
     // on-device frame generation: all K info positions, payload syndrome rows
@@ -491,25 +493,35 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         cudaGetLastError();
     }
 
-    // ---- single-path pass plan (k_ssc): one warp per frame, everything in
-    // shared memory; up to 16 frames per CTA
+    // ---- single-path pass plan (k_ssc): one warp per frame, up to
+    // PB_SSC_MAXT/32 frames per CTA; the channel goes to global scratch when
+    // that fits more frames (shared memory holds alpha, beta, codeword)
     {
         pb::SscLayout &sl = h->ssc.lay;
-        int off = 0;
-        sl.ch_off = 0;
-        off = align_up(N * es, 16);
-        for (int s = 0; s <= n - 2; ++s) {
-            sl.a_off[s] = off;
-            off = align_up(off + (1 << s) * es, 16);
-        }
-        for (int s = 0; s < n; ++s) {
-            sl.b_off[s] = off;
-            off = align_up(off + std::max(1, (1 << s) / 32) * 4, 16);
-        }
-        sl.root_off = off;
-        off = align_up(off + std::max(1, N / 32) * 4, 16);
-        sl.smem_bytes = off;
-        int sfpc = std::min(16, smem_cap / std::max(1, off));
+        auto plan = [&](bool chg) {
+            int off = 0;
+            sl.ch_off = 0;
+            off = chg ? 0 : align_up(N * es, 16);
+            for (int s = 0; s <= n - 2; ++s) {
+                sl.a_off[s] = off;
+                off = align_up(off + (1 << s) * es, 16);
+            }
+            for (int s = 0; s < n; ++s) {
+                sl.b_off[s] = off;
+                off = align_up(off + std::max(1, (1 << s) / 32) * 4, 16);
+            }
+            sl.root_off = off;
+            off = align_up(off + std::max(1, N / 32) * 4, 16);
+            sl.smem_bytes = off;
+            return off;
+        };
+        const int maxf = PB_SSC_MAXT / 32;
+        const int fs = plan(false), fg = plan(true);
+        const int chg_env = env_int("PB_SSC_CH_GLOBAL", -1);
+        bool chg = std::min(maxf, smem_cap / std::max(1, fg)) > std::min(maxf, smem_cap / std::max(1, fs));
+        if (chg_env >= 0) chg = chg_env != 0;
+        const int off = plan(chg);
+        int sfpc = std::min(std::min(maxf, env_int("PB_SSC_FPC", maxf)), smem_cap / std::max(1, off));
         int bps = 0;
         while (sfpc >= 1) {
             if (pb_occupancy_ssc(mode, sfpc, off, &bps) == cudaSuccess && bps >= 1) break;
@@ -520,6 +532,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
             h->ssc_ok = true;
             h->ssc.fpc = sfpc;
             h->ssc_grid = h->sms * bps;
+            h->ssc_chg = chg;
         }
         h->l1_ssc = h->ssc_ok && L == 1 && env_int("PB_L1_LIST", 0) == 0;
     }
@@ -573,6 +586,12 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
             return cuda_fail(e, "cudaMalloc scratch");
         }
     }
+    if (h->ssc_ok && h->ssc_chg) {
+        if ((e = cudaMalloc(&h->d_ssc_ch, (size_t)h->ssc_grid * h->ssc.fpc * N * es)) != cudaSuccess) {
+            pb_destroy(h);
+            return cuda_fail(e, "cudaMalloc single-path channel scratch");
+        }
+    }
     cudaEventCreate(&h->ev0);
     cudaEventCreate(&h->ev1);
 
@@ -613,6 +632,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         sp.k = code->k;
         sp.has_crc = w != 0;
         sp.crc_const = crc_const;
+        sp.gch = h->d_ssc_ch;
     }
 
     char buf[1024];
@@ -621,11 +641,11 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
              "\"smem_per_frame\": %d, \"alpha_global_from_stage\": %d, \"global_scratch_per_frame\": %d, "
              "\"frames_per_sm\": %d, \"sms\": %d, \"grid\": %d, \"block\": %d, \"warps_per_frame\": %d, "
              "\"paths_per_warp\": %d, \"frames_per_cta\": %d, \"channel_in_global\": %d, "
-             "\"ssc\": {\"smem_per_frame\": %d, \"frames_per_cta\": %d, \"grid\": %d, \"l1_decodes\": %d}}",
+             "\"ssc\": {\"smem_per_frame\": %d, \"frames_per_cta\": %d, \"grid\": %d, \"l1_decodes\": %d, \"channel_in_global\": %d}}",
              N, code->k, L, mode == PB_MODE_F32 ? "f32" : "int8", n_ops, (int)h->prog.size(),
              lay.smem_bytes, lay.a_gfrom, lay.gbytes, h->blocks_per_sm * h->fpc, h->sms, h->grid,
              32 * h->warps * h->fpc, h->warps, h->ppw, h->fpc, (int)h->chg, h->ssc.lay.smem_bytes,
-             h->ssc_ok ? h->ssc.fpc : 0, h->ssc_grid, (int)h->l1_ssc);
+             h->ssc_ok ? h->ssc.fpc : 0, h->ssc_grid, (int)h->l1_ssc, (int)h->ssc_chg);
     h->plan_json = buf;
     *out = h;
     return PB_OK;
@@ -640,6 +660,7 @@ int pb_destroy(pb_handle *h) {
     cudaFree(h->d_in);
     cudaFree(h->d_out);
     cudaFree(h->d_fail);
+    cudaFree(h->d_ssc_ch);
     cudaFree(h->d_info_all);
     cudaFree(h->d_hu);
     if (h->ev0) cudaEventDestroy(h->ev0);

@@ -96,7 +96,10 @@ struct Frame {
     unsigned char *sm;
     int lane;
     double pm;
-    __device__ __forceinline__ T *ch() const { return reinterpret_cast<T *>(sm + P.lay.ch_off); }
+    unsigned char *gch;  // this frame slot's global channel, or null
+    __device__ __forceinline__ T *ch() const {
+        return reinterpret_cast<T *>(gch ? gch : sm + P.lay.ch_off);
+    }
     __device__ __forceinline__ T *a(int s) const { return reinterpret_cast<T *>(sm + P.lay.a_off[s]); }
     __device__ __forceinline__ uint32_t *b(int s) const { return reinterpret_cast<uint32_t *>(sm + P.lay.b_off[s]); }
     __device__ __forceinline__ uint32_t *root() const { return reinterpret_cast<uint32_t *>(sm + P.lay.root_off); }
@@ -328,9 +331,10 @@ __device__ __forceinline__ void run_frame(Frame<T> &F, long long f) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(512, 1) k_ssc(const __grid_constant__ SscParams P) {
+__global__ void __launch_bounds__(PB_SSC_MAXT, 1) k_ssc(const __grid_constant__ SscParams P) {
     const int warp = threadIdx.x >> 5;
-    Frame<T> F{P, g_smem + (size_t)warp * P.lay.smem_bytes, (int)(threadIdx.x & 31), 0.0};
+    unsigned char *gch = P.gch ? P.gch + ((size_t)blockIdx.x * P.fpc + warp) * P.N * sizeof(T) : nullptr;
+    Frame<T> F{P, g_smem + (size_t)warp * P.lay.smem_bytes, (int)(threadIdx.x & 31), 0.0, gch};
     const long long stride = (long long)gridDim.x * P.fpc;
     for (long long f = (long long)blockIdx.x * P.fpc + warp; f < P.batch; f += stride) run_frame(F, f);
 }
