@@ -307,6 +307,8 @@ struct Dec {
     static constexpr int LP = ilog2(PPW);
     static constexpr int GSS = 32 / PPW;           // steady-state lanes per path
     static constexpr int NBUF = W > 1 ? 2 : 1;     // candidate buffers
+    static constexpr int RW = PPW * W;              // path rows (>= L): the per-path arrays' stride
+    static constexpr int IW = (kMaxLog + 3) / 4;    // index words per path (4 stages each)
     const Params &P;
     CFG cfg;
     unsigned char *sm;  // this frame's shared-memory block
@@ -337,34 +339,34 @@ struct Dec {
         return reinterpret_cast<T *>((CFG::kChGlobal ? gs : sm) + cfg.ch_off());
     }
     __device__ __forceinline__ double *pm(int b) const {
-        return reinterpret_cast<double *>(sm + cfg.pm_off()) + b * cfg.L();
+        return reinterpret_cast<double *>(sm + cfg.pm_off()) + b * RW;
     }
     // alpha / beta row index of path q at stage / slot s, four stages per
     // word: byte (s & 3) of word [buf][s >> 2][path]
     __device__ __forceinline__ uint8_t &ia(int b, int s, int q) const {
-        return sm[cfg.ia_off() + ((b * cfg.idx_stride() + (s >> 2)) * cfg.L() + q) * 4 + (s & 3)];
+        return sm[cfg.ia_off() + ((b * IW + (s >> 2)) * RW + q) * 4 + (s & 3)];
     }
     __device__ __forceinline__ uint8_t &ib(int b, int s, int q) const {
-        return sm[cfg.ib_off() + ((b * cfg.idx_stride() + (s >> 2)) * cfg.L() + q) * 4 + (s & 3)];
+        return sm[cfg.ib_off() + ((b * IW + (s >> 2)) * RW + q) * 4 + (s & 3)];
     }
     __device__ __forceinline__ uint32_t &iaw(int b, int x, int q) const {
-        return reinterpret_cast<uint32_t *>(sm + cfg.ia_off())[(b * cfg.idx_stride() + x) * cfg.L() + q];
+        return reinterpret_cast<uint32_t *>(sm + cfg.ia_off())[(b * IW + x) * RW + q];
     }
     __device__ __forceinline__ uint32_t &ibw(int b, int x, int q) const {
-        return reinterpret_cast<uint32_t *>(sm + cfg.ib_off())[(b * cfg.idx_stride() + x) * cfg.L() + q];
+        return reinterpret_cast<uint32_t *>(sm + cfg.ib_off())[(b * IW + x) * RW + q];
     }
     __device__ __forceinline__ int bsel(int b) const { return NBUF > 1 ? b : 0; }
     // candidate data: [buf][entry][source path]
     __device__ __forceinline__ double &cd(int b, int c, int q) const {
-        return reinterpret_cast<double *>(sm + cfg.cd_off())[(bsel(b) * kMaxCand + c) * cfg.L() + q];
+        return reinterpret_cast<double *>(sm + cfg.cd_off())[(bsel(b) * kMaxCand + c) * RW + q];
     }
     __device__ __forceinline__ uint16_t &clrb(int b, int j, int q) const {
-        return reinterpret_cast<uint16_t *>(sm + cfg.clrb_off())[(bsel(b) * 4 + j) * cfg.L() + q];
+        return reinterpret_cast<uint16_t *>(sm + cfg.clrb_off())[(bsel(b) * 4 + j) * RW + q];
     }
-    __device__ __forceinline__ uint8_t *cflag(int b) const { return sm + cfg.cflag_off() + bsel(b) * cfg.L(); }
-    __device__ __forceinline__ uint8_t *asg(int b) const { return sm + cfg.asg_off() + bsel(b) * 2 * cfg.L(); }
+    __device__ __forceinline__ uint8_t *cflag(int b) const { return sm + cfg.cflag_off() + bsel(b) * RW; }
+    __device__ __forceinline__ uint8_t *asg(int b) const { return sm + cfg.asg_off() + bsel(b) * 2 * RW; }
     __device__ __forceinline__ uint32_t &hard(int b, int w, int q) const {
-        return reinterpret_cast<uint32_t *>(sm + cfg.hard_off())[(bsel(b) * cfg.hard_words() + w) * cfg.L() + q];
+        return reinterpret_cast<uint32_t *>(sm + cfg.hard_off())[(bsel(b) * cfg.hard_words() + w) * RW + q];
     }
     __device__ __forceinline__ uint32_t *root() const { return reinterpret_cast<uint32_t *>(sm + cfg.root_off()); }
 
@@ -1094,6 +1096,7 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW, CFG> &F, const DOp &o, 
     TopK<K> tk;
     tk.init();
     int par = 0;
+    float mag4[4] = {0.f, 0.f, 0.f, 0.f};  // SPC of size 4: |a| by position
     if (Gl == 1) {
         if (active && sub == 0 && m >= 32) {
             // whole 32-element blocks: all (quad) loads in flight, then NCH
@@ -1126,6 +1129,35 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW, CFG> &F, const DOp &o, 
             for (int h = 1; h < NCH; ++h)
 #pragma unroll
                 for (int e = 0; e < K; ++e) tk.insert(tc[h].m[e], tc[h].i[e]);
+        } else if (K == 4 && active && sub == 0 && m == 4) {
+            // SPC of size 4 (the default cap): every position is a least
+            // reliable one -- a stable 5-comparator sort of (|a|, index)
+            float qv[4];
+            src.get4(0, qv);
+            uint32_t word = 0u;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                word |= (qv[e] < 0.f ? 1u : 0u) << e;
+                mag4[e] = fabsf(qv[e]);
+                tk.m[e] = mag4[e];
+                tk.i[e] = e;
+            }
+            auto cx = [&](int a, int b) {  // (m, i) lexicographic: a before b
+                const bool sw = tk.m[b] < tk.m[a] || (tk.m[b] == tk.m[a] && tk.i[b] < tk.i[a]);
+                const float ma = tk.m[a], mb = tk.m[b];
+                const int ia = tk.i[a], ib = tk.i[b];
+                tk.m[a] = sw ? mb : ma;
+                tk.m[b] = sw ? ma : mb;
+                tk.i[a] = sw ? ib : ia;
+                tk.i[b] = sw ? ia : ib;
+            };
+            cx(0, 1);
+            cx(2, 3);
+            cx(0, 2);
+            cx(1, 3);
+            cx(1, 2);
+            F.hard(F.par, 0, q) = word;
+            par ^= __popc(word);
         } else if (S::kQuad && active && sub == 0 && m >= 4) {
             // m = 4, 8, 16: quads, loads first
             float v[16];
@@ -1210,19 +1242,27 @@ __device__ __forceinline__ void leaf_scan(Dec<T, W, PPW, CFG> &F, const DOp &o, 
     // rank of each LRB slot by position (the reference sums net flips in
     // ascending position order); all indices static
     int rk[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        rk[x] = 0;
-#pragma unroll
-        for (int y = 0; y < 4; ++y) rk[x] += tk.i[y & (K - 1)] < tk.i[x & (K - 1)] ? 1 : 0;
-    }
     double wr[4];  // magnitudes by position rank
+    if (m == 4 && Gl == 1) {  // the four positions are 0..3: rank = position
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        double v = 0.0;
+        for (int x = 0; x < 4; ++x) {
+            rk[x] = tk.i[x & (K - 1)];
+            wr[x] = (double)mag4[x];
+        }
+    } else {
 #pragma unroll
-        for (int x = 0; x < 4; ++x) v = rk[x] == r ? (double)tk.m[x & (K - 1)] : v;
-        wr[r] = v;
+        for (int x = 0; x < 4; ++x) {
+            rk[x] = 0;
+#pragma unroll
+            for (int y = 0; y < 4; ++y) rk[x] += tk.i[y & (K - 1)] < tk.i[x & (K - 1)] ? 1 : 0;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double v = 0.0;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) v = rk[x] == r ? (double)tk.m[x & (K - 1)] : v;
+            wr[r] = v;
+        }
     }
 #pragma unroll
     for (int c = 0; c < kMaxCand; ++c) {

@@ -364,25 +364,28 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
                 off = align_up(off + L * lay.b_stride[s] * 4, 16);
             }
         }
+        // per-path arrays: stride `rows` (= PPW * W >= L, compile-time in the
+        // kernel), index vectors (kMaxLog + 3) / 4 words per path
+        const int iw = (pb::kMaxLog + 3) / 4;
         lay.pm_off = off;
-        off = align_up(off + 2 * L * 8, 16);
-        lay.idx_stride = std::max(1, (n + 3) / 4);  // index words per path (4 stages per word)
+        off = align_up(off + 2 * rows * 8, 16);
+        lay.idx_stride = std::max(1, (n + 3) / 4);  // index words in use per path (4 stages per word)
         lay.ia_off = off;
-        off = align_up(off + 2 * L * lay.idx_stride * 4, 16);
+        off = align_up(off + 2 * rows * iw * 4, 16);
         lay.ib_off = off;
-        off = align_up(off + 2 * L * lay.idx_stride * 4, 16);
+        off = align_up(off + 2 * rows * iw * 4, 16);
         const int nbuf = warps > 1 ? 2 : 1;  // candidate buffers (by leaf parity across warps)
         lay.cd_off = off;
-        off = align_up(off + nbuf * L * pb::kMaxCand * 8, 16);
+        off = align_up(off + nbuf * rows * pb::kMaxCand * 8, 16);
         lay.clrb_off = off;
-        off = align_up(off + nbuf * L * 4 * 2, 16);
+        off = align_up(off + nbuf * rows * 4 * 2, 16);
         lay.cflag_off = off;
-        off = align_up(off + nbuf * L, 16);
+        off = align_up(off + nbuf * rows, 16);
         lay.asg_off = off;
-        off = align_up(off + nbuf * 2 * L, 16);
+        off = align_up(off + nbuf * 2 * rows, 16);
         lay.hard_words = std::max(1, max_hard / 32);
         lay.hard_off = off;
-        off = align_up(off + nbuf * L * lay.hard_words * 4, 16);
+        off = align_up(off + nbuf * rows * lay.hard_words * 4, 16);
         lay.root_words = std::max(1, N / 32);
         lay.root_off = off;
         off = align_up(off + lay.root_words * 4, 16);
