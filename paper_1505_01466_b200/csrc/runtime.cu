@@ -899,7 +899,10 @@ int decode_impl(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8
     // last copy-out, the less of them is exposed (measured e2e / device-
     // resident: 6 waves 95 %, 1 wave 99 % on c3 L=32); consecutive chunks'
     // kernels overlap across the two streams, hiding each wave's tail
-    const long long chunk = std::max<long long>(1, env_int("PB_CHUNK_FRAMES", std::max(2048, h->grid * h->fpc)));
+    // (adaptive decoding: 6 waves, so each chunk's list pass over its few
+    // CRC failures amortises its launch and its grid-wide occupancy)
+    const long long chunk = std::max<long long>(
+        1, env_int("PB_CHUNK_FRAMES", std::max(2048, (adaptive ? 6 : 1) * h->grid * h->fpc)));
     if (!dev_in && batch > chunk)
         return decode_pipelined(h, h->base, llr, in_type, in_es, batch, chunk, info_out, crc_ok, pm_out, paths_used,
                                 invoked, adaptive, st);
