@@ -395,6 +395,19 @@ struct Dec {
         m.q = warp * PPW + ql;
         return m;
     }
+    // the same with log2 lanes per path precomputed on the host (DOp::lgi /
+    // lgo; one warp per frame, where every path is this warp's)
+    __device__ __forceinline__ Map map(int np, int lgp) const {
+        if (W > 1) return map(np);
+        Map m;
+        m.lg = lgp;
+        m.G = 1 << lgp;
+        const int ql = lane >> lgp;
+        m.sub = lane & (m.G - 1);
+        m.active = ql < np;
+        m.q = ql;
+        return m;
+    }
 };
 
 // ---------------------------------------------------------------- F / G
@@ -566,7 +579,7 @@ __device__ __noinline__ void fg_far(const Params &P, unsigned char *sm, unsigned
 
 template <typename T, int W, int PPW, class CFG, bool IS_G>
 __device__ __forceinline__ void fg_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
-    const auto mp = F.map(o.pin);
+    const auto mp = F.map(o.pin, o.lgi);
     if (!mp.active || PB_ABL(F.P, 8)) return;
     const CFG &cfg = F.cfg;
     const int s = o.stage, h = 1 << (s - 1), q = mp.q;
@@ -1352,7 +1365,7 @@ __device__ __forceinline__ void leaf_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
 
     // Phase A: per-source sums / scans, this warp's sources
     if (!PB_ABL(P, 1)) {
-        const auto mp = F.map(o.pin);
+        const auto mp = F.map(o.pin, o.lgi);
         leaf_read(F, o, kind, mp.q, mp.active, mp.G, mp.sub);
     }
     F.sync();
@@ -1370,7 +1383,7 @@ __device__ __forceinline__ void leaf_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
     F.mark(1);
 
     // Phase C: materialise survivors k < pout (this warp's)
-    const auto mp = F.map(o.pout);
+    const auto mp = F.map(o.pout, o.lgo);
     const int k = mp.q;
     const int nxt = fork ? F.cur ^ 1 : F.cur;
     const int b = F.par;

@@ -38,7 +38,9 @@ struct __align__(16) DOp {
     int8_t select;   // leaf: pin*ncand > L (a real 2L->L selection)
     int8_t vmode;    // how this op reads stage n-1 (VM_*), else VM_NONE
     int32_t off;     // leaf: first u index covered
+    int8_t lgi, lgo; // one warp per frame: log2 lanes per path for pin / pout paths
 };
+static_assert(sizeof(DOp) == 16, "DOp is one 16-byte load");
 
 // Per-frame storage plan.  Offsets in bytes from the frame's shared-memory
 // block, or from its global scratch block for alpha stages >= a_gfrom.

@@ -336,6 +336,17 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     const int rows = ppw * warps;  // alpha rows, padded to whole interleave blocks
     h->ppw = ppw;
     h->warps = warps;
+    // lanes per path of each op's input / output path count (one warp per frame)
+    for (pb::DOp &d : h->prog) {
+        auto lg = [&](int np) {
+            const int act = std::max(1, std::min(np, ppw));
+            int c = 0;
+            while ((1 << c) < act) ++c;
+            return (int8_t)(5 - c);
+        };
+        d.lgi = lg(d.pin);
+        d.lgo = lg(d.pout);
+    }
     const int smem_cap = 227 * 1024;
     // resident frames per SM: one warp each, up to the launch bound
     const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", pb::kMaxThreads / 32));
