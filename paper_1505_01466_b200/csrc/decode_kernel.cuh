@@ -1581,17 +1581,30 @@ __device__ __forceinline__ void load_channel(const Dec<T, W, PPW, CFG> &F, long 
     }
 }
 
+#ifndef PB_OP_PREFETCH
+#define PB_OP_PREFETCH 0
+#endif
 // The op program interpreted from the schedule (runtime configuration).
 struct RtOps {
     template <typename T, int W, int PPW, class CFG>
     __device__ __forceinline__ static void run(Dec<T, W, PPW, CFG> &F, int &np, bool prof) {
         const Params &P = F.P;
         const DOp *prog = F.prog;
+#if PB_OP_PREFETCH
         DOp onext = prog[0];
+#endif
         for (int oi = 0; oi < P.n_ops; ++oi) {
             const long long t0 = prof ? clock64() : 0;
+#if PB_OP_PREFETCH
             const DOp o = onext;
             if (oi + 1 < P.n_ops) onext = prog[oi + 1];
+#else
+            // loaded at the top of the op (constant bank, or an L1 / shared
+            // hit): a prefetched next op stays live across the whole op body
+            // and was spilled and reloaded around every op (~15 local
+            // accesses per op)
+            const DOp o = P.prog_inline ? P.iprog[oi] : prog[oi];
+#endif
             switch (o.kind) {
                 case DK_F:
                     fg_op<T, W, PPW, CFG, false>(F, o);

@@ -10,6 +10,7 @@ namespace pb {
 constexpr int kMaxLog = 16;     // N <= 65536
 constexpr int kMaxL = 32;       // selection runs on one warp: one lane per source path
 constexpr int kMaxCand = 8;
+constexpr int kInlineOps = 1536;  // op programs up to this long travel in the kernel parameters (24 KB)
 
 // threads per CTA the kernels are compiled for (__launch_bounds__): the
 // register budget per thread is 65536 / PB_MAXT.  512 = 16 single-warp frames
@@ -103,6 +104,10 @@ struct Params {
     int prog_smem;              // stage the op program in shared memory (after the frames' blocks)
     int sync_mask;              // CTA barrier after ops with (index & mask) == 0; -1: none
     FrameLayout lay;
+    // the op program in the kernel's parameter space (constant bank: a
+    // warp-uniform load per op, no L1 / register residency) when it fits
+    int prog_inline;
+    DOp iprog[kInlineOps];
 };
 
 // ---------------------------------------------------------------------

@@ -462,6 +462,10 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         pr.fpc = 1;
         pr.sync_mask = -1;
         pr.prog_smem = 0;
+        // measured (same-box A/B): +3 % c3 L=32, +4 % c5 L=16, +1 % int8
+        // L=32 over a global-memory program; -4 % at 8 paths per warp (c3 L=8)
+        pr.prog_inline = (int)h->prog.size() <= pb::kInlineOps && env_int("PB_PROG_PARAM", ppw >= 16 ? 1 : 0) != 0;
+        if (pr.prog_inline) std::copy(h->prog.begin(), h->prog.end(), pr.iprog);
     }
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
