@@ -254,6 +254,35 @@ struct VirtG {
         for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(a[j], b[j], bits, j);
     }
 };
+// Leaf fusion (DOp::fuse) is compiled for the int8 shapes only: measured
+// +3.5 % on c4 int8 L=32, while in the float32 shapes the extra leaf
+// instantiations cost registers / spills and lost 2.5-5 % (c3 L=32).
+template <typename T>
+constexpr bool kFuseLeaf = Elem<T>::kInt;
+
+// f / g of a stored parent row's halves (a leaf fused with the F / G that
+// would have stored its LLRs, DOp::fuse); g with the path's left-sibling bits
+template <typename T, bool IS_G, class S>
+struct FusedSrc {
+    static constexpr bool kQuad = true;
+    S in;
+    const uint32_t *bw;
+    int half;  // the leaf's size
+    __device__ __forceinline__ float get(int i) const {
+        const float a = in.get(i), b = in.get(i + half);
+        return IS_G ? g_op<T>(a, b, (bw[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+    }
+    __device__ __forceinline__ void get4(int x, float (&v)[4]) const {
+        float a[4], b[4];
+        in.get4(x, a);
+        in.get4(x + (half >> 2), b);
+        const unsigned bits = IS_G ? bw[x >> 3] >> ((x & 7) * 4) : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = IS_G ? g_op_bits<T>(a[j], b[j], bits, j) : f_op(a[j], b[j]);
+    }
+    __device__ __forceinline__ unsigned bits_word(int) const { return 0u; }
+    __device__ __forceinline__ void get4w(int x, float (&v)[4], unsigned) const { get4(x, v); }
+};
 // the channel itself (a root leaf)
 template <typename T>
 struct ChanSrc {
@@ -579,6 +608,7 @@ __device__ __noinline__ void fg_far(const Params &P, unsigned char *sm, unsigned
 
 template <typename T, int W, int PPW, class CFG, bool IS_G>
 __device__ __forceinline__ void fg_op(Dec<T, W, PPW, CFG> &F, const DOp &o) {
+    if (kFuseLeaf<T> && o.fuse < 0) return;  // fused into the next leaf (it reads this op's source)
     const auto mp = F.map(o.pin, o.lgi);
     if (!mp.active || PB_ABL(F.P, 8)) return;
     const CFG &cfg = F.cfg;
@@ -1344,6 +1374,19 @@ __device__ __forceinline__ void leaf_read(Dec<T, W, PPW, CFG> &F, const DOp &o, 
                                           int sub) {
     const CFG &cfg = F.cfg;
     const int t = o.stage;
+    if constexpr (kFuseLeaf<T>) {
+        if (o.fuse > 0) {  // f / g of the parent's shared-memory row (DOp::fuse)
+            const int qq = active ? q : F.warp * PPW;
+            const int r = F.ia(F.cur, t + 1, qq);
+            const RowSrc<T, PPW> in{F.a_sm(t + 1) + F.blkoff(t + 1, r), r & (PPW - 1)};
+            if (o.fuse == 1)
+                leaf_phase_a(F, o, kind, FusedSrc<T, false, RowSrc<T, PPW>>{in, nullptr, 1 << t}, q, active, G, sub);
+            else
+                leaf_phase_a(F, o, kind, FusedSrc<T, true, RowSrc<T, PPW>>{in, F.beta_row(t, F.ib(F.cur, t, qq)), 1 << t},
+                             q, active, G, sub);
+            return;
+        }
+    }
     if (t >= cfg.n() - 1 || t >= cfg.a_gfrom()) {
         if (PB_FAR && !PB_PROFILE)
             leaf_read_far<T, W, PPW, CFG>(F.P, F.sm, F.gs, F.cur, F.par, o, kind, q, active, G, sub);

@@ -40,6 +40,10 @@ struct __align__(16) DOp {
     int8_t vmode;    // how this op reads stage n-1 (VM_*), else VM_NONE
     int32_t off;     // leaf: first u index covered
     int8_t lgi, lgo; // one warp per frame: log2 lanes per path for pin / pout paths
+    // list kernel, F / G fused into the leaf that reads its output (PB_FUSE_LEAF):
+    // -1 on the F / G (skipped), 1 / 2 on the leaf (reads f / g of its parent's
+    // stored rows); else 0.  The single-path kernel ignores it.
+    int8_t fuse;
 };
 static_assert(sizeof(DOp) == 16, "DOp is one 16-byte load");
 

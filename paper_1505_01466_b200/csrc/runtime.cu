@@ -445,6 +445,24 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
                                    std::to_string(lay.smem_bytes) + " bytes)");
     }
     h->smem_frame = lay.smem_bytes;
+    // A leaf reads f / g of its parent's rows directly when those are in
+    // shared memory (PB_FUSE_LEAF; int8 only, the kernels compile it for the
+    // int8 shapes alone): the F / G before it (the one that would store the
+    // leaf's LLRs) is skipped -- one op, one row store and one row load fewer
+    // per leaf.  Stage n-1 parents are recomputed from the channel and
+    // global-scratch parents keep their F / G.
+    if (mode == PB_MODE_INT8 && env_int("PB_FUSE_LEAF", 1) != 0) {
+        for (size_t i = 1; i < h->prog.size(); ++i) {
+            pb::DOp &d = h->prog[i], &pf = h->prog[i - 1];
+            const bool leaf = d.kind == pb::DK_R0 || d.kind == pb::DK_REP || d.kind == pb::DK_R1 || d.kind == pb::DK_SPC;
+            const bool fg = pf.kind == pb::DK_F || pf.kind == pb::DK_G;
+            const int ps = d.stage + 1;
+            if (leaf && fg && pf.stage == ps && ps <= n - 2 && ps < lay.a_gfrom && pf.pin == d.pin) {
+                pf.fuse = -1;
+                d.fuse = pf.kind == pb::DK_F ? 1 : 2;
+            }
+        }
+    }
 
     {
         // host-side launch parameters (device pointers are filled in below)
