@@ -1726,7 +1726,7 @@ __device__ __forceinline__ void decode_frames(const Params &P, const CFG &cfg) {
 }
 
 template <typename T, int W, int PPW, bool CHG>
-__global__ void __launch_bounds__(kMaxThreads, 1) k_decode(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(shape_max_threads(W, PPW), 1) k_decode(const __grid_constant__ Params P) {
     decode_frames<T, W, PPW, RtCfg<CHG>, RtOps>(P, RtCfg<CHG>{&P});
 }
 

@@ -21,6 +21,17 @@ constexpr int kInlineOps = 1536;  // op programs up to this long travel in the k
 #define PB_MAXT 512
 #endif
 constexpr int kMaxThreads = PB_MAXT;
+// Shapes with <= 4 path slots per warp (L <= 4, one warp per frame) are
+// compiled for 1024 threads (64 registers, 32 resident frames per SM): their
+// per-frame state is small and more frames win (same-box A/B: c1 L=4
+// 2.36 -> 2.98, c3 L=2 6.06 -> 8.19 Gbit/s).  At 8 paths per warp it was
+// mixed (c2 +11 %, c3 L=8 -7 %) and those shapes stay at PB_MAXT.
+#ifndef PB_MAXT_SMALL
+#define PB_MAXT_SMALL 1024
+#endif
+__host__ __device__ constexpr int shape_max_threads(int warps, int ppw) {
+    return warps == 1 && ppw <= 4 ? PB_MAXT_SMALL : kMaxThreads;
+}
 
 // Device op kinds.  Combines never appear: each leaf carries its chain of
 // combines.

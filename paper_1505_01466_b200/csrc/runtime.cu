@@ -349,7 +349,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     }
     const int smem_cap = 227 * 1024;
     // resident frames per SM: one warp each, up to the launch bound
-    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", pb::kMaxThreads / 32));
+    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", pb::shape_max_threads(warps, ppw) / 32));
     // Per-frame layout for a channel in shared memory or in global scratch.
     auto plan_layout = [&](bool chg, pb::FrameLayout &lay) {
         lay = pb::FrameLayout{};
@@ -505,7 +505,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     // (A CTA barrier after every op to force lockstep measured slower.)
     {
         const int fpc_env = env_int("PB_FPC", 0);
-        int fpc = std::min(fpc_env > 0 ? fpc_env : h->blocks_per_sm, pb::kMaxThreads / 32 / h->warps);  // launch bound
+        int fpc = std::min(fpc_env > 0 ? fpc_env : h->blocks_per_sm, pb::shape_max_threads(h->warps, h->ppw) / 32 / h->warps);  // launch bound
         while (fpc > 1 && (size_t)fpc * h->smem_frame > (size_t)smem_cap) --fpc;
         int bps = 0;
         while (fpc > 1) {
