@@ -959,10 +959,11 @@ __device__ __forceinline__ void select_phase_c(const Dec<T, W, PPW, CFG> &F, con
         long long kept = lane < L ? srt[0] : LLONG_MAX;
 #pragma unroll
         for (int c = 0; c < NC; ++c) srt[c] = c + 1 < C ? srt[c + 1 < NC ? c + 1 : c] : LLONG_MIN;
+        long long worst;
         for (;;) {
             const long long cand = srt[0];
             const long long best = warp_max_ll(cand);
-            const long long worst = warp_min_ll(kept);
+            worst = warp_min_ll(kept);
             if (best <= worst) break;
             const int from = __ffs(__ballot_sync(FULL_MASK, cand == best)) - 1;
             const int into = __ffs(__ballot_sync(FULL_MASK, kept == worst)) - 1;
@@ -972,7 +973,7 @@ __device__ __forceinline__ void select_phase_c(const Dec<T, W, PPW, CFG> &F, con
             }
             if (lane == into) kept = best;
         }
-        const long long Tk = warp_min_ll(kept);
+        const long long Tk = worst;  // kept is unchanged since the exit test
         F.mark(5);
         // Tk = the L-th best key; keep all better, then the earliest ties
         int gt = 0, eq = 0;
