@@ -16,7 +16,8 @@ from .schedule import (NodeKind, NodeOp, Schedule, ScheduleConfig, build_schedul
 from .channel import (LLR_CLAMP, ChannelConfig, clamp_llr, frame_rng, generate_frames,
                       quantize_int8, transmit)
 from .listdec import (AdaptiveBatchResult, AdaptiveDecoder, BatchResult, DecodeResult,
-                      ListDecoder, PathOutcome, decode, select_candidates)
+                      ListDecoder, PathOutcome, adaptive_decode, decode, schedule_op_rows,
+                      select_candidates)
 from .fastssc import execute_schedule
 from .sim import CSV_FIELDS, DeviceFrames, SimRecord, run_sweep, write_csv
 
@@ -32,7 +33,7 @@ __all__ = [
     "LLR_CLAMP", "ChannelConfig", "clamp_llr", "frame_rng", "generate_frames",
     "quantize_int8", "transmit",
     "AdaptiveBatchResult", "AdaptiveDecoder", "BatchResult", "DecodeResult", "ListDecoder",
-    "PathOutcome", "decode", "execute_schedule",
+    "PathOutcome", "adaptive_decode", "decode", "execute_schedule", "schedule_op_rows",
     "CSV_FIELDS", "DeviceFrames", "SimRecord", "run_sweep", "write_csv",
     "select_candidates", "__version__",
 ]

@@ -110,6 +110,12 @@ struct pb_handle {
     unsigned char *d_out = nullptr;
     size_t d_out_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // last use of the per-handle device scratch (alpha/beta global scratch,
+    // single-path channel scratch, adaptive failure queue): every launch
+    // waits on it and records it, so kernels of one handle never overlap,
+    // whichever streams the calls use (pipelined chunks included)
+    cudaEvent_t ev_busy = nullptr;
+    bool busy_recorded = false;
     // pipelined host-buffer calls: two internal streams + join events
     cudaStream_t aux[2] = {nullptr, nullptr};
     cudaEvent_t evs = nullptr, evj[2] = {nullptr, nullptr};
@@ -706,6 +712,7 @@ int pb_destroy(pb_handle *h) {
         if (h->evj[j]) cudaEventDestroy(h->evj[j]);
     }
     if (h->evs) cudaEventDestroy(h->evs);
+    if (h->ev_busy) cudaEventDestroy(h->ev_busy);
     delete h;
     return PB_OK;
 }
@@ -768,8 +775,30 @@ struct Job {
 //   adaptive              k_ssc (fastssc semantics) settles the frames whose
 //                         CRC passes and queues the rest; k_decode then takes
 //                         the queued frames (count and rows read on the device)
+// Order a launch on `st` after the handle's previous kernels (scratch reuse).
+int scratch_acquire(pb_handle *h, cudaStream_t st) {
+    if (!h->ev_busy) PB_CUDA(cudaEventCreateWithFlags(&h->ev_busy, cudaEventDisableTiming));
+    if (h->busy_recorded) PB_CUDA(cudaStreamWaitEvent(st, h->ev_busy, 0));
+    return PB_OK;
+}
+int scratch_release(pb_handle *h, cudaStream_t st) {
+    PB_CUDA(cudaEventRecord(h->ev_busy, st));
+    h->busy_recorded = true;
+    return PB_OK;
+}
+
+int run_kernels_unordered(pb_handle *h, const pb::Params &base, int in_type, const Job &j, bool adaptive,
+                          cudaStream_t st);
 int run_kernels(pb_handle *h, const pb::Params &base, int in_type, const Job &j, bool adaptive, cudaStream_t st) {
     if (j.batch <= 0) return PB_OK;
+    int rc = scratch_acquire(h, st);
+    if (rc) return rc;
+    rc = run_kernels_unordered(h, base, in_type, j, adaptive, st);
+    if (rc) return rc;
+    return scratch_release(h, st);
+}
+int run_kernels_unordered(pb_handle *h, const pb::Params &base, int in_type, const Job &j, bool adaptive,
+                          cudaStream_t st) {
     const bool use_ssc = adaptive || h->l1_ssc;
     if (use_ssc) {
         if (adaptive) PB_CUDA(cudaMemsetAsync(j.fail_count, 0, sizeof(int32_t), st));
@@ -846,7 +875,7 @@ int decode_pipelined(pb_handle *h, const pb::Params &base, const void *llr, int 
         cudaStream_t sa = h->aux[i & 1];
         const long long nb = std::min<long long>(chunk, batch - f0);
         const size_t io = (size_t)f0 * h->N * in_es, ib = (size_t)nb * h->N * in_es;
-        PB_CUDA(cudaMemcpyAsync(din + io, hin + io, ib, cudaMemcpyHostToDevice, sa));
+        PB_CUDA(cudaMemcpyAsync(din + io, hin + io, ib, cudaMemcpyDefault, sa));
         Job jb{};
         jb.llr = din + io;
         jb.batch = nb;
@@ -859,11 +888,11 @@ int decode_pipelined(pb_handle *h, const pb::Params &base, const void *llr, int 
         jb.fail_count = adaptive ? h->d_fail + batch + 64 + i : nullptr;
         if ((rc = run_kernels(h, base, in_type, jb, adaptive, sa))) return rc;
         if (info_out)
-            PB_CUDA(cudaMemcpyAsync(info_out + (size_t)f0 * h->k, jb.info, (size_t)nb * h->k, cudaMemcpyDeviceToHost, sa));
-        if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok + f0, jb.ok, (size_t)nb, cudaMemcpyDeviceToHost, sa));
-        if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out + f0, jb.pm, (size_t)nb * 8, cudaMemcpyDeviceToHost, sa));
-        if (paths_used) PB_CUDA(cudaMemcpyAsync(paths_used + f0, jb.pu, (size_t)nb * 4, cudaMemcpyDeviceToHost, sa));
-        if (invoked) PB_CUDA(cudaMemcpyAsync(invoked + f0, jb.inv, (size_t)nb, cudaMemcpyDeviceToHost, sa));
+            PB_CUDA(cudaMemcpyAsync(info_out + (size_t)f0 * h->k, jb.info, (size_t)nb * h->k, cudaMemcpyDefault, sa));
+        if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok + f0, jb.ok, (size_t)nb, cudaMemcpyDefault, sa));
+        if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out + f0, jb.pm, (size_t)nb * 8, cudaMemcpyDefault, sa));
+        if (paths_used) PB_CUDA(cudaMemcpyAsync(paths_used + f0, jb.pu, (size_t)nb * 4, cudaMemcpyDefault, sa));
+        if (invoked) PB_CUDA(cudaMemcpyAsync(invoked + f0, jb.inv, (size_t)nb, cudaMemcpyDefault, sa));
     }
     for (int j = 0; j < 2; ++j) {
         PB_CUDA(cudaEventRecord(h->evj[j], h->aux[j]));
@@ -889,13 +918,15 @@ int launch_timed(pb_handle *h, const pb::Params &base, int in_type, const Job &j
 int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
     int grid = (int)std::min<long long>(h->grid, (pr.batch + h->fpc - 1) / h->fpc);
     if (grid < 1) return PB_OK;
+    int rc = scratch_acquire(h, st);
+    if (rc) return rc;
     PB_CUDA(cudaEventRecord(h->ev0, st));
     cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc + h->prog_smem, st);
     if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
     PB_CUDA(cudaEventRecord(h->ev1, st));
     h->timed = true;
     h->launches += 1;
-    return PB_OK;
+    return scratch_release(h, st);
 }
 
 int decode_impl(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8_t *info_out, uint8_t *crc_ok,
@@ -943,7 +974,7 @@ int decode_impl(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8
     if (!dev_in) {
         int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
         if (rc) return rc;
-        PB_CUDA(cudaMemcpyAsync(h->d_in, llr, in_bytes, cudaMemcpyHostToDevice, st));
+        PB_CUDA(cudaMemcpyAsync(h->d_in, llr, in_bytes, cudaMemcpyDefault, st));
         dllr = h->d_in;
     }
     const OutLayout ol(batch, h->k);
@@ -962,11 +993,11 @@ int decode_impl(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8
     jb.fail_count = adaptive ? h->d_fail + batch + 64 : nullptr;
     rc = launch_timed(h, h->base, in_type, jb, adaptive, st);
     if (rc) return rc;
-    if (info_out) PB_CUDA(cudaMemcpyAsync(info_out, jb.info, (size_t)batch * h->k, cudaMemcpyDeviceToHost, st));
-    if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok, jb.ok, (size_t)batch, cudaMemcpyDeviceToHost, st));
-    if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out, jb.pm, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));
-    if (paths_used) PB_CUDA(cudaMemcpyAsync(paths_used, jb.pu, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
-    if (invoked) PB_CUDA(cudaMemcpyAsync(invoked, jb.inv, (size_t)batch, cudaMemcpyDeviceToHost, st));
+    if (info_out) PB_CUDA(cudaMemcpyAsync(info_out, jb.info, (size_t)batch * h->k, cudaMemcpyDefault, st));
+    if (crc_ok) PB_CUDA(cudaMemcpyAsync(crc_ok, jb.ok, (size_t)batch, cudaMemcpyDefault, st));
+    if (pm_out) PB_CUDA(cudaMemcpyAsync(pm_out, jb.pm, (size_t)batch * 8, cudaMemcpyDefault, st));
+    if (paths_used) PB_CUDA(cudaMemcpyAsync(paths_used, jb.pu, (size_t)batch * 4, cudaMemcpyDefault, st));
+    if (invoked) PB_CUDA(cudaMemcpyAsync(invoked, jb.inv, (size_t)batch, cudaMemcpyDefault, st));
     PB_CUDA(cudaStreamSynchronize(st));
     PB_CUDA(cudaGetLastError());
     return PB_OK;
@@ -1113,9 +1144,11 @@ extern "C" int pb_fastssc(pb_handle *h, const void *llr, int in_type, int64_t ba
     sp.fail_count = nullptr;
     sp.cw_out = reinterpret_cast<uint32_t *>(h->d_out);
     const int grid = (int)std::min<long long>(h->ssc_grid, (batch + sp.fpc - 1) / sp.fpc);
+    if ((rc = scratch_acquire(h, st))) return rc;
     cudaError_t e = pb_launch_ssc(&sp, h->mode, grid, st);
     if (e != cudaSuccess) return cuda_fail(e, "single-path kernel launch");
     h->launches += 1;
+    if ((rc = scratch_release(h, st))) return rc;
     std::vector<uint32_t> cw((size_t)batch * nwd);
     PB_CUDA(cudaMemcpyAsync(cw.data(), sp.cw_out, n_cw, cudaMemcpyDeviceToHost, st));
     PB_CUDA(cudaMemcpyAsync(pm_out, sp.pm_out, (size_t)batch * 8, cudaMemcpyDeviceToHost, st));

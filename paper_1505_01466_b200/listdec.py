@@ -22,7 +22,29 @@ from .encode import extract_payload, polar_encode
 from .schedule import Schedule
 
 __all__ = ["DecodeResult", "PathOutcome", "BatchResult", "AdaptiveBatchResult",
-           "select_candidates", "ListDecoder", "AdaptiveDecoder", "decode"]
+           "select_candidates", "ListDecoder", "AdaptiveDecoder", "decode",
+           "adaptive_decode", "schedule_op_rows"]
+
+# NodeKind values of the reference (schedule.py:29-41) -> pb_op kind codes
+_KIND_BY_VALUE = {"F": 0, "G": 1, "Combine": 2, "Rate0": 3, "Rate1": 4, "Rep": 5, "SPC": 6}
+
+
+def schedule_op_rows(schedule) -> np.ndarray:
+    """The schedule's ops as the C ABI's ``pb_op`` rows (kind, size, stage,
+    side, spc_truncated), read by duck typing from any object shaped like the
+    reference's ``Schedule`` (``schedule.py:119-125``): ``schedule.ops`` is a
+    sequence of ``NodeOp`` (``schedule.py:44-58``) whose ``kind`` is a
+    ``NodeKind`` enum member (or its string value).  Works for this package's
+    mirror and for ``polaris.schedule.Schedule`` objects alike."""
+    ops = list(schedule.ops)
+    rows = np.zeros((len(ops), 5), dtype=np.int32)
+    for i, op in enumerate(ops):
+        kind = getattr(op.kind, "value", op.kind)
+        if kind not in _KIND_BY_VALUE:
+            raise ValueError(f"op {i}: unsupported node kind {kind!r}")
+        rows[i] = (_KIND_BY_VALUE[kind], int(op.size), int(op.stage), int(op.side),
+                   int(bool(op.spc_truncated)))
+    return rows
 
 
 @dataclass(eq=False)
@@ -90,6 +112,45 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
+# output buffers: (field, accepted numpy dtypes, accepted torch dtype names, rows per frame)
+_OUT_SPECS = {
+    "info_bits": ((np.uint8, np.bool_), ("uint8", "bool"), "k"),
+    "crc_ok": ((np.uint8, np.bool_), ("uint8", "bool"), 1),
+    "chosen_pm": ((np.float64,), ("float64",), 1),
+    "paths_used": ((np.int32,), ("int32",), 1),
+    "invoked_list": ((np.uint8, np.bool_), ("uint8", "bool"), 1),
+}
+
+
+def _check_out(name, a, batch: int, k: int, cuda_device=None) -> None:
+    """Reject an output buffer the kernel or the copies could overrun or
+    misread: wrong dtype, too small, non-contiguous, or on the wrong side
+    (``cuda_device`` None = host memory, else that CUDA ordinal)."""
+    if a is None:
+        return
+    np_dtypes, torch_dtypes, per = _OUT_SPECS[name]
+    need = batch * (k if per == "k" else per)
+    if _is_torch(a):
+        dt = str(a.dtype).replace("torch.", "")
+        numel, contig = a.numel(), a.is_contiguous()
+        dev = a.device.index if a.is_cuda else None
+        if a.is_cuda and dev is None:
+            dev = 0
+    else:
+        dt, numel, contig, dev = a.dtype, a.size, a.flags.c_contiguous, None
+        if a.dtype.type not in np_dtypes:
+            raise ValueError(f"{name}: dtype {a.dtype} not one of {[d.__name__ for d in np_dtypes]}")
+    if _is_torch(a) and dt not in torch_dtypes:
+        raise ValueError(f"{name}: dtype {dt} not one of {list(torch_dtypes)}")
+    if not contig:
+        raise ValueError(f"{name}: output buffer must be contiguous")
+    if numel < need:
+        raise ValueError(f"{name}: output buffer holds {numel} elements, the batch needs {need}")
+    if dev != cuda_device:
+        where = "host memory" if cuda_device is None else f"cuda:{cuda_device}"
+        raise ValueError(f"{name}: output buffer must be in {where}")
+
+
 def _addr(a):
     """Raw address of a numpy array or torch tensor (None passes through)."""
     if a is None:
@@ -137,7 +198,7 @@ class ListDecoder:
             0 if crc is None else crc.width, 0 if crc is None else crc.polynomial,
             0 if crc is None else crc.init, 0 if crc is None else int(crc.reflect),
             0 if crc is None else crc.xor_out)
-        arr = schedule.op_array()
+        arr = schedule_op_rows(schedule)
         ops = (_native.PbOp * max(1, len(arr)))()
         for i, row in enumerate(arr.tolist()):
             ops[i] = _native.PbOp(*row)
@@ -221,6 +282,8 @@ class ListDecoder:
         if out is None:
             out = BatchResult(np.empty((B, k), np.uint8), np.empty(B, np.bool_),
                               np.empty(B, np.float64), np.empty(B, np.int32))
+        for name in ("info_bits", "crc_ok", "chosen_pm", "paths_used"):
+            _check_out(name, getattr(out, name), B, k)
         rc = _native.lib().pb_decode(self._h, ctypes.c_void_p(ptr), in_type, B,
                                      _addr(out.info_bits), _addr(out.crc_ok),
                                      _addr(out.chosen_pm), _addr(out.paths_used),
@@ -247,6 +310,12 @@ class ListDecoder:
             in_type = _native.PB_IN_F32
         else:
             raise ValueError(f"unsupported LLR dtype {llrs.dtype}")
+        if (llrs.device.index or 0) != self.device:
+            raise ValueError(f"LLRs on {llrs.device}, decoder on cuda:{self.device}")
+        B, k = llrs.shape[0], self.spec.k
+        for name, t in (("info_bits", info_out), ("crc_ok", crc_ok), ("chosen_pm", pm_out),
+                        ("paths_used", paths_used)):
+            _check_out(name, t, B, k, cuda_device=self.device)
         if stream is None:
             stream = torch.cuda.current_stream(llrs.device).cuda_stream
 
@@ -335,6 +404,8 @@ class AdaptiveDecoder:
             out = AdaptiveBatchResult(np.empty((B, k), np.uint8), np.empty(B, np.bool_),
                                       np.empty(B, np.float64), np.empty(B, np.int32),
                                       np.empty(B, np.bool_))
+        for name in ("info_bits", "crc_ok", "chosen_pm", "paths_used", "invoked_list"):
+            _check_out(name, getattr(out, name), B, k)
         rc = _native.lib().pb_decode_adaptive(
             self._list._h, ctypes.c_void_p(ptr), in_type, B, _addr(out.info_bits),
             _addr(out.crc_ok), _addr(out.chosen_pm), _addr(out.paths_used),
@@ -354,6 +425,12 @@ class AdaptiveDecoder:
         in_type = _native.PB_IN_I8 if llrs.dtype == torch.int8 else _native.PB_IN_F32
         if llrs.dtype not in (torch.int8, torch.float32):
             raise ValueError(f"unsupported LLR dtype {llrs.dtype}")
+        if llrs.dtype == torch.int8 and self._list.mode != "int8":
+            raise ValueError("int8 LLRs need a decoder built with mode='int8'")
+        B, k = llrs.shape[0], self.spec.k
+        for name, t in (("info_bits", info_out), ("crc_ok", crc_ok), ("chosen_pm", pm_out),
+                        ("paths_used", paths_used), ("invoked_list", invoked_list)):
+            _check_out(name, t, B, k, cuda_device=self._list.device)
         if stream is None:
             stream = torch.cuda.current_stream(llrs.device).cuda_stream
 
@@ -379,3 +456,8 @@ class AdaptiveDecoder:
 def decode(llr, schedule: Schedule, list_size: int) -> DecodeResult:
     """One-shot list decode of a single frame (reference ``listdec.py:462-468``)."""
     return ListDecoder(schedule, list_size).decode(llr)
+
+
+def adaptive_decode(llr, schedule: Schedule, list_size: int) -> DecodeResult:
+    """One-shot adaptive decode of a single frame (reference ``listdec.py:471-473``)."""
+    return AdaptiveDecoder(schedule, list_size).decode(llr)

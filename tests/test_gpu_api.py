@@ -155,3 +155,80 @@ def test_chunked_host_pipeline_matches_device_call(c1, monkeypatch, pinned):
     for a, b in zip((got.info_bits, got.crc_ok, got.chosen_pm, got.paths_used),
                     (ref.info_bits, ref.crc_ok, ref.chosen_pm, ref.paths_used)):
         assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+def test_pinned_pipeline_with_global_scratch_matches_device_call(monkeypatch):
+    """pinned host buffers in AND out, several chunks, a
+    config whose frames use global scratch (c3 L=32): the chunks' kernels
+    must not share the handle's scratch concurrently."""
+    import torch
+    spec = pb.CodeSpec.from_design_ebn0(2048, 1691, pb.CRC32, 4.0)
+    sch = pb.build_schedule(spec)
+    fb = pb.generate_frames(spec, 3.5, seed=21, start=0, count=3000, workers=4)
+    dec = pb.ListDecoder(sch, 32)
+    assert __import__("json").loads(dec.plan)["global_scratch_per_frame"] > 0
+    x = torch.from_numpy(fb.llrs).cuda()
+    B, k = x.shape[0], spec.k
+    dinfo = torch.empty((B, k), dtype=torch.uint8, device="cuda")
+    dok = torch.empty(B, dtype=torch.uint8, device="cuda")
+    dpm = torch.empty(B, dtype=torch.float64, device="cuda")
+    dpu = torch.empty(B, dtype=torch.int32, device="cuda")
+    dec.decode_device(x, dinfo, dok, dpm, dpu)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("PB_CHUNK_FRAMES", "700")   # 5 chunks, ragged tail
+    llr_h = torch.from_numpy(fb.llrs).pin_memory()
+    out = pb.BatchResult(torch.empty((B, k), dtype=torch.uint8).pin_memory(),
+                         torch.empty(B, dtype=torch.uint8).pin_memory(),
+                         torch.empty(B, dtype=torch.float64).pin_memory(),
+                         torch.empty(B, dtype=torch.int32).pin_memory())
+    for _ in range(2):
+        got = dec.decode_batch(llr_h, out=out)
+        assert torch.equal(got.info_bits, dinfo.cpu()) and torch.equal(got.crc_ok, dok.cpu())
+        assert torch.equal(got.chosen_pm, dpm.cpu()) and torch.equal(got.paths_used, dpu.cpu())
+
+
+def test_handle_shared_across_streams_is_ordered():
+    """a device call on a side stream followed by a host
+    call on the legacy stream, same handle, without a user sync."""
+    import torch
+    spec = pb.CodeSpec.from_design_ebn0(2048, 1691, pb.CRC32, 4.0)
+    sch = pb.build_schedule(spec)
+    fb = pb.generate_frames(spec, 3.5, seed=22, start=0, count=2000, workers=4)
+    dec = pb.ListDecoder(sch, 32)
+    ref = dec.decode_batch(fb.llrs[1000:])
+    x = torch.from_numpy(fb.llrs[:1000]).cuda()
+    info = torch.empty((1000, spec.k), dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        dec.decode_device(x, info)
+    got = dec.decode_batch(fb.llrs[1000:])
+    torch.cuda.synchronize()
+    assert np.array_equal(got.info_bits, ref.info_bits)
+    assert np.array_equal(got.chosen_pm, ref.chosen_pm)
+    assert np.array_equal(info.cpu().numpy(), dec.decode_batch(fb.llrs[:1000]).info_bits)
+
+
+def test_output_buffers_are_validated(c1):
+    import torch
+    spec, sch, fb = c1
+    dec = pb.ListDecoder(sch, 4)
+    B, k = 10, spec.k
+    good = lambda: pb.BatchResult(np.empty((B, k), np.uint8), np.empty(B, np.bool_),
+                                  np.empty(B, np.float64), np.empty(B, np.int32))
+    bad = good(); bad.chosen_pm = np.empty(B, np.float32)
+    with pytest.raises(ValueError, match="chosen_pm"):
+        dec.decode_batch(fb.llrs[:B], out=bad)
+    bad = good(); bad.info_bits = np.empty((B - 1, k), np.uint8)
+    with pytest.raises(ValueError, match="info_bits"):
+        dec.decode_batch(fb.llrs[:B], out=bad)
+    bad = good(); bad.paths_used = np.empty((B, 2), np.int32)[:, 0]
+    with pytest.raises(ValueError, match="contiguous"):
+        dec.decode_batch(fb.llrs[:B], out=bad)
+    bad = good(); bad.crc_ok = torch.empty(B, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError, match="host memory"):
+        dec.decode_batch(fb.llrs[:B], out=bad)
+    x = torch.from_numpy(fb.llrs[:B]).cuda()
+    with pytest.raises(ValueError, match="cuda:0"):
+        dec.decode_device(x, torch.empty((B, k), dtype=torch.uint8))
+    with pytest.raises(ValueError, match="paths_used"):
+        dec.decode_device(x, paths_used=torch.empty(B, dtype=torch.int64, device="cuda"))
