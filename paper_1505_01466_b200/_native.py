@@ -105,10 +105,13 @@ def build(verbose: bool = False, jobs: int | None = None, profile: bool = False)
         if _stale(obj, [inst, *hdrs]):
             cmds.append(["nvcc", *NVCC_FLAGS, *extra, "-I", INCLUDE, f"-DPB_T={t}", f"-DPB_W={w}",
                          f"-DPB_PPW={ppw}", f"-DPB_CHG={chg}", f"-DPB_TAG={tag}", "-c", inst, "-o", obj])
-    for src in ("dispatch.cu", "runtime.cu", "ssc_kernel.cu", "frame_gen.cu"):
+    for src in ("dispatch.cu", "runtime.cu", "ssc_kernel.cu", "frame_gen.cu", "lane_inst.cu"):
         obj = os.path.join(BUILD_DIR, src.replace(".cu", ".o"))
         objs.append(obj)
-        if _stale(obj, [os.path.join(CSRC, src), *hdrs]) or (only and src == "dispatch.cu"):
+        deps = [os.path.join(CSRC, src), *hdrs]
+        if src == "lane_inst.cu":
+            deps.append(os.path.join(CSRC, "lane_kernel.cuh"))
+        if _stale(obj, deps) or (only and src == "dispatch.cu"):
             cmds.append(["nvcc", *NVCC_FLAGS, "-I", INCLUDE, *(dispatch_defs if src == "dispatch.cu" else []),
                          "-c", os.path.join(CSRC, src), "-o", obj])
     jobs = jobs or max(1, min(len(cmds), os.cpu_count() or 1))

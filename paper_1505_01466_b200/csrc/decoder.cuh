@@ -126,6 +126,72 @@ struct Params {
 };
 
 // ---------------------------------------------------------------------
+// Lane-per-path list kernel (lane_kernel.cuh): one warp per frame, lane q =
+// path slot q (L <= 32), per-path state (metric, row indices, leaf data) in
+// registers, the channel in shared memory, the top two stages (n-1, n-2)
+// recomputed from it instead of stored.
+namespace lk {
+constexpr int kMaxOps = 2048;  // the op program travels in the kernel parameters (16 KB)
+enum : uint8_t { K_F = 0, K_G = 1, K_R0 = 2, K_REP = 3, K_R1 = 4, K_SPC = 5, K_NOP = 6 };
+// where an op's input stage lives: a stored row in shared memory / global
+// scratch, recomputed stage n-1 (f / g of the channel halves), recomputed
+// stage n-2, or the channel itself (a root leaf)
+enum : uint8_t { S_SM = 0, S_GL = 1, S_V1 = 2, S_V2 = 3, S_CH = 4 };
+enum : uint8_t { LF_SELECT = 1, LF_V1G = 2, LF_V2G = 4 };
+
+struct __align__(8) LOp {
+    uint8_t kind;    // K_*
+    uint8_t stage;   // F / G: stage read (writes stage - 1); leaf: its stage t
+    uint8_t pin;     // active paths before the op
+    uint8_t pout;    // active paths after (leaf)
+    uint8_t ncand;   // leaf: candidates per path (2 / 4 / 8; 0 for Rate-0)
+    uint8_t src;     // S_*: where the input stage lives
+    uint8_t aux;     // F / G: S_SM / S_GL of the output stage; leaf: chain target slot (n = root)
+    uint8_t flags;   // LF_*: selection needed; recomputed stages' F / G modes
+};
+static_assert(sizeof(LOp) == 8, "LOp is one 8-byte load");
+
+struct LLayout {
+    int ch_off;               // channel, N elements of T (shared memory)
+    int a_off[kMaxLog];       // stored alpha stage s: quad-interleaved rows, 32 rows
+    uint32_t a_gl;            // bit s: stage s in global scratch
+    int b_off[kMaxLog];       // beta slot s: 32 rows of b_stride[s] words
+    int b_stride[kMaxLog];
+    uint32_t b_gl;            // bit s: slot s in global scratch
+    int asg_off;              // uint8 [32] survivor -> (source << 3 | cand)
+    int met_off;              // double [32] survivor metrics
+    int root_off;             // uint32 [max(1, N/32)] codeword scratch (finalise)
+    int smem_bytes;           // per frame (16-byte multiple)
+    int gbytes;               // per frame global scratch (256-byte multiple)
+};
+
+struct LParams {
+    const uint32_t *xsyn4;
+    const uint32_t *info_pos;
+    int N, n, k, L, has_crc;
+    uint32_t crc_const;
+    int n_ops, final_op;
+    const void *llr;
+    int in_type;
+    long long batch;
+    uint8_t *info_out;
+    uint8_t *crc_ok;
+    double *pm_out;
+    int32_t *paths_used;
+    uint32_t *path_cw;
+    double *path_pm;
+    uint8_t *path_crc;
+    unsigned char *gscratch;
+    const int32_t *frame_map;
+    const int32_t *batch_dev;
+    int fpc;
+    int sync_mask;
+    LLayout lay;
+    LOp prog[kMaxOps];
+};
+}  // namespace lk
+
+// ---------------------------------------------------------------------
 // Single-path (L = 1) pass: polaris.fastssc.execute_schedule
 // (fastssc.py:20-83) and the first stage of AdaptiveDecoder
 // (listdec.py:437-459).  One warp per frame, lanes over elements; the frame

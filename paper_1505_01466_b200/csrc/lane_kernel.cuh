@@ -1,0 +1,999 @@
+// lane_kernel.cuh -- lane-per-path Fast-SSC list-CRC decode kernel (sm_100a).
+//
+// One warp decodes one frame; lane q owns path slot q (L <= 32).  Compared
+// with the interpreted multi-shape kernel (decode_kernel.cuh) this one is
+// built for the L > 16 north-star shape around three choices:
+//   * per-path state in registers: metric (f64), the row index of every
+//     alpha stage / beta slot (8-bit fields), the leaf data a survivor needs
+//     from its source (hard word, least reliable positions, parity) --
+//     survivors gather it from the source lane with shuffles
+//     (listdec.py:397-434 lazy copy == inheriting the source's row indices);
+//   * the channel in shared memory and the two top stages n-1, n-2 never
+//     stored: every read recomputes them from the channel (all lanes read
+//     the same channel quad, a broadcast) and the path's beta bits, which
+//     halves the per-frame global scratch (c3 L=32: 144 KB -> 70 KB) so the
+//     resident frames' scratch about fits the L2;
+//   * survivor selection on the high 32 bits of the order-preserving metric
+//     keys (one REDUX per max / min), with an exact 64-bit resolution of the
+//     candidates tied at the threshold (listdec.py:63-100 exactly).
+// Code size is kept small (one code path per op kind and source placement)
+// so the SM's warps hit in the instruction cache.
+#pragma once
+#include "decode_kernel.cuh"
+
+namespace pb {
+namespace lk {
+
+__device__ __forceinline__ int get8(const uint32_t (&w)[4], int s) {
+    const int j = s >> 2;
+    const uint32_t x = j == 0 ? w[0] : (j == 1 ? w[1] : (j == 2 ? w[2] : w[3]));
+    return (x >> ((s & 3) * 8)) & 0xff;
+}
+__device__ __forceinline__ void set8(uint32_t (&w)[4], int s, int v) {
+    const int sh = (s & 3) * 8, j = s >> 2;
+    const uint32_t m = ~(0xffu << sh), vv = (uint32_t)v << sh;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (j == i) w[i] = (w[i] & m) | vv;
+}
+
+// the inverse of okey (an involution on the bit pattern)
+__device__ __forceinline__ double unkey(long long k) {
+    return __longlong_as_double(k ^ ((k >> 63) & 0x7fffffffffffffffLL));
+}
+
+// per-frame warp state
+template <typename T>
+struct Fr {
+    const LParams &P;
+    unsigned char *sm;   // frame's shared-memory block
+    unsigned char *gs;   // frame's global scratch block
+    int lane;
+    double pm;           // path metric (listdec.py:146-153)
+    uint32_t ia[4];      // alpha row of stage s: byte s
+    uint32_t ib[4];      // beta row of slot s: byte s
+    // leaf data of the path's last forking leaf decision (kept for the
+    // final pick: the root codeword is built from it on demand)
+    uint32_t hard;       // hard decisions (leaf size <= 32)
+    uint32_t lrb01;      // least reliable positions 0, 1 (16 bits each)
+    uint32_t lrb23;      // positions 2, 3
+    uint32_t lflag;      // Rep: ones first; SPC: odd parity
+    uint32_t dec;        // candidate chosen (0 .. 7)
+
+    __device__ __forceinline__ Fr(const LParams &p, unsigned char *s, unsigned char *g)
+        : P(p), sm(s), gs(g), lane(threadIdx.x & 31), pm(0.0), hard(0), lrb01(0), lrb23(0), lflag(0), dec(0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ia[i] = ib[i] = 0u;
+    }
+    __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(sm + P.lay.ch_off); }
+    __device__ __forceinline__ uint32_t *beta_row(int s, int row) const {
+        unsigned char *base = ((P.lay.b_gl >> s) & 1u) ? gs : sm;
+        return reinterpret_cast<uint32_t *>(base + P.lay.b_off[s]) + row * P.lay.b_stride[s];
+    }
+    // stored alpha row r of stage s: quad x at element x * 128 (32 rows x 4)
+    __device__ __forceinline__ T *a_row(int s, int r) const {
+        unsigned char *base = ((P.lay.a_gl >> s) & 1u) ? gs : sm;
+        return reinterpret_cast<T *>(base + P.lay.a_off[s]) + r * 4;
+    }
+    template <int WHERE>
+    __device__ __forceinline__ T *a_row_t(int s, int r) const {
+        return reinterpret_cast<T *>((WHERE == S_GL ? gs : sm) + P.lay.a_off[s]) + r * 4;
+    }
+};
+
+// ------------------------------------------------------------ sources
+// A path's view of one alpha stage: quad(x) = elements 4x .. 4x+3, get(i).
+
+template <typename T>
+struct RowLd {  // a stored row (quad stride 128: 32 interleaved rows) or the channel (4)
+    const T *p;
+    int qs;
+    __device__ __forceinline__ void quad(int x, float (&v)[4]) const { V4<T>::ld(p + x * qs, v); }
+    __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(p + (i >> 2) * qs + (i & 3)); }
+};
+// stage n-1: f or g of the channel halves (g with the path's left-half bits,
+// beta slot n-1)
+template <typename T>
+struct V1Ld {
+    const T *ch;
+    const uint32_t *b1;
+    int half;  // N / 2
+    bool g;
+    __device__ __forceinline__ void quad(int x, float (&v)[4]) const {
+        float a[4], b[4];
+        V4<T>::ld(ch + 4 * x, a);
+        V4<T>::ld(ch + 4 * x + half, b);
+        if (g) {
+            const unsigned bits = b1[x >> 3] >> ((x & 7) * 4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(a[j], b[j], bits, j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = f_op(a[j], b[j]);
+        }
+    }
+    __device__ __forceinline__ float get(int i) const {
+        const float a = Elem<T>::ld(ch + i), b = Elem<T>::ld(ch + i + half);
+        return g ? g_op<T>(a, b, (b1[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+    }
+};
+// stage n-2: f or g of two stage n-1 values (beta slot n-2), each f or g of
+// two channel values -- four channel loads per element, all lanes reading
+// the same address
+template <typename T>
+struct V2Ld {
+    const T *ch;
+    const uint32_t *b1, *b2;
+    int q;  // N / 4
+    bool g1, g2;
+    __device__ __forceinline__ void quad(int x, float (&v)[4]) const {
+        float c0[4], c1[4], c2[4], c3[4];
+        V4<T>::ld(ch + 4 * x, c0);
+        V4<T>::ld(ch + 4 * x + q, c1);
+        V4<T>::ld(ch + 4 * x + 2 * q, c2);
+        V4<T>::ld(ch + 4 * x + 3 * q, c3);
+        float u0[4], u1[4];
+        if (g1) {
+            const unsigned bl = b1[x >> 3] >> ((x & 7) * 4);
+            const int xh = x + (q >> 2);
+            const unsigned bh = b1[xh >> 3] >> ((xh & 7) * 4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                u0[j] = g_op_bits<T>(c0[j], c2[j], bl, j);
+                u1[j] = g_op_bits<T>(c1[j], c3[j], bh, j);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                u0[j] = f_op(c0[j], c2[j]);
+                u1[j] = f_op(c1[j], c3[j]);
+            }
+        }
+        if (g2) {
+            const unsigned b = b2[x >> 3] >> ((x & 7) * 4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(u0[j], u1[j], b, j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = f_op(u0[j], u1[j]);
+        }
+    }
+    __device__ __forceinline__ float v1(int i) const {
+        const float a = Elem<T>::ld(ch + i), b = Elem<T>::ld(ch + i + 2 * q);
+        return g1 ? g_op<T>(a, b, (b1[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+    }
+    __device__ __forceinline__ float get(int i) const {
+        const float a = v1(i), b = v1(i + q);
+        return g2 ? g_op<T>(a, b, (b2[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+    }
+};
+template <typename T>
+__device__ __forceinline__ V1Ld<T> make_v1(const Fr<T> &F, const LOp &o) {
+    const int n = F.P.n;
+    return V1Ld<T>{F.channel(), F.beta_row(n - 1, get8(F.ib, n - 1)), F.P.N >> 1, (o.flags & LF_V1G) != 0};
+}
+template <typename T>
+__device__ __forceinline__ V2Ld<T> make_v2(const Fr<T> &F, const LOp &o) {
+    const int n = F.P.n;
+    return V2Ld<T>{F.channel(), F.beta_row(n - 1, get8(F.ib, n - 1)), F.beta_row(n - 2, get8(F.ib, n - 2)),
+                   F.P.N >> 2, (o.flags & LF_V1G) != 0, (o.flags & LF_V2G) != 0};
+}
+// a leaf's LLRs: its stage's stored row (stages n-1 / n-2 are stored for
+// leaves: the F / G before such a leaf writes them, runtime.cu) or the channel
+template <typename T>
+__device__ __forceinline__ RowLd<T> leaf_src(const Fr<T> &F, const LOp &o, int t, const uint32_t (&ia)[4]) {
+    return o.src == S_CH ? RowLd<T>{F.channel(), 4} : RowLd<T>{F.a_row(t, get8(ia, t)), 128};
+}
+
+// ---------------------------------------------------------------- F / G
+
+template <typename T, bool IS_G, int U, class S>
+__device__ __forceinline__ void fg_body(const S &src, T *dst, const uint32_t *bw, int h) {
+    if (h < 4) {  // stage 1 / 2: one (padded) quad
+        float o4[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int i = 0; i < h; ++i) {
+            const float a = src.get(i), b = src.get(i + h);
+            o4[i] = IS_G ? g_op<T>(a, b, (bw[0] >> i) & 1u) : f_op(a, b);
+        }
+        V4<T>::st(dst, o4);
+        return;
+    }
+    const int nq = h >> 2;
+    int x0 = 0;
+    for (; x0 + U <= nq; x0 += U) {
+        float a[U][4], b[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            src.quad(x0 + u, a[u]);
+            src.quad(x0 + u + nq, b[u]);
+        }
+        unsigned wd = 0u;
+        if (IS_G) wd = bw[x0 >> 3];  // U <= 8 quads of one 32-bit word (x0 multiple of U)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float o[4];
+            const unsigned bits = IS_G ? wd >> (((x0 + u) & 7) * 4) : 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op_bits<T>(a[u][j], b[u][j], bits, j) : f_op(a[u][j], b[u][j]);
+            V4<T>::st(dst + (x0 + u) * 128, o);
+        }
+    }
+    for (; x0 < nq; ++x0) {
+        float a[4], b[4], o[4];
+        src.quad(x0, a);
+        src.quad(x0 + nq, b);
+        const unsigned bits = IS_G ? bw[x0 >> 3] >> ((x0 & 7) * 4) : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op_bits<T>(a[j], b[j], bits, j) : f_op(a[j], b[j]);
+        V4<T>::st(dst + x0 * 128, o);
+    }
+}
+
+// F / G of stage s into the path's own row of stage s-1 (listdec.py:317-326)
+template <typename T, bool IS_G, int SRC, int DST>
+__device__ __forceinline__ void fg_op(Fr<T> &F, const LOp &o) {
+    const int s = o.stage, h = 1 << (s - 1);
+    if (F.lane < o.pin) {
+        T *dst = F.template a_row_t<DST>(s - 1, F.lane);
+        const uint32_t *bw = IS_G ? F.beta_row(s - 1, get8(F.ib, s - 1)) : nullptr;
+        if (SRC == S_V2) {
+            fg_body<T, IS_G, 2>(make_v2(F, o), dst, bw, h);
+        } else if (SRC == S_V1) {
+            fg_body<T, IS_G, 4>(make_v1(F, o), dst, bw, h);
+        } else if (SRC == S_CH) {
+            fg_body<T, IS_G, 4>(RowLd<T>{F.channel(), 4}, dst, bw, h);
+        } else {
+            const RowLd<T> src{F.template a_row_t<SRC>(s, get8(F.ia, s)), 128};
+            fg_body<T, IS_G, SRC == S_GL ? 8 : 4>(src, dst, bw, h);
+        }
+    }
+    set8(F.ia, s - 1, F.lane);
+}
+
+// ------------------------------------------------------------- leaves
+
+// numpy float32 pairwise sums (listdec.py:341,348-350): n < 8 sequential;
+// 8 <= n <= 128 eight strided accumulators combined ((0+1)+(2+3))+((4+5)+(6+7));
+// larger n halves recursively (a balanced tree of 128-element blocks).
+// NS = 1: sum min(a,0); NS = 3: (sum min(a,0), sum max(a,0), sum a).
+template <int NS, class S>
+__device__ __forceinline__ void pw_sums_lane(const S &src, int m, float (&out)[NS]) {
+    if (m < 8) {
+        float r[NS];
+#pragma unroll
+        for (int t = 0; t < NS; ++t) r[t] = 0.f;
+        if (m >= 4) {
+            float q[4];
+            src.quad(0, q);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc_add<NS>(r, q[j]);
+        } else {
+            for (int i = 0; i < m; ++i) acc_add<NS>(r, src.get(i));
+        }
+#pragma unroll
+        for (int t = 0; t < NS; ++t) out[t] = r[t];
+        return;
+    }
+    const int blk = m < 128 ? m : 128, nb = m / blk, per = blk >> 3;
+    float stk[10][NS];
+    float carry[NS];
+    for (int b = 0; b < nb; ++b) {
+        float acc[8][NS];
+        const int xb = (b * blk) >> 2;
+        {
+            float q0[4], q1[4];
+            src.quad(xb, q0);
+            src.quad(xb + 1, q1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                acc_init<NS>(acc[j], q0[j]);
+                acc_init<NS>(acc[j + 4], q1[j]);
+            }
+        }
+        for (int r = 1; r < per; ++r) {
+            float q0[4], q1[4];
+            src.quad(xb + 2 * r, q0);
+            src.quad(xb + 2 * r + 1, q1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                acc_add<NS>(acc[j], q0[j]);
+                acc_add<NS>(acc[j + 4], q1[j]);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+            const float s01 = __fadd_rn(acc[0][t], acc[1][t]), s23 = __fadd_rn(acc[2][t], acc[3][t]);
+            const float s45 = __fadd_rn(acc[4][t], acc[5][t]), s67 = __fadd_rn(acc[6][t], acc[7][t]);
+            acc[0][t] = __fadd_rn(__fadd_rn(s01, s23), __fadd_rn(s45, s67));
+        }
+        // combine block sums in numpy's halving order (binary counter)
+#pragma unroll
+        for (int t = 0; t < NS; ++t) carry[t] = acc[0][t];
+        int lvl = 0;
+        while ((b >> lvl) & 1) {
+#pragma unroll
+            for (int t = 0; t < NS; ++t) carry[t] = __fadd_rn(stk[lvl][t], carry[t]);
+            ++lvl;
+        }
+#pragma unroll
+        for (int t = 0; t < NS; ++t) stk[lvl][t] = carry[t];
+    }
+#pragma unroll
+    for (int t = 0; t < NS; ++t) out[t] = carry[t];
+}
+
+// Rate-1 / SPC scan: stable K least reliable positions (argsort kind="stable",
+// listdec.py:362,375), hard-decision word(s), parity.  Returns the parity;
+// `hard` = the hard word when m <= 32.
+template <int K, class S>
+__device__ __forceinline__ int leaf_scan_lane(const S &src, int m, TopK<K> &tk, uint32_t &hard) {
+    tk.init();
+    int par = 0;
+    hard = 0u;
+    if (m >= 32) {
+        constexpr int NCH = K == 2 ? 4 : 2;
+        TopK<K> tc[NCH];
+#pragma unroll
+        for (int h = 0; h < NCH; ++h) tc[h].init();
+        for (int w0 = 0; w0 < m; w0 += 32) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float q[4];
+                src.quad((w0 >> 2) + j, q);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[4 * j + e] = q[e];
+            }
+            uint32_t word = 0u;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                word |= (v[j] < 0.f ? 1u : 0u) << j;
+                tc[j % NCH].push_scan(fabsf(v[j]), w0 + j);
+            }
+            hard = word;
+            par ^= __popc(word);
+        }
+        tk = tc[0];
+#pragma unroll
+        for (int h = 1; h < NCH; ++h)
+#pragma unroll
+            for (int e = 0; e < K; ++e) tk.insert(tc[h].m[e], tc[h].i[e]);
+    } else if (m >= 4) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (4 * j < m) {
+                float q[4];
+                src.quad(j, q);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[4 * j + e] = q[e];
+            }
+        if (m <= 16) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < m) {
+                    hard |= (v[j] < 0.f ? 1u : 0u) << j;
+                    tk.push_scan(fabsf(v[j]), j);
+                }
+        }
+        par = __popc(hard);
+    } else {
+        for (int j = 0; j < m; ++j) {
+            const float a = src.get(j);
+            hard |= (a < 0.f ? 1u : 0u) << j;
+            tk.push_scan(fabsf(a), j);
+        }
+        par = __popc(hard);
+    }
+    return par;
+}
+
+// SPC flip sets relative to the ML word over the four LRB slots, emission
+// order of listdec.py:157 (_SPC_PAIRS)
+__device__ __forceinline__ int lk_flip_mask(int kind, int c, int odd) {
+    if (kind == K_R1) return c;  // (), (b1), (b2), (b1, b2)
+    const int ml = odd ? 1 : 0;
+    return c == 0 ? ml : (kSpcPairs[c - 1] ^ ml);
+}
+
+// Phase A of a leaf for this lane's path: Rate-0 adds to the metric;
+// forking leaves produce candidate keys okey(pm + delta) in candidate order
+// and the leaf data the survivors will need.  Returns false for Rate-0.
+template <typename T>
+__device__ __forceinline__ void leaf_phase_a(Fr<T> &F, const LOp &o, int kind, long long (&key)[8]) {
+    const int t = o.stage, m = 1 << t;
+    const RowLd<T> src = leaf_src(F, o, t, F.ia);
+    if (kind == K_R0) {  // listdec.py:340-346
+        float r[1];
+        pw_sums_lane<1>(src, m, r);
+        F.pm += (double)r[0];
+        return;
+    }
+    double cd[8];
+    if (kind == K_REP) {  // listdec.py:347-359
+        float r[3];
+        pw_sums_lane<3>(src, m, r);
+        const bool ones_first = r[2] < 0.f;
+        const double neg = (double)r[0], pos = (double)r[1];
+        cd[0] = ones_first ? -pos : neg;
+        cd[1] = ones_first ? neg : -pos;
+        F.lflag = ones_first;
+#pragma unroll
+        for (int c = 2; c < 8; ++c) cd[c] = 0.0;
+    } else if (kind == K_R1) {  // listdec.py:360-372
+        TopK<2> tk;
+        uint32_t hard;
+        leaf_scan_lane<2>(src, m, tk, hard);
+        F.hard = hard;
+        F.lrb01 = (uint32_t)tk.i[0] | ((uint32_t)tk.i[1] << 16);
+        F.lrb23 = 0u;
+        F.lflag = 0u;
+        const double w1 = (double)tk.m[0], w2 = (double)tk.m[1];
+        cd[0] = 0.0;
+        cd[1] = -w1;
+        cd[2] = -w2;
+        cd[3] = -(w1 + w2);
+#pragma unroll
+        for (int c = 4; c < 8; ++c) cd[c] = 0.0;
+    } else {  // SPC, listdec.py:373-394
+        TopK<4> tk;
+        uint32_t hard;
+        const int par = leaf_scan_lane<4>(src, m, tk, hard);
+        const int odd = par & 1;
+        F.hard = hard;
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+            if (tk.i[x] >= m) tk.i[x] = 0;  // m < 4 never happens (SPC >= 4)
+        F.lrb01 = (uint32_t)tk.i[0] | ((uint32_t)tk.i[1] << 16);
+        F.lrb23 = (uint32_t)tk.i[2] | ((uint32_t)tk.i[3] << 16);
+        F.lflag = odd;
+        // deltas sum the net flips in ascending position order
+        int rk[4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            rk[x] = 0;
+#pragma unroll
+            for (int y = 0; y < 4; ++y) rk[x] += tk.i[y] < tk.i[x] ? 1 : 0;
+        }
+        double wr[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double v = 0.0;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) v = rk[x] == r ? (double)tk.m[x] : v;
+            wr[r] = v;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int fm = lk_flip_mask(K_SPC, c, odd);
+            int fr = 0;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) fr |= ((fm >> x) & 1) << rk[x];
+            double acc = 0.0;
+            bool any = false;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if ((fr >> r) & 1) {
+                    acc = any ? acc + wr[r] : wr[r];
+                    any = true;
+                }
+            cd[c] = any ? -acc : 0.0;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) key[c] = okey(F.pm + cd[c]);
+}
+
+// ------------------------------------------------------------ selection
+
+__device__ __forceinline__ int hi32(long long k) { return (int)(k >> 32); }
+
+// The survivors of one forking leaf: bit c of the result = candidate c of
+// this lane's path survives.  Exactly the list_size best (source, cand)
+// pairs by (metric desc, source asc, cand asc) == the bounded heap of
+// listdec.py:63-100 (tests/oracles.py:74-89).
+//
+// Pass 1 finds the L-th best high half Th of the order-preserving keys by a
+// k-way merge (each lane's candidates a sorted column; the kept set, slot =
+// lane, trades its worst for the best exposed candidate while that is
+// strictly better; one 32-bit REDUX per max / min).  Every key whose high
+// half is > Th survives; among the keys with high half == Th the `need`
+// best by full key survive, ties to the earlier (source, cand).
+template <int C>
+__device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool valid, int L, int lane) {
+    int srt[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) srt[c] = valid ? hi32(key[c]) : INT_MIN;
+    auto cs = [&](int a, int b) {
+        const int x = srt[a], y = srt[b];
+        srt[a] = max(x, y);
+        srt[b] = min(x, y);
+    };
+    if (C == 2) {
+        cs(0, 1);
+    } else if (C == 4) {  // Rate-1 columns are already sorted (0 >= -m1 >= -m2 >= -(m1+m2))
+        cs(0, 1); cs(2, 3); cs(0, 2); cs(1, 3); cs(1, 2);
+    } else {  // Batcher odd-even merge sort, 19 comparators
+        cs(0, 1); cs(2, 3); cs(4, 5); cs(6, 7);
+        cs(0, 2); cs(1, 3); cs(4, 6); cs(5, 7);
+        cs(1, 2); cs(5, 6);
+        cs(0, 4); cs(1, 5); cs(2, 6); cs(3, 7);
+        cs(2, 4); cs(3, 5);
+        cs(1, 2); cs(3, 4); cs(5, 6);
+    }
+    int kept = lane < L ? srt[0] : INT_MAX;
+#pragma unroll
+    for (int c = 0; c < C; ++c) srt[c] = c + 1 < C ? srt[c + 1 < C ? c + 1 : c] : INT_MIN;
+    int worst;
+    for (;;) {
+        const int best = __reduce_max_sync(FULL_MASK, srt[0]);
+        worst = __reduce_min_sync(FULL_MASK, kept);
+        if (best <= worst) break;
+        const int from = __ffs(__ballot_sync(FULL_MASK, srt[0] == best)) - 1;
+        const int into = __ffs(__ballot_sync(FULL_MASK, kept == worst)) - 1;
+        if (lane == from) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) srt[c] = c + 1 < C ? srt[c + 1 < C ? c + 1 : c] : INT_MIN;
+        }
+        if (lane == into) kept = best;
+    }
+    const int Th = worst;
+    unsigned mask = 0u, bmask = 0u;
+    int gt = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const int hk = valid ? hi32(key[c]) : INT_MIN;
+        if (hk > Th) {
+            mask |= 1u << c;
+            ++gt;
+        } else if (valid && hk == Th) {
+            bmask |= 1u << c;
+        }
+    }
+    const int need = L - (int)__reduce_add_sync(FULL_MASK, (unsigned)gt);
+    const int eqt = (int)__reduce_add_sync(FULL_MASK, (unsigned)__popc(bmask));
+    if (eqt <= need) return mask | bmask;  // the usual case: no surplus at the threshold
+    // surplus at Th: full keys decide, then (source, cand)
+    long long bmax = LLONG_MIN, bmin = LLONG_MAX;
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+        if ((bmask >> c) & 1u) {
+            bmax = max(bmax, key[c]);
+            bmin = min(bmin, key[c]);
+        }
+    if (warp_max_ll(bmax) == warp_min_ll(bmin)) {
+        // all tied exactly (int8 mode): the earliest `need` in (source, cand) order
+        int r = excl_scan4(__popc(bmask), lane);
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            if ((bmask >> c) & 1u) {
+                if (r < need) mask |= 1u << c;
+                ++r;
+            }
+        return mask;
+    }
+    // rare: one survivor at a time by (full key desc, source asc, cand asc)
+    for (int it = 0; it < need; ++it) {
+        long long mine = LLONG_MIN;
+        int mc = -1;
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            if (((bmask >> c) & 1u) && key[c] > mine) {
+                mine = key[c];
+                mc = c;
+            }
+        const long long best = warp_max_ll(mine);
+        const int from = __ffs(__ballot_sync(FULL_MASK, mc >= 0 && mine == best)) - 1;
+        if (lane == from) {
+            mask |= 1u << mc;
+            bmask &= ~(1u << mc);
+        }
+    }
+    return mask;
+}
+
+// ------------------------------------------------------- materialisation
+
+// word w (m >= 32) / the m-bit value (m < 32) of decision c of a path whose
+// leaf data is (hard, lrb, flag); `row` reads the leaf's LLRs again when the
+// hard decisions are wider than one word
+template <typename T, class S>
+__device__ __forceinline__ uint32_t leaf_word(int kind, int m, int c, uint32_t hard, uint32_t l01, uint32_t l23,
+                                              uint32_t flag, const S &row, int w) {
+    const uint32_t fullw = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+    if (kind == K_R0) return 0u;
+    if (kind == K_REP) {
+        const bool ones = flag ? (c == 0) : (c == 1);
+        return ones ? fullw : 0u;
+    }
+    uint32_t v = hard;
+    if (m > 32) {
+        v = 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float q[4];
+            row.quad(w * 8 + j, q);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v |= (q[e] < 0.f ? 1u : 0u) << (4 * j + e);
+        }
+    }
+    const int fm = lk_flip_mask(kind, c, (int)flag);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if ((fm >> j) & 1) {
+            const int pos = (int)(((j < 2 ? l01 : l23) >> ((j & 1) * 16)) & 0xffffu);
+            if ((pos >> 5) == w) v ^= 1u << (pos & 31);
+        }
+    return v;
+}
+
+// Leaf word of this lane's survivor into slot sE's row, then the chain of
+// Combines t .. sE-1 in place (listdec.py:327-332):
+//   dst[E - 2^(s+1), E - 2^s) = slot_s[row_s] ^ dst[E - 2^s, E)
+template <typename T>
+__device__ __forceinline__ void write_chain(Fr<T> &F, const LOp &o, int kind, uint32_t *dst, int c, uint32_t hard,
+                                            uint32_t l01, uint32_t l23, uint32_t flag) {
+    const int t = o.stage, sE = o.aux, m = 1 << t, E = 1 << sE;
+    const RowLd<T> row = leaf_src(F, o, t, F.ia);
+    if (m >= 32) {
+        for (int w = 0; w < (m >> 5); ++w)
+            dst[((E - m) >> 5) + w] = leaf_word<T>(kind, m, c, hard, l01, l23, flag, row, w);
+    } else {
+        const int s_sub = sE < 5 ? sE : 5;
+        const int W0 = E >= 32 ? E - 32 : 0;
+        uint32_t R = leaf_word<T>(kind, m, c, hard, l01, l23, flag, row, 0) << (E - m - W0);
+        for (int s = t; s < s_sub; ++s) {
+            const uint32_t sl = F.beta_row(s, get8(F.ib, s))[0];
+            const int seg = 1 << s;
+            R |= ((sl ^ (R >> (E - seg - W0))) & ((1u << seg) - 1u)) << (E - 2 * seg - W0);
+        }
+        if (E >= 32)
+            dst[(E >> 5) - 1] = R;
+        else
+            dst[0] = R & ((1u << E) - 1u);
+    }
+    for (int s = t > 5 ? t : 5; s < sE; ++s) {
+        const int seg = 1 << s, nw = seg >> 5;
+        const uint32_t *sl = F.beta_row(s, get8(F.ib, s));
+        uint32_t *da = dst + ((E - 2 * seg) >> 5);
+        const uint32_t *db = dst + ((E - seg) >> 5);
+        int w = 0;
+        for (; w + 4 <= nw; w += 4) {
+            uint32_t a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a[u] = sl[w + u];
+                b[u] = db[w + u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) da[w + u] = a[u] ^ b[u];
+        }
+        for (; w < nw; ++w) da[w] = sl[w] ^ db[w];
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
+    const LParams &P = F.P;
+    const int t = o.stage;
+    int kind = o.kind;
+    if (kind == K_R1 && t == 0) kind = K_REP;  // listdec.py:347
+    const bool valid = F.lane < o.pin;
+    long long key[8];
+    if (valid) leaf_phase_a(F, o, kind, key);
+    const int sE = o.aux;
+    if (kind == K_R0) {
+        if (sE < P.n && valid) {
+            uint32_t *dst = F.beta_row(sE, F.lane);
+            write_chain(F, o, K_R0, dst, 0, 0u, 0u, 0u, 0u);
+            set8(F.ib, sE, F.lane);
+        }
+        F.dec = 0;
+        return;
+    }
+    unsigned mask;
+    const int C = o.ncand;
+    if (!(o.flags & LF_SELECT)) {
+        mask = valid ? (1u << C) - 1u : 0u;
+    } else if (C == 2) {
+        mask = select_mask<2>(key, valid, P.L, F.lane);
+    } else if (C == 4) {
+        mask = select_mask<4>(key, valid, P.L, F.lane);
+    } else {
+        mask = select_mask<8>(key, valid, P.L, F.lane);
+    }
+    // survivors in (source, cand) order: this lane's go to slots off ..
+    uint8_t *asg = F.sm + P.lay.asg_off;
+    double *met = reinterpret_cast<double *>(F.sm + P.lay.met_off);
+    int k = excl_scan4(__popc(mask), F.lane);
+    while (mask) {
+        const int c = __ffs(mask) - 1;
+        mask &= mask - 1;
+        asg[k] = (uint8_t)((F.lane << 3) | c);
+        met[k] = unkey(key[c]);
+        ++k;
+    }
+    __syncwarp();
+    const bool live = F.lane < o.pout;
+    int p = F.lane, c = 0;
+    double pmn = F.pm;
+    if (live) {
+        const int v = asg[F.lane];
+        p = v >> 3;
+        c = v & 7;
+        pmn = met[F.lane];
+    }
+    __syncwarp();
+    // inherit the source's rows and leaf data (lazy copy, listdec.py:403-418)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        F.ia[j] = __shfl_sync(FULL_MASK, F.ia[j], p);
+        F.ib[j] = __shfl_sync(FULL_MASK, F.ib[j], p);
+    }
+    const uint32_t hard = __shfl_sync(FULL_MASK, F.hard, p);
+    const uint32_t l01 = __shfl_sync(FULL_MASK, F.lrb01, p);
+    const uint32_t l23 = __shfl_sync(FULL_MASK, F.lrb23, p);
+    const uint32_t flag = __shfl_sync(FULL_MASK, F.lflag, p);
+    F.pm = pmn;
+    F.hard = hard;
+    F.lrb01 = l01;
+    F.lrb23 = l23;
+    F.lflag = flag;
+    F.dec = (uint32_t)c;
+    if (live && sE < P.n) {
+        uint32_t *dst = F.beta_row(sE, F.lane);
+        write_chain(F, o, kind, dst, c, hard, l01, l23, flag);
+        set8(F.ib, sE, F.lane);
+    }
+}
+
+// ------------------------------------------------------------ finalise
+
+// Root codeword of survivor kk (listdec.py:275-287: the root row), built
+// on demand from its final leaf decision and its beta rows; warp-parallel.
+template <typename T>
+__device__ __forceinline__ void build_root(const Fr<T> &F, int kk, uint32_t *x) {
+    const LParams &P = F.P;
+    const LOp fo = P.prog[P.final_op];
+    const int N = P.N, n = P.n, t = fo.stage, m = 1 << t, lane = F.lane;
+    int kind = fo.kind;
+    if (kind == K_R1 && t == 0) kind = K_REP;
+    const int c = (int)__shfl_sync(FULL_MASK, F.dec, kk);
+    const uint32_t hard = __shfl_sync(FULL_MASK, F.hard, kk);
+    const uint32_t l01 = __shfl_sync(FULL_MASK, F.lrb01, kk);
+    const uint32_t l23 = __shfl_sync(FULL_MASK, F.lrb23, kk);
+    const uint32_t flag = __shfl_sync(FULL_MASK, F.lflag, kk);
+    uint32_t ib[4], ia[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        ib[j] = __shfl_sync(FULL_MASK, F.ib[j], kk);
+        ia[j] = __shfl_sync(FULL_MASK, F.ia[j], kk);
+    }
+    // the final leaf's LLR row (only read for words of leaves wider than 32)
+    const RowLd<T> src = leaf_src(F, fo, t, ia);
+    const int E = N;
+    if (m >= 32) {
+        for (int w = lane; w < (m >> 5); w += 32)
+            x[((E - m) >> 5) + w] = leaf_word<T>(kind, m, c, hard, l01, l23, flag, src, w);
+    } else if (lane == 0) {
+        const int s_sub = n < 5 ? n : 5;
+        const int W0 = E >= 32 ? E - 32 : 0;
+        uint32_t R = leaf_word<T>(kind, m, c, hard, l01, l23, flag, src, 0) << (E - m - W0);
+        for (int s = t; s < s_sub; ++s) {
+            const uint32_t sl = F.beta_row(s, get8(ib, s))[0];
+            const int seg = 1 << s;
+            R |= ((sl ^ (R >> (E - seg - W0))) & ((1u << seg) - 1u)) << (E - 2 * seg - W0);
+        }
+        if (E >= 32)
+            x[(E >> 5) - 1] = R;
+        else
+            x[0] = R & ((1u << E) - 1u);
+    }
+    __syncwarp();
+    for (int s = t > 5 ? t : 5; s < n; ++s) {
+        const int seg = 1 << s, nw = seg >> 5;
+        const uint32_t *sl = F.beta_row(s, get8(ib, s));
+        const int a = (E - 2 * seg) >> 5, b = (E - seg) >> 5;
+        for (int w = lane; w < nw; w += 32) x[a + w] = sl[w] ^ x[b + w];
+        __syncwarp();
+    }
+}
+
+__device__ __forceinline__ uint32_t syndrome(const LParams &P, const uint32_t *x, int lane) {
+    const int N = P.N, nw = N >= 32 ? N >> 5 : 1;
+    uint32_t s = 0u;
+    for (int w = lane; w < nw; w += 32) {
+        uint32_t v = x[w];
+        if (N < 32) v &= (1u << N) - 1u;
+        const uint32_t *t = P.xsyn4 + (size_t)w * 128;
+#pragma unroll
+        for (int nb = 0; nb < 8; ++nb) s ^= __ldg(t + nb * 16 + ((v >> (4 * nb)) & 15u));
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) s ^= __shfl_xor_sync(FULL_MASK, s, d);
+    return s;
+}
+
+// listdec.py:289-308: among CRC-passing survivors the strictly greater
+// metric wins, earliest survivor on ties; with none passing, the best metric
+// overall -- survivors visited by (metric desc, index asc), first pass wins.
+template <typename T>
+__device__ __forceinline__ void finalize(Fr<T> &F, long long f, int np) {
+    const LParams &P = F.P;
+    const int lane = F.lane;
+    const bool live = lane < np;
+    const double pmk = live ? F.pm : -INFINITY;
+    uint32_t *u = reinterpret_cast<uint32_t *>(F.sm + P.lay.root_off);
+    const int rw = P.N >= 32 ? P.N >> 5 : 1;
+    if (P.path_cw) {  // decode_paths: every survivor's codeword, metric and CRC flag
+        for (int kk = 0; kk < np; ++kk) {
+            uint32_t *dst = P.path_cw + ((size_t)f * P.L + kk) * rw;
+            if (P.N < 32 && lane == 0) dst[0] = 0u;
+            __syncwarp();
+            build_root(F, kk, dst);
+            const uint32_t syn = syndrome(P, dst, lane);
+            if (lane == 0) P.path_crc[(size_t)f * P.L + kk] = P.has_crc && syn == P.crc_const;
+        }
+        if (live) P.path_pm[(size_t)f * P.L + lane] = pmk;
+        __syncwarp();
+    }
+    unsigned tried = 0u;
+    int first = -1, wnr = -1;
+    double wpm = -INFINITY;
+    for (int it = 0; it < np; ++it) {
+        double bm = (live && !((tried >> lane) & 1u)) ? pmk : -INFINITY;
+        int bk = (live && !((tried >> lane) & 1u)) ? lane : 64;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const double om = __shfl_xor_sync(FULL_MASK, bm, d);
+            const int ok2 = __shfl_xor_sync(FULL_MASK, bk, d);
+            if (om > bm || (om == bm && ok2 < bk)) {
+                bm = om;
+                bk = ok2;
+            }
+        }
+        if (first < 0) first = bk;
+        tried |= 1u << bk;
+        if (!P.has_crc) {
+            wnr = bk;
+            wpm = bm;
+            break;
+        }
+        if (P.N < 32 && lane == 0) u[0] = 0u;
+        __syncwarp();
+        build_root(F, bk, u);
+        if (syndrome(P, u, lane) == P.crc_const) {
+            wnr = bk;
+            wpm = bm;
+            break;
+        }
+    }
+    const bool wok = wnr >= 0 && P.has_crc;
+    if (wnr < 0) {
+        wnr = first;
+        wpm = __shfl_sync(FULL_MASK, pmk, first & 31);
+    }
+    if (P.info_out) {
+        if (!wok) {
+            if (P.N < 32 && lane == 0) u[0] = 0u;
+            __syncwarp();
+            build_root(F, wnr, u);
+        }
+        polar_transform_words(u, P.N, lane);
+        uint8_t *out = P.info_out + (size_t)f * P.k;
+        for (int i = lane; i < P.k; i += 32) {
+            const uint32_t pos = __ldg(P.info_pos + i);
+            out[i] = (uint8_t)((u[pos >> 5] >> (pos & 31)) & 1u);
+        }
+    }
+    if (lane == 0) {
+        if (P.crc_ok) P.crc_ok[f] = wok;
+        if (P.pm_out) P.pm_out[f] = wpm;
+        if (P.paths_used) P.paths_used[f] = np;
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------------- kernel
+
+template <typename T>
+__device__ __forceinline__ void load_channel_lane(const LParams &P, T *ch, long long f, int lane) {
+    const int N = P.N;
+    if (P.in_type == PB_IN_I8) {
+        const int8_t *src = reinterpret_cast<const int8_t *>(P.llr) + (size_t)f * N;
+        for (int i = lane; i < N; i += 32) ch[i] = (T)src[i];
+        return;
+    }
+    const float *src = reinterpret_cast<const float *>(P.llr) + (size_t)f * N;
+    if ((N & 3) == 0) {
+        const float4 *s4 = reinterpret_cast<const float4 *>(src);
+        for (int i = lane; i < (N >> 2); i += 32) {
+            const float4 v = __ldcs(s4 + i);  // read once: evict-first
+            float q[4] = {ingest<T>(v.x), ingest<T>(v.y), ingest<T>(v.z), ingest<T>(v.w)};
+            V4<T>::st(ch + 4 * i, q);
+        }
+    } else {
+        for (int i = lane; i < N; i += 32) Elem<T>::st(ch + i, ingest<T>(src[i]));
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
+    const LParams &P = F.P;
+    for (int oi = 0; oi < P.n_ops; ++oi) {
+        const LOp o = P.prog[oi];
+        const int sel = o.kind <= K_G ? (o.kind * 16 + o.src * 2 + (o.aux == S_GL ? 1 : 0)) : -1;
+        switch (sel) {
+            // F: (source, destination) placements that occur (channel and
+            // stage n-1 sources only write stages read by a leaf)
+            case 0 * 16 + S_CH * 2 + 1: fg_op<T, false, S_CH, S_GL>(F, o); break;
+            case 1 * 16 + S_CH * 2 + 1: fg_op<T, true, S_CH, S_GL>(F, o); break;
+            case 0 * 16 + S_SM * 2 + 0: fg_op<T, false, S_SM, S_SM>(F, o); break;
+            case 0 * 16 + S_GL * 2 + 0: fg_op<T, false, S_GL, S_SM>(F, o); break;
+            case 0 * 16 + S_GL * 2 + 1: fg_op<T, false, S_GL, S_GL>(F, o); break;
+            case 0 * 16 + S_V1 * 2 + 1: fg_op<T, false, S_V1, S_GL>(F, o); break;
+            case 0 * 16 + S_V2 * 2 + 0: fg_op<T, false, S_V2, S_SM>(F, o); break;
+            case 0 * 16 + S_V2 * 2 + 1: fg_op<T, false, S_V2, S_GL>(F, o); break;
+            case 1 * 16 + S_SM * 2 + 0: fg_op<T, true, S_SM, S_SM>(F, o); break;
+            case 1 * 16 + S_GL * 2 + 0: fg_op<T, true, S_GL, S_SM>(F, o); break;
+            case 1 * 16 + S_GL * 2 + 1: fg_op<T, true, S_GL, S_GL>(F, o); break;
+            case 1 * 16 + S_V1 * 2 + 1: fg_op<T, true, S_V1, S_GL>(F, o); break;
+            case 1 * 16 + S_V2 * 2 + 0: fg_op<T, true, S_V2, S_SM>(F, o); break;
+            case 1 * 16 + S_V2 * 2 + 1: fg_op<T, true, S_V2, S_GL>(F, o); break;
+            default:
+                if (o.kind != K_NOP) {
+                    leaf_op(F, o);
+                    np = o.pout;
+                }
+                break;
+        }
+        if (P.sync_mask >= 0 && (oi & P.sync_mask) == 0)
+            __syncthreads();  // regroup the CTA's frames (shared instruction fetch)
+        else
+            __syncwarp();
+    }
+}
+
+// Persistent frame loop: a CTA holds P.fpc frames (one warp each).
+template <typename T>
+__global__ void __launch_bounds__(512, 1) k_lane(const __grid_constant__ LParams P) {
+    extern __shared__ __align__(16) unsigned char lk_smem[];
+    const int grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long slot = (long long)blockIdx.x * P.fpc + grp;
+    unsigned char *gs = P.gscratch ? P.gscratch + (size_t)slot * P.lay.gbytes : nullptr;
+    unsigned char *sm = lk_smem + (size_t)grp * P.lay.smem_bytes;
+    const long long stride = (long long)gridDim.x * P.fpc;
+    const long long batch = P.batch_dev ? (long long)*P.batch_dev : P.batch;
+    for (long long f0 = (long long)blockIdx.x * P.fpc; f0 < batch; f0 += stride) {
+        // tail: idle slots decode the last frame again and write nothing
+        const long long fi = f0 + grp < batch ? f0 + grp : batch - 1;
+        const long long f = P.frame_map ? (long long)P.frame_map[fi] : fi;
+        const bool own = f0 + grp < batch;
+        Fr<T> F(P, sm, gs);
+        load_channel_lane<T>(P, F.channel(), f, lane);
+        __syncwarp();
+        int np = 1;
+        run_ops(F, np);
+        if (own) finalize(F, f, np);
+        if (P.fpc > 1) __syncthreads();
+    }
+}
+
+#ifndef __CUDACC_RTC__
+template <typename T>
+cudaError_t lane_launch_t(const LParams *p, int grid, size_t smem, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(k_lane<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_lane<T><<<grid, 32 * p->fpc, smem, st>>>(*p);
+    return cudaGetLastError();
+}
+template <typename T>
+cudaError_t lane_occ_t(size_t smem, int fpc, int *bps) {
+    cudaError_t e = cudaFuncSetAttribute(k_lane<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(bps, k_lane<T>, 32 * fpc, smem);
+}
+#endif
+
+}  // namespace lk
+}  // namespace pb

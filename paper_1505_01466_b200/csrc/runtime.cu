@@ -31,6 +31,8 @@ extern "C" cudaError_t pb_launch_decode(const pb::Params *p, int mode, int warps
                                         cudaStream_t stream);
 extern "C" cudaError_t pb_occupancy(int mode, int warps, int ppw, int chg, size_t smem, int fpc, int *blocks_per_sm);
 extern "C" int pb_shape_supported(int mode, int warps, int ppw, int chg);
+extern "C" cudaError_t pb_lane_launch(const pb::lk::LParams *p, int mode, int grid, size_t smem, cudaStream_t st);
+extern "C" cudaError_t pb_lane_occupancy(int mode, size_t smem, int fpc, int *bps);
 extern "C" cudaError_t pb_launch_ssc(const pb::SscParams *p, int mode, int grid, cudaStream_t st);
 extern "C" cudaError_t pb_occupancy_ssc(int mode, int fpc, size_t smem_frame, int *bps);
 extern "C" cudaError_t pb_launch_gen(const pb::gen::GenParams *p, int sms, cudaStream_t st);
@@ -131,6 +133,12 @@ struct pb_handle {
     unsigned char *d_ssc_ch = nullptr;
     int32_t *d_fail = nullptr;   // adaptive: failing frame indices + per-chunk counts
     size_t d_fail_cap = 0;
+    // lane-per-path list kernel (lane_kernel.cuh), L in 17..32
+    bool lane = false;
+    pb::lk::LParams *lp = nullptr;  // host copy of the launch parameters (IO fields per call)
+    int lane_fpc = 0, lane_grid = 0;
+    size_t lane_smem = 0;           // per CTA
+    unsigned char *d_lane_scratch = nullptr;
     // on-device frame generation: all K info positions, payload syndrome rows
     uint32_t *d_info_all = nullptr, *d_hu = nullptr;
     int crc_w = 0;
@@ -206,6 +214,180 @@ int n_cands(int kind, int size, int L) {
 int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
 }  // namespace
+
+
+// ---- lane-per-path kernel plan (lane_kernel.cuh): lowering + storage.
+// Stages n-1 and n-2 are recomputed from the channel by F / G ops (never
+// stored); a leaf AT one of those stages reads a staging row in global
+// scratch that the F / G before it writes.  Returns false (the interpreted
+// kernel is used) when the plan does not fit.
+static bool is_leaf_kind(int k) { return k == PB_OP_RATE0 || k == PB_OP_RATE1 || k == PB_OP_REP || k == PB_OP_SPC; }
+
+static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vector<pb::DOp> &dprog, std::string &why) {
+    using namespace pb::lk;
+    const int N = h->N, n = h->n, L = h->L, mode = h->mode;
+    const int es = mode == PB_MODE_F32 ? 4 : 1;
+    const int NV = n >= 2 ? 2 : 1;
+    auto virt = [&](int s) { return s < n && s >= n - NV; };
+    if ((int)dprog.size() > kMaxOps) {
+        why = "op program too long";
+        return false;
+    }
+    bool staged[pb::kMaxLog] = {};
+    for (int i = 0; i + 1 < n_ops; ++i)
+        if ((ops[i].kind == PB_OP_F || ops[i].kind == PB_OP_G) && virt(ops[i].stage - 1) && is_leaf_kind(ops[i + 1].kind))
+            staged[ops[i].stage - 1] = true;
+    LLayout lay{};
+    const int smem_cap = 227 * 1024;
+    const int target_fps = std::max(1, env_int("PB_LANE_FPS", 16));
+    const int budget = smem_cap / target_fps / 16 * 16;
+    int off = 0, goff = 0;
+    lay.ch_off = 0;
+    off = align_up(N * es, 16);
+    lay.asg_off = off;
+    off = align_up(off + 32, 8);
+    lay.met_off = off;
+    off += 256;
+    lay.root_off = off;
+    off = align_up(off + std::max(1, N / 32) * 4, 16);
+    const int b_sm = env_int("PB_LANE_BETA_SM", 6);
+    for (int s = 0; s < n; ++s) {
+        const int words = std::max(1, (1 << s) / 32);
+        lay.b_stride[s] = words > 1 ? words + 1 : 1;
+        const int bytes = 32 * lay.b_stride[s] * 4;
+        if (s < b_sm && off + bytes <= budget) {
+            lay.b_off[s] = off;
+            off = align_up(off + bytes, 16);
+        } else {
+            lay.b_gl |= 1u << s;
+            lay.b_off[s] = goff;
+            goff = align_up(goff + bytes, 128);
+        }
+    }
+    bool spill = false;
+    for (int s = 0; s < n; ++s) {
+        if (virt(s) && !staged[s]) continue;
+        const int bytes = 32 * std::max(4, 1 << s) * es;
+        if (!virt(s) && !spill && off + bytes <= budget) {
+            lay.a_off[s] = off;
+            off = align_up(off + bytes, 16);
+        } else {
+            if (!virt(s)) spill = true;
+            lay.a_gl |= 1u << s;
+            lay.a_off[s] = goff;
+            goff = align_up(goff + bytes, 256);
+        }
+    }
+    lay.smem_bytes = align_up(off, 16);
+    lay.gbytes = align_up(goff, 256);
+    if (lay.smem_bytes > smem_cap) {
+        why = "shared-memory plan too large";
+        return false;
+    }
+    auto src_of = [&](int s) -> uint8_t {
+        if (s == n) return S_CH;
+        if (s == n - 1) return S_V1;
+        if (NV == 2 && s == n - 2) return S_V2;
+        return ((lay.a_gl >> s) & 1u) ? S_GL : S_SM;
+    };
+    // lowering (the interpreted kernel's program gives each leaf's path
+    // counts, candidates and Combine chain target)
+    std::vector<LOp> prog;
+    int di = 0, final_op = -1;
+    bool v1g = false, v2g = false;
+    for (int i = 0; i < n_ops; ++i) {
+        const pb_op &op = ops[i];
+        if (op.kind == PB_OP_COMBINE) continue;
+        const pb::DOp &d = dprog[di++];
+        if (op.kind == PB_OP_F || op.kind == PB_OP_G) {
+            const int s = op.stage;
+            const uint8_t flags = (v1g ? LF_V1G : 0) | (v2g ? LF_V2G : 0);
+            if (s == n) v1g = op.kind == PB_OP_G;
+            if (NV == 2 && s == n - 1) v2g = op.kind == PB_OP_G;
+            const bool out_virtual = virt(s - 1);
+            if (out_virtual && !staged[s - 1]) continue;  // a mode switch only
+            if (out_virtual && !(i + 1 < n_ops && is_leaf_kind(ops[i + 1].kind))) continue;
+            LOp l{};
+            l.kind = op.kind == PB_OP_F ? K_F : K_G;
+            l.stage = (uint8_t)s;
+            l.pin = l.pout = (uint8_t)d.pin;
+            l.src = src_of(s);
+            l.aux = ((lay.a_gl >> (s - 1)) & 1u) ? S_GL : S_SM;
+            l.flags = flags;
+            prog.push_back(l);
+            continue;
+        }
+        LOp l{};
+        l.kind = d.kind == pb::DK_R0 ? K_R0 : d.kind == pb::DK_REP ? K_REP : d.kind == pb::DK_R1 ? K_R1 : K_SPC;
+        l.stage = (uint8_t)op.stage;
+        l.pin = (uint8_t)d.pin;
+        l.pout = (uint8_t)d.pout;
+        l.ncand = (uint8_t)(d.kind == pb::DK_R0 ? 0 : d.ncand);
+        l.src = op.stage == n ? S_CH : (virt(op.stage) ? S_GL : src_of(op.stage));
+        l.aux = (uint8_t)d.target;
+        l.flags = (uint8_t)((d.select ? LF_SELECT : 0) | (v1g ? LF_V1G : 0) | (v2g ? LF_V2G : 0));
+        final_op = (int)prog.size();
+        prog.push_back(l);
+        // skip the Combines the leaf absorbed (the interpreted program did too)
+        if (op.side == 1) {
+            int j = i + 1;
+            while (j < n_ops && ops[j].kind == PB_OP_COMBINE) {
+                const int sd = ops[j].side, tg = ops[j].stage;
+                ++j;
+                if (sd == 0 || tg == n) break;
+            }
+            i = j - 1;
+        }
+    }
+    if ((int)prog.size() > kMaxOps) {
+        why = "op program too long";
+        return false;
+    }
+    int fpc = std::min(16, smem_cap / std::max(16, lay.smem_bytes));
+    int bps = 0;
+    while (fpc >= 1) {
+        if (pb_lane_occupancy(mode, (size_t)fpc * lay.smem_bytes, fpc, &bps) == cudaSuccess && bps >= 1) break;
+        cudaGetLastError();
+        --fpc;
+    }
+    if (fpc < 1) {
+        why = "no resident CTA";
+        return false;
+    }
+    LParams *lp = new LParams();
+    std::memset(lp, 0, sizeof(LParams));
+    lp->xsyn4 = h->d_xsyn4;
+    lp->info_pos = h->d_info;
+    lp->N = N;
+    lp->n = n;
+    lp->k = h->k;
+    lp->L = L;
+    lp->has_crc = h->base.has_crc;
+    lp->crc_const = h->base.crc_const;
+    lp->n_ops = (int)prog.size();
+    lp->final_op = final_op;
+    lp->fpc = fpc;
+    lp->sync_mask = fpc > 1 ? env_int("PB_LANE_SYNC_MASK", 31) : -1;
+    lp->lay = lay;
+    std::copy(prog.begin(), prog.end(), lp->prog);
+    h->lp = lp;
+    h->lane_fpc = fpc;
+    h->lane_grid = h->sms * bps;
+    h->lane_smem = (size_t)fpc * lay.smem_bytes;
+    if (lay.gbytes) {
+        cudaError_t e = cudaMalloc(&h->d_lane_scratch, (size_t)h->lane_grid * fpc * lay.gbytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            delete lp;
+            h->lp = nullptr;
+            why = "scratch allocation failed";
+            return false;
+        }
+    }
+    lp->gscratch = h->d_lane_scratch;
+    h->lane = true;
+    return true;
+}
 
 extern "C" {
 
@@ -677,6 +859,10 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         sp.gch = h->d_ssc_ch;
     }
 
+    std::string lane_why = "list size <= 16";
+    if (L > 16 && h->warps == 1 && env_int("PB_LANE", 1) != 0) plan_lane(h, ops, n_ops, h->prog, lane_why);
+    if (env_int("PB_LANE", 1) == 0) lane_why = "disabled";
+
     char buf[1024];
     snprintf(buf, sizeof buf,
              "{\"N\": %d, \"k\": %d, \"L\": %d, \"mode\": \"%s\", \"ops\": %d, \"device_ops\": %d, "
@@ -689,6 +875,19 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
              32 * h->warps * h->fpc, h->warps, h->ppw, h->fpc, (int)h->chg, h->ssc.lay.smem_bytes,
              h->ssc_ok ? h->ssc.fpc : 0, h->ssc_grid, (int)h->l1_ssc, (int)h->ssc_chg);
     h->plan_json = buf;
+    if (h->plan_json.size() > 1) {
+        char lb[512];
+        if (h->lane)
+            snprintf(lb, sizeof lb,
+                     ", \"lane_kernel\": {\"ops\": %d, \"smem_per_frame\": %d, \"global_scratch_per_frame\": %d, "
+                     "\"frames_per_cta\": %d, \"grid\": %d, \"alpha_global_mask\": %u, \"beta_global_mask\": %u}}",
+                     h->lp->n_ops, h->lp->lay.smem_bytes, h->lp->lay.gbytes, h->lane_fpc, h->lane_grid, h->lp->lay.a_gl,
+                     h->lp->lay.b_gl);
+        else
+            snprintf(lb, sizeof lb, ", \"lane_kernel\": null, \"lane_kernel_why\": \"%s\"}", lane_why.c_str());
+        h->plan_json.pop_back();
+        h->plan_json += lb;
+    }
     *out = h;
     return PB_OK;
 }
@@ -713,6 +912,8 @@ int pb_destroy(pb_handle *h) {
     }
     if (h->evs) cudaEventDestroy(h->evs);
     if (h->ev_busy) cudaEventDestroy(h->ev_busy);
+    cudaFree(h->d_lane_scratch);
+    delete h->lp;
     delete h;
     return PB_OK;
 }
@@ -821,6 +1022,26 @@ int run_kernels_unordered(pb_handle *h, const pb::Params &base, int in_type, con
         h->launches += 1;
         if (!adaptive) return PB_OK;
     }
+    if (h->lane) {
+        pb::lk::LParams *lp = h->lp;
+        lp->llr = j.llr;
+        lp->in_type = in_type;
+        lp->batch = j.batch;
+        lp->info_out = j.info;
+        lp->crc_ok = j.ok;
+        lp->pm_out = j.pm;
+        lp->paths_used = j.pu;
+        lp->path_cw = nullptr;
+        lp->path_pm = nullptr;
+        lp->path_crc = nullptr;
+        lp->frame_map = adaptive ? j.fail_idx : nullptr;
+        lp->batch_dev = adaptive ? j.fail_count : nullptr;
+        const int grid = (int)std::min<long long>(h->lane_grid, (j.batch + h->lane_fpc - 1) / h->lane_fpc);
+        cudaError_t e = pb_lane_launch(lp, h->mode, grid, h->lane_smem, st);
+        if (e != cudaSuccess) return cuda_fail(e, "lane decode kernel launch");
+        h->launches += 1;
+        return PB_OK;
+    }
     pb::Params pr = base;
     pr.llr = j.llr;
     pr.in_type = in_type;
@@ -921,7 +1142,26 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
     int rc = scratch_acquire(h, st);
     if (rc) return rc;
     PB_CUDA(cudaEventRecord(h->ev0, st));
-    cudaError_t e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc + h->prog_smem, st);
+    cudaError_t e;
+    if (h->lane && !pr.op_cycles) {
+        pb::lk::LParams *lp = h->lp;
+        lp->llr = pr.llr;
+        lp->in_type = pr.in_type;
+        lp->batch = pr.batch;
+        lp->info_out = pr.info_out;
+        lp->crc_ok = pr.crc_ok;
+        lp->pm_out = pr.pm_out;
+        lp->paths_used = pr.paths_used;
+        lp->path_cw = pr.path_cw;
+        lp->path_pm = pr.path_pm;
+        lp->path_crc = pr.path_crc;
+        lp->frame_map = nullptr;
+        lp->batch_dev = nullptr;
+        grid = (int)std::min<long long>(h->lane_grid, (pr.batch + h->lane_fpc - 1) / h->lane_fpc);
+        e = pb_lane_launch(lp, h->mode, grid, h->lane_smem, st);
+    } else {
+        e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc + h->prog_smem, st);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
     PB_CUDA(cudaEventRecord(h->ev1, st));
     h->timed = true;
