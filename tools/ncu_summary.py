@@ -12,7 +12,7 @@ import subprocess
 import sys
 
 REPO = __file__.rsplit("/tools/", 1)[0]
-KSRC = f"{REPO}/paper_1505_01466_b200/csrc/decode_kernel.cuh"
+KSRC = f"{REPO}/paper_1505_01466_b200/csrc/" + (sys.argv[4] if len(sys.argv) > 4 else "decode_kernel.cuh")
 
 
 def ncu(rep, *args):
