@@ -93,17 +93,18 @@ struct RowLd {  // a stored row (quad stride 128: 32 interleaved rows) or the ch
 };
 // stage n-1: f or g of the channel halves (g with the path's left-half bits,
 // beta slot n-1)
-template <typename T>
+template <typename T, int MODE = -1>  // MODE >= 0: g known at compile time (MODE & 1)
 struct V1Ld {
     const T *ch;
     const uint32_t *b1;
     int half;  // N / 2
-    bool g;
+    bool g_;
+    __device__ __forceinline__ bool gm() const { return MODE >= 0 ? (MODE & 1) != 0 : g_; }
     __device__ __forceinline__ void quad(int x, float (&v)[4]) const {
         float a[4], b[4];
         V4<T>::ld(ch + 4 * x, a);
         V4<T>::ld(ch + 4 * x + half, b);
-        if (g) {
+        if (gm()) {
             const unsigned bits = b1[x >> 3] >> ((x & 7) * 4);
 #pragma unroll
             for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(a[j], b[j], bits, j);
@@ -114,18 +115,39 @@ struct V1Ld {
     }
     __device__ __forceinline__ float get(int i) const {
         const float a = Elem<T>::ld(ch + i), b = Elem<T>::ld(ch + i + half);
-        return g ? g_op<T>(a, b, (b1[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+        return gm() ? g_op<T>(a, b, (b1[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+    }
+    // beta words of the 8-quad block starting at quad x (x % 8 == 0), loaded
+    // once per block; quadw = quad with them
+    struct Words {
+        uint32_t w1;
+    };
+    __device__ __forceinline__ Words words(int x) const { return Words{gm() ? b1[x >> 3] : 0u}; }
+    __device__ __forceinline__ void quadw(int x, float (&v)[4], const Words &w) const {
+        float a[4], b[4];
+        V4<T>::ld(ch + 4 * x, a);
+        V4<T>::ld(ch + 4 * x + half, b);
+        if (gm()) {
+            const unsigned bits = w.w1 >> ((x & 7) * 4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(a[j], b[j], bits, j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = f_op(a[j], b[j]);
+        }
     }
 };
 // stage n-2: f or g of two stage n-1 values (beta slot n-2), each f or g of
 // two channel values -- four channel loads per element, all lanes reading
 // the same address
-template <typename T>
+template <typename T, int MODE = -1>  // MODE >= 0: (g1, g2) = (MODE & 1, MODE >> 1) at compile time
 struct V2Ld {
     const T *ch;
     const uint32_t *b1, *b2;
     int q;  // N / 4
-    bool g1, g2;
+    bool g1_, g2_;
+    __device__ __forceinline__ bool m1() const { return MODE >= 0 ? (MODE & 1) != 0 : g1_; }
+    __device__ __forceinline__ bool m2() const { return MODE >= 0 ? (MODE & 2) != 0 : g2_; }
     __device__ __forceinline__ void quad(int x, float (&v)[4]) const {
         float c0[4], c1[4], c2[4], c3[4];
         V4<T>::ld(ch + 4 * x, c0);
@@ -133,7 +155,7 @@ struct V2Ld {
         V4<T>::ld(ch + 4 * x + 2 * q, c2);
         V4<T>::ld(ch + 4 * x + 3 * q, c3);
         float u0[4], u1[4];
-        if (g1) {
+        if (m1()) {
             const unsigned bl = b1[x >> 3] >> ((x & 7) * 4);
             const int xh = x + (q >> 2);
             const unsigned bh = b1[xh >> 3] >> ((xh & 7) * 4);
@@ -149,7 +171,7 @@ struct V2Ld {
                 u1[j] = f_op(c1[j], c3[j]);
             }
         }
-        if (g2) {
+        if (m2()) {
             const unsigned b = b2[x >> 3] >> ((x & 7) * 4);
 #pragma unroll
             for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(u0[j], u1[j], b, j);
@@ -160,11 +182,48 @@ struct V2Ld {
     }
     __device__ __forceinline__ float v1(int i) const {
         const float a = Elem<T>::ld(ch + i), b = Elem<T>::ld(ch + i + 2 * q);
-        return g1 ? g_op<T>(a, b, (b1[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+        return m1() ? g_op<T>(a, b, (b1[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
     }
     __device__ __forceinline__ float get(int i) const {
         const float a = v1(i), b = v1(i + q);
-        return g2 ? g_op<T>(a, b, (b2[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+        return m2() ? g_op<T>(a, b, (b2[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+    }
+    struct Words {
+        uint32_t wl, wh, w2;
+    };
+    __device__ __forceinline__ Words words(int x) const {
+        return Words{m1() ? b1[x >> 3] : 0u, m1() ? b1[(x + (q >> 2)) >> 3] : 0u, m2() ? b2[x >> 3] : 0u};
+    }
+    __device__ __forceinline__ void quadw(int x, float (&v)[4], const Words &w) const {
+        float c0[4], c1[4], c2[4], c3[4];
+        V4<T>::ld(ch + 4 * x, c0);
+        V4<T>::ld(ch + 4 * x + q, c1);
+        V4<T>::ld(ch + 4 * x + 2 * q, c2);
+        V4<T>::ld(ch + 4 * x + 3 * q, c3);
+        const int sh = (x & 7) * 4;
+        float u0[4], u1[4];
+        if (m1()) {
+            const unsigned bl = w.wl >> sh, bh = w.wh >> sh;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                u0[j] = g_op_bits<T>(c0[j], c2[j], bl, j);
+                u1[j] = g_op_bits<T>(c1[j], c3[j], bh, j);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                u0[j] = f_op(c0[j], c2[j]);
+                u1[j] = f_op(c1[j], c3[j]);
+            }
+        }
+        if (m2()) {
+            const unsigned b = w.w2 >> sh;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(u0[j], u1[j], b, j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = f_op(u0[j], u1[j]);
+        }
     }
 };
 template <typename T>
@@ -229,6 +288,35 @@ __device__ __forceinline__ void fg_body(const S &src, T *dst, const uint32_t *bw
     }
 }
 
+// F / G over a recomputed source: blocks of 8 quads share their beta words
+// (the source's and the G's), loaded once per block; U quads in flight
+template <typename T, bool IS_G, int U, class S>
+__device__ __forceinline__ void fg_body_v(const S &src, T *dst, const uint32_t *bw, int h) {
+    const int nq = h >> 2;  // >= 8 (callers take fg_body below)
+    for (int x0 = 0; x0 < nq; x0 += 8) {
+        const typename S::Words wa = src.words(x0), wb = src.words(x0 + nq);
+        const unsigned wd = IS_G ? bw[x0 >> 3] : 0u;
+#pragma unroll 1
+        for (int u0 = 0; u0 < 8; u0 += U) {
+            float a[U][4], b[U][4];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                src.quadw(x0 + u0 + u, a[u], wa);
+                src.quadw(x0 + u0 + u + nq, b[u], wb);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float o[4];
+                const unsigned bits = IS_G ? wd >> ((u0 + u) * 4) : 0u;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    o[j] = IS_G ? g_op_bits<T>(a[u][j], b[u][j], bits, j) : f_op(a[u][j], b[u][j]);
+                V4<T>::st(dst + (x0 + u0 + u) * 128, o);
+            }
+        }
+    }
+}
+
 // F / G of stage s into the path's own row of stage s-1 (listdec.py:317-326)
 template <typename T, bool IS_G, int SRC, int DST>
 __device__ __forceinline__ void fg_op(Fr<T> &F, const LOp &o) {
@@ -237,9 +325,25 @@ __device__ __forceinline__ void fg_op(Fr<T> &F, const LOp &o) {
         T *dst = F.template a_row_t<DST>(s - 1, F.lane);
         const uint32_t *bw = IS_G ? F.beta_row(s - 1, get8(F.ib, s - 1)) : nullptr;
         if (SRC == S_V2) {
-            fg_body<T, IS_G, 2>(make_v2(F, o), dst, bw, h);
+            // the recomputed stages' F / G modes are fixed for the whole op:
+            // one loop per mode pair, no per-quad branches
+            const V2Ld<T> v = make_v2(F, o);
+            if (h < 32) {
+                fg_body<T, IS_G, 2>(v, dst, bw, h);
+            } else switch ((v.g1_ ? 1 : 0) | (v.g2_ ? 2 : 0)) {
+                case 0: fg_body_v<T, IS_G, 2>(V2Ld<T, 0>{v.ch, v.b1, v.b2, v.q, false, false}, dst, bw, h); break;
+                case 1: fg_body_v<T, IS_G, 2>(V2Ld<T, 1>{v.ch, v.b1, v.b2, v.q, true, false}, dst, bw, h); break;
+                case 2: fg_body_v<T, IS_G, 2>(V2Ld<T, 2>{v.ch, v.b1, v.b2, v.q, false, true}, dst, bw, h); break;
+                default: fg_body_v<T, IS_G, 2>(V2Ld<T, 3>{v.ch, v.b1, v.b2, v.q, true, true}, dst, bw, h); break;
+            }
         } else if (SRC == S_V1) {
-            fg_body<T, IS_G, 4>(make_v1(F, o), dst, bw, h);
+            const V1Ld<T> v = make_v1(F, o);
+            if (h < 32)
+                fg_body<T, IS_G, 4>(v, dst, bw, h);
+            else if (v.g_)
+                fg_body_v<T, IS_G, 4>(V1Ld<T, 1>{v.ch, v.b1, v.half, true}, dst, bw, h);
+            else
+                fg_body_v<T, IS_G, 4>(V1Ld<T, 0>{v.ch, v.b1, v.half, false}, dst, bw, h);
         } else if (SRC == S_CH) {
             fg_body<T, IS_G, 4>(RowLd<T>{F.channel(), 4}, dst, bw, h);
         } else {
@@ -486,24 +590,28 @@ __device__ __forceinline__ void leaf_phase_a(Fr<T> &F, const LOp &o, int kind, l
 
 // ------------------------------------------------------------ selection
 
-__device__ __forceinline__ int hi32(long long k) { return (int)(k >> 32); }
+// the top 27 bits of the order-preserving metric key (sign, exponent, 15
+// mantissa bits; weakly monotone), low 5 bits free for a lane id
+__device__ __forceinline__ int hi27(long long k) { return (int)(k >> 32) & ~31; }
 
 // The survivors of one forking leaf: bit c of the result = candidate c of
 // this lane's path survives.  Exactly the list_size best (source, cand)
 // pairs by (metric desc, source asc, cand asc) == the bounded heap of
 // listdec.py:63-100 (tests/oracles.py:74-89).
 //
-// Pass 1 finds the L-th best high half Th of the order-preserving keys by a
-// k-way merge (each lane's candidates a sorted column; the kept set, slot =
-// lane, trades its worst for the best exposed candidate while that is
-// strictly better; one 32-bit REDUX per max / min).  Every key whose high
-// half is > Th survives; among the keys with high half == Th the `need`
+// Pass 1 finds the L-th best 27-bit key prefix Th by a k-way merge: each
+// lane's candidates form a sorted column and expose their best unconsumed
+// one; the kept set (slot = lane) trades its worst for the best exposed
+// candidate while that is strictly better.  Exposed keys carry their source
+// lane and kept keys their slot in the low 5 bits, so one REDUX max / min
+// names both lanes (no ballots): 2 independent REDUX per iteration.  Every
+// candidate whose prefix is > Th survives; among those == Th the `need`
 // best by full key survive, ties to the earlier (source, cand).
 template <int C>
 __device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool valid, int L, int lane) {
     int srt[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) srt[c] = valid ? hi32(key[c]) : INT_MIN;
+    for (int c = 0; c < C; ++c) srt[c] = (valid ? hi27(key[c]) : INT_MIN) | lane;
     auto cs = [&](int a, int b) {
         const int x = srt[a], y = srt[b];
         srt[a] = max(x, y);
@@ -521,28 +629,26 @@ __device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool 
         cs(2, 4); cs(3, 5);
         cs(1, 2); cs(3, 4); cs(5, 6);
     }
-    int kept = lane < L ? srt[0] : INT_MAX;
+    int kept = lane < L ? ((srt[0] & ~31) | lane) : INT_MAX;
 #pragma unroll
-    for (int c = 0; c < C; ++c) srt[c] = c + 1 < C ? srt[c + 1 < C ? c + 1 : c] : INT_MIN;
+    for (int c = 0; c < C; ++c) srt[c] = c + 1 < C ? srt[c + 1 < C ? c + 1 : c] : (INT_MIN | lane);
     int worst;
     for (;;) {
         const int best = __reduce_max_sync(FULL_MASK, srt[0]);
         worst = __reduce_min_sync(FULL_MASK, kept);
-        if (best <= worst) break;
-        const int from = __ffs(__ballot_sync(FULL_MASK, srt[0] == best)) - 1;
-        const int into = __ffs(__ballot_sync(FULL_MASK, kept == worst)) - 1;
-        if (lane == from) {
+        if ((best & ~31) <= (worst & ~31)) break;
+        if (lane == (best & 31)) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) srt[c] = c + 1 < C ? srt[c + 1 < C ? c + 1 : c] : INT_MIN;
+            for (int c = 0; c < C; ++c) srt[c] = c + 1 < C ? srt[c + 1 < C ? c + 1 : c] : (INT_MIN | lane);
         }
-        if (lane == into) kept = best;
+        if (lane == (worst & 31)) kept = (best & ~31) | lane;
     }
-    const int Th = worst;
+    const int Th = worst & ~31;
     unsigned mask = 0u, bmask = 0u;
     int gt = 0;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        const int hk = valid ? hi32(key[c]) : INT_MIN;
+        const int hk = valid ? hi27(key[c]) : INT_MIN;
         if (hk > Th) {
             mask |= 1u << c;
             ++gt;
@@ -572,7 +678,7 @@ __device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool 
             }
         return mask;
     }
-    // rare: one survivor at a time by (full key desc, source asc, cand asc)
+    // one survivor at a time by (full key desc, source asc, cand asc)
     for (int it = 0; it < need; ++it) {
         long long mine = LLONG_MIN;
         int mc = -1;
@@ -917,11 +1023,31 @@ __device__ __forceinline__ void load_channel_lane(const LParams &P, T *ch, long 
     }
 }
 
+// barrier over this frame's group of the CTA (all frames: bar 0; 2 groups:
+// named barriers 1 / 2)
+__device__ __forceinline__ void group_sync(int gid, int nthreads, bool whole) {
+    if (whole)
+        __syncthreads();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + gid), "r"(nthreads) : "memory");
+}
+
 template <typename T>
-__device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
+__device__ __forceinline__ void run_ops(Fr<T> &F, int &np, int o0, int o1, int gid, int gthreads) {
     const LParams &P = F.P;
-    for (int oi = 0; oi < P.n_ops; ++oi) {
-        const LOp o = P.prog[oi];
+    const bool whole = P.groups <= 1;
+#if PB_PROFILE
+    const bool prof = P.op_cycles && blockIdx.x == 0 && threadIdx.x == 0;
+#endif
+    for (int oi = o0; oi < o1; ++oi) {
+#if PB_PROFILE
+        if (prof) P.op_cycles[oi] = clock64();
+#endif
+        LOp o;
+        {
+            const uint2 raw = reinterpret_cast<const uint2 *>(P.prog)[oi];  // one 8-byte constant load
+            o = *reinterpret_cast<const LOp *>(&raw);
+        }
         const int sel = o.kind <= K_G ? (o.kind * 16 + o.src * 2 + (o.aux == S_GL ? 1 : 0)) : -1;
         switch (sel) {
             // F: (source, destination) placements that occur (channel and
@@ -931,12 +1057,14 @@ __device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
             case 0 * 16 + S_SM * 2 + 0: fg_op<T, false, S_SM, S_SM>(F, o); break;
             case 0 * 16 + S_GL * 2 + 0: fg_op<T, false, S_GL, S_SM>(F, o); break;
             case 0 * 16 + S_GL * 2 + 1: fg_op<T, false, S_GL, S_GL>(F, o); break;
+            case 0 * 16 + S_V1 * 2 + 0: fg_op<T, false, S_V1, S_SM>(F, o); break;
             case 0 * 16 + S_V1 * 2 + 1: fg_op<T, false, S_V1, S_GL>(F, o); break;
             case 0 * 16 + S_V2 * 2 + 0: fg_op<T, false, S_V2, S_SM>(F, o); break;
             case 0 * 16 + S_V2 * 2 + 1: fg_op<T, false, S_V2, S_GL>(F, o); break;
             case 1 * 16 + S_SM * 2 + 0: fg_op<T, true, S_SM, S_SM>(F, o); break;
             case 1 * 16 + S_GL * 2 + 0: fg_op<T, true, S_GL, S_SM>(F, o); break;
             case 1 * 16 + S_GL * 2 + 1: fg_op<T, true, S_GL, S_GL>(F, o); break;
+            case 1 * 16 + S_V1 * 2 + 0: fg_op<T, true, S_V1, S_SM>(F, o); break;
             case 1 * 16 + S_V1 * 2 + 1: fg_op<T, true, S_V1, S_GL>(F, o); break;
             case 1 * 16 + S_V2 * 2 + 0: fg_op<T, true, S_V2, S_SM>(F, o); break;
             case 1 * 16 + S_V2 * 2 + 1: fg_op<T, true, S_V2, S_GL>(F, o); break;
@@ -948,10 +1076,13 @@ __device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
                 break;
         }
         if (P.sync_mask >= 0 && (oi & P.sync_mask) == 0)
-            __syncthreads();  // regroup the CTA's frames (shared instruction fetch)
+            group_sync(gid, gthreads, whole);  // regroup the frames (shared instruction fetch)
         else
             __syncwarp();
     }
+#if PB_PROFILE
+    if (prof) P.op_cycles[P.n_ops] = clock64();
+#endif
 }
 
 // Persistent frame loop: a CTA holds P.fpc frames (one warp each).
@@ -964,18 +1095,30 @@ __global__ void __launch_bounds__(512, 1) k_lane(const __grid_constant__ LParams
     unsigned char *sm = lk_smem + (size_t)grp * P.lay.smem_bytes;
     const long long stride = (long long)gridDim.x * P.fpc;
     const long long batch = P.batch_dev ? (long long)*P.batch_dev : P.batch;
-    for (long long f0 = (long long)blockIdx.x * P.fpc; f0 < batch; f0 += stride) {
+    // frame groups: with two, the second starts half a program late (its
+    // first pass runs the second half of the ops on a throwaway frame) so the
+    // groups' op mixes interleave on the SM; each group keeps its frames in step
+    const int gsize = P.groups > 1 ? P.fpc / P.groups : P.fpc;
+    const int gid = grp / gsize, gthreads = 32 * gsize;
+    int o_start = (P.groups > 1 && gid == 1) ? P.n_ops / 2 : 0;
+    long long f0 = (long long)blockIdx.x * P.fpc;
+    while (f0 < batch) {
+        const bool dummy = o_start > 0;
         // tail: idle slots decode the last frame again and write nothing
         const long long fi = f0 + grp < batch ? f0 + grp : batch - 1;
         const long long f = P.frame_map ? (long long)P.frame_map[fi] : fi;
-        const bool own = f0 + grp < batch;
+        const bool own = f0 + grp < batch && !dummy;
         Fr<T> F(P, sm, gs);
-        load_channel_lane<T>(P, F.channel(), f, lane);
+        if (!dummy) load_channel_lane<T>(P, F.channel(), f, lane);
         __syncwarp();
         int np = 1;
-        run_ops(F, np);
+        run_ops(F, np, o_start, P.n_ops, gid, gthreads);
         if (own) finalize(F, f, np);
-        if (P.fpc > 1) __syncthreads();
+        if (P.fpc > 1) group_sync(gid, gthreads, P.groups <= 1);
+        if (dummy)
+            o_start = 0;
+        else
+            f0 += stride;
     }
 }
 

@@ -227,7 +227,9 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     using namespace pb::lk;
     const int N = h->N, n = h->n, L = h->L, mode = h->mode;
     const int es = mode == PB_MODE_F32 ? 4 : 1;
-    const int NV = n >= 2 ? 2 : 1;
+    // measured (c3 L=32): float32 3.09 Gbit/s with n-2 recomputed vs 2.86 stored;
+    // int8 3.53 stored vs 2.89 recomputed (small rows, costly conversions)
+    const int NV = n >= 2 ? std::max(1, std::min(2, env_int("PB_LANE_NV", mode == PB_MODE_F32 ? 2 : 1))) : 1;
     auto virt = [&](int s) { return s < n && s >= n - NV; };
     if ((int)dprog.size() > kMaxOps) {
         why = "op program too long";
@@ -367,7 +369,8 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     lp->n_ops = (int)prog.size();
     lp->final_op = final_op;
     lp->fpc = fpc;
-    lp->sync_mask = fpc > 1 ? env_int("PB_LANE_SYNC_MASK", 31) : -1;
+    lp->sync_mask = fpc > 1 ? env_int("PB_LANE_SYNC_MASK", 7) : -1;
+    lp->groups = (fpc >= 4 && fpc % 2 == 0) ? std::max(1, std::min(2, env_int("PB_LANE_GROUPS", 1))) : 1;
     lp->lay = lay;
     std::copy(prog.begin(), prog.end(), lp->prog);
     h->lp = lp;
@@ -1036,6 +1039,7 @@ int run_kernels_unordered(pb_handle *h, const pb::Params &base, int in_type, con
         lp->path_crc = nullptr;
         lp->frame_map = adaptive ? j.fail_idx : nullptr;
         lp->batch_dev = adaptive ? j.fail_count : nullptr;
+        lp->op_cycles = nullptr;
         const int grid = (int)std::min<long long>(h->lane_grid, (j.batch + h->lane_fpc - 1) / h->lane_fpc);
         cudaError_t e = pb_lane_launch(lp, h->mode, grid, h->lane_smem, st);
         if (e != cudaSuccess) return cuda_fail(e, "lane decode kernel launch");
@@ -1143,7 +1147,7 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
     if (rc) return rc;
     PB_CUDA(cudaEventRecord(h->ev0, st));
     cudaError_t e;
-    if (h->lane && !pr.op_cycles) {
+    if (h->lane) {
         pb::lk::LParams *lp = h->lp;
         lp->llr = pr.llr;
         lp->in_type = pr.in_type;
@@ -1157,6 +1161,7 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
         lp->path_crc = pr.path_crc;
         lp->frame_map = nullptr;
         lp->batch_dev = nullptr;
+        lp->op_cycles = pr.op_cycles;
         grid = (int)std::min<long long>(h->lane_grid, (pr.batch + h->lane_fpc - 1) / h->lane_fpc);
         e = pb_lane_launch(lp, h->mode, grid, h->lane_smem, st);
     } else {
@@ -1259,7 +1264,7 @@ extern "C" int pb_decode_adaptive(pb_handle *h, const void *llr, int in_type, in
 // Debug: decode `batch` host frames and return the clock64 cycles each device
 // op took for CTA 0's first frame (out: [pb_device_op_count] int64), plus
 // the op kinds/stages (kinds/stages may be null).
-extern "C" int pb_device_op_count(pb_handle *h) { return h ? (int)h->prog.size() : 0; }
+extern "C" int pb_device_op_count(pb_handle *h) { return h ? (h->lane ? h->lp->n_ops : (int)h->prog.size()) : 0; }
 extern "C" int pb_profile_ops(pb_handle *h, const void *llr, int in_type, int64_t batch, long long *cycles,
                               int8_t *kinds, int8_t *stages) {
     if (!h || !llr || !cycles) return fail(PB_EINVAL, "null argument");
@@ -1288,8 +1293,22 @@ extern "C" int pb_profile_ops(pb_handle *h, const void *llr, int in_type, int64_
     rc = launch(h, pr, 0);
     if (rc) return rc;
     PB_CUDA(cudaDeviceSynchronize());
-    PB_CUDA(cudaMemcpy(cycles, d_cyc, sizeof(long long) * 12 * h->prog.size(), cudaMemcpyDeviceToHost));
+    PB_CUDA(cudaMemcpy(cycles, d_cyc, sizeof(long long) * 12 * pb_device_op_count(h), cudaMemcpyDeviceToHost));
     cudaFree(d_cyc);
+    if (h->lane) {
+        // lane kernel: cycles[i] = clock64 at the start of op i (i <= n_ops);
+        // converted here to per-op durations in the 12-long rows the tool reads
+        const int n = h->lp->n_ops;
+        std::vector<long long> t(cycles, cycles + n + 1);
+        for (int i = 0; i < n; ++i) {
+            for (int x = 0; x < 12; ++x) cycles[i * 12 + x] = 0;
+            cycles[i * 12] = t[i + 1] - t[i];
+            cycles[i * 12 + 1] = t[i];
+            if (kinds) kinds[i] = (int8_t)h->lp->prog[i].kind;
+            if (stages) stages[i] = (int8_t)h->lp->prog[i].stage;
+        }
+        return PB_OK;
+    }
     for (size_t i = 0; i < h->prog.size(); ++i) {
         if (kinds) kinds[i] = h->prog[i].kind;
         if (stages) stages[i] = h->prog[i].stage;

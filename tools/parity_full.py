@@ -117,7 +117,8 @@ def run_oracle(names, threads):
         for c0, cn in _blocks(spec, frames // CHUNK, threads):
             fb = pb.generate_frames(spec, ebn0, seed=seed, start=c0 * CHUNK, count=cn * CHUNK,
                                     workers=threads)
-            r = oracle.decode_batch(sch, L, fb.llrs, int8=(mode == "int8"), threads=threads)
+            feed = pb.quantize_int8(fb.llrs) if mode == "int8" else fb.llrs  # the oracle's int8 mode takes quantised LLRs
+            r = oracle.decode_batch(sch, L, feed, int8=(mode == "int8"), threads=threads)
             for j in range(cn):
                 s = slice(j * CHUNK, (j + 1) * CHUNK)
                 rec["digests"].append(digest(r.info_bits[s], r.crc_ok[s], r.chosen_pm[s],
@@ -190,7 +191,8 @@ def run_gpu(names, max_chunks, out_path, workers):
 def _bisect(sch, L, mode, llrs, rb, s, c):
     """Frames of a mismatching chunk that differ from the oracle."""
     from oracle import oracle
-    o = oracle.decode_batch(sch, L, llrs, int8=(mode == "int8"), threads=os.cpu_count() or 1)
+    feed = pb.quantize_int8(llrs) if mode == "int8" else llrs
+    o = oracle.decode_batch(sch, L, feed, int8=(mode == "int8"), threads=os.cpu_count() or 1)
     ib, ok, pm, pu = rb.info_bits[s], rb.crc_ok[s], rb.chosen_pm[s], rb.paths_used[s]
     diff = np.nonzero((o.info_bits != ib).any(axis=1) | (o.crc_ok != ok)
                       | (o.chosen_pm != pm) | (o.paths_used != pu))[0]
