@@ -21,6 +21,12 @@
 #pragma once
 #include "decode_kernel.cuh"
 
+// stage n-2 reads specialised on the (n-1, n-2) F / G modes (one loop per
+// mode pair) instead of a uniform branch per quad
+#ifndef PB_LANE_V2SPEC
+#define PB_LANE_V2SPEC 1
+#endif
+
 namespace pb {
 namespace lk {
 
@@ -64,6 +70,12 @@ struct Fr {
         : P(p), sm(s), gs(g), lane(threadIdx.x & 31), pm(0.0), hard(0), lrb01(0), lrb23(0), lflag(0), dec(0) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) ia[i] = ib[i] = 0u;
+    }
+    long long *marks = nullptr;  // profiling build: this op's phase marks (CTA 0, frame slot 0, lane 0)
+    __device__ __forceinline__ void mark(int k) const {
+#if PB_PROFILE
+        if (marks) marks[k] = clock64();
+#endif
     }
     __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(sm + P.lay.ch_off); }
     __device__ __forceinline__ uint32_t *beta_row(int s, int row) const {
@@ -330,6 +342,8 @@ __device__ __forceinline__ void fg_op(Fr<T> &F, const LOp &o) {
             const V2Ld<T> v = make_v2(F, o);
             if (h < 32) {
                 fg_body<T, IS_G, 2>(v, dst, bw, h);
+            } else if (!PB_LANE_V2SPEC) {
+                fg_body_v<T, IS_G, 2>(v, dst, bw, h);
             } else switch ((v.g1_ ? 1 : 0) | (v.g2_ ? 2 : 0)) {
                 case 0: fg_body_v<T, IS_G, 2>(V2Ld<T, 0>{v.ch, v.b1, v.b2, v.q, false, false}, dst, bw, h); break;
                 case 1: fg_body_v<T, IS_G, 2>(V2Ld<T, 1>{v.ch, v.b1, v.b2, v.q, true, false}, dst, bw, h); break;
@@ -787,6 +801,8 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
     const bool valid = F.lane < o.pin;
     long long key[8];
     if (valid) leaf_phase_a(F, o, kind, key);
+    __syncwarp();
+    F.mark(0);
     const int sE = o.aux;
     if (kind == K_R0) {
         if (sE < P.n && valid) {
@@ -808,6 +824,7 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
     } else {
         mask = select_mask<8>(key, valid, P.L, F.lane);
     }
+    F.mark(1);
     // survivors in (source, cand) order: this lane's go to slots off ..
     uint8_t *asg = F.sm + P.lay.asg_off;
     double *met = reinterpret_cast<double *>(F.sm + P.lay.met_off);
@@ -846,6 +863,7 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
     F.lrb23 = l23;
     F.lflag = flag;
     F.dec = (uint32_t)c;
+    F.mark(2);
     if (live && sE < P.n) {
         uint32_t *dst = F.beta_row(sE, F.lane);
         write_chain(F, o, kind, dst, c, hard, l01, l23, flag);
@@ -1042,6 +1060,7 @@ __device__ __forceinline__ void run_ops(Fr<T> &F, int &np, int o0, int o1, int g
     for (int oi = o0; oi < o1; ++oi) {
 #if PB_PROFILE
         if (prof) P.op_cycles[oi] = clock64();
+        F.marks = prof ? P.op_cycles + P.n_ops + 1 + 4 * oi : nullptr;
 #endif
         LOp o;
         {

@@ -1277,8 +1277,9 @@ extern "C" int pb_profile_ops(pb_handle *h, const void *llr, int in_type, int64_
     int rc = ensure(&h->d_in, &h->d_in_cap, in_bytes);
     if (rc) return rc;
     long long *d_cyc = nullptr;
-    PB_CUDA(cudaMalloc(&d_cyc, sizeof(long long) * 12 * h->prog.size()));
-    PB_CUDA(cudaMemset(d_cyc, 0, sizeof(long long) * 12 * h->prog.size()));
+    const size_t ncyc = 12 * std::max<size_t>(h->prog.size(), h->lane ? (size_t)h->lp->n_ops + 1 : 0);
+    PB_CUDA(cudaMalloc(&d_cyc, sizeof(long long) * ncyc));
+    PB_CUDA(cudaMemset(d_cyc, 0, sizeof(long long) * ncyc));
     PB_CUDA(cudaMemcpy(h->d_in, llr, in_bytes, cudaMemcpyHostToDevice));
     pb::Params pr = h->base;
     pr.llr = h->d_in;
@@ -1294,16 +1295,28 @@ extern "C" int pb_profile_ops(pb_handle *h, const void *llr, int in_type, int64_
     if (rc) return rc;
     PB_CUDA(cudaDeviceSynchronize());
     PB_CUDA(cudaMemcpy(cycles, d_cyc, sizeof(long long) * 12 * pb_device_op_count(h), cudaMemcpyDeviceToHost));
+    if (h->lane) {  // the lane kernel's marks follow its op start times: fetch them too
+        std::vector<long long> all(ncyc);
+        PB_CUDA(cudaMemcpy(all.data(), d_cyc, sizeof(long long) * ncyc, cudaMemcpyDeviceToHost));
+        const int n = h->lp->n_ops;
+        // pack [n+1 starts][4n marks] into the caller's buffer (12n longs >= 5n+1)
+        std::copy(all.begin(), all.begin() + (n + 1 + 4 * n), cycles);
+    }
     cudaFree(d_cyc);
     if (h->lane) {
         // lane kernel: cycles[i] = clock64 at the start of op i (i <= n_ops);
         // converted here to per-op durations in the 12-long rows the tool reads
         const int n = h->lp->n_ops;
-        std::vector<long long> t(cycles, cycles + n + 1);
+        std::vector<long long> t(cycles, cycles + n + 1 + 4 * n);
         for (int i = 0; i < n; ++i) {
             for (int x = 0; x < 12; ++x) cycles[i * 12 + x] = 0;
             cycles[i * 12] = t[i + 1] - t[i];
             cycles[i * 12 + 1] = t[i];
+            // leaf phase marks -> the tool's columns: A end (2+0), B end (2+1), C copies (2+7)
+            const long long *mk = t.data() + n + 1 + 4 * i;
+            cycles[i * 12 + 2 + 0] = mk[0];
+            cycles[i * 12 + 2 + 1] = mk[1];
+            cycles[i * 12 + 2 + 7] = mk[2];
             if (kinds) kinds[i] = (int8_t)h->lp->prog[i].kind;
             if (stages) stages[i] = (int8_t)h->lp->prog[i].stage;
         }
