@@ -43,6 +43,16 @@ __device__ __forceinline__ void set8(uint32_t (&w)[4], int s, int v) {
         if (j == i) w[i] = (w[i] & m) | vv;
 }
 
+// min-sum F with the sign from a product: FMNMX and LOP3 on the ALU pipe,
+// FMUL on the FMA pipe (f_op is three ALU-pipe instructions; the two pipes
+// each take a warp instruction every other cycle).  sign(a*b) = sign(a) ^
+// sign(b) for all finite a, b (LLRs are clamped), zero products included.
+__device__ __forceinline__ float f_op(float a, float b) {
+    const float m = fminf(fabsf(a), fabsf(b));
+    const float s = __fmul_rn(a, b);
+    return __uint_as_float(__float_as_uint(m) | (__float_as_uint(s) & 0x80000000u));
+}
+
 // the inverse of okey (an involution on the bit pattern)
 __device__ __forceinline__ double unkey(long long k) {
     return __longlong_as_double(k ^ ((k >> 63) & 0x7fffffffffffffffLL));

@@ -55,3 +55,31 @@ for kk, sg in groups:
         v = v[v > 0]
         return f"{v.mean():7.0f}" if v.size else "      -"
     print(f'  {names[kk]:4s}{"" if sg is None else sg:>3} n={int(sel.sum()):3d} ' + ' '.join(mm(m) for m in (2, 0, 4, 5, 6, 1, 7)) + f' {cyc4[sel,0].mean():7.0f}')
+
+# lane kernel: cycles by active-path count (pin) bucket
+try:
+    import json as _json
+    plan = _json.loads(dec.plan)
+    if plan.get("lane_kernel"):
+        n = spec.n
+        cand = lambda op: (1 if op.kind is pb.NodeKind.RATE0 else 2 if (op.kind is pb.NodeKind.REP or (op.kind is pb.NodeKind.RATE1 and op.size == 1)) else 4 if op.kind is pb.NodeKind.RATE1 else (2 if L == 2 else 8))
+        P, pins = 1, []
+        for op in sch.ops:
+            k = op.kind
+            if k is pb.NodeKind.COMBINE:
+                continue
+            if k in (pb.NodeKind.F, pb.NodeKind.G):
+                if op.stage >= n - 1 and mode == "f32" or op.stage >= n and mode != "f32":
+                    continue
+                pins.append(P)
+                continue
+            pins.append(P)
+            if k is not pb.NodeKind.RATE0:
+                P = min(L, P * cand(op))
+        pins = np.array(pins[:len(cyc)])
+        print("cycles by active paths before the op:")
+        for lo, hi in ((1, 1), (2, 4), (5, 16), (17, 31), (32, 32)):
+            sel = (pins >= lo) & (pins <= hi)
+            print(f"  pin {lo:2d}..{hi:2d}: {sel.sum():4d} ops {cyc[:len(pins)][sel].sum():9d} cycles {100 * cyc[:len(pins)][sel].sum() / tot:5.1f}%")
+except Exception as e:  # noqa: BLE001
+    print("pin buckets unavailable:", e)
