@@ -161,6 +161,7 @@ struct LLayout {
     int asg_off;              // uint8 [32] survivor -> (source << 3 | cand)
     int met_off;              // double [32] survivor metrics
     int root_off;             // uint32 [max(1, N/32)] codeword scratch (finalise)
+    int hard_off;             // global: uint32 [hard_words][32] hard decisions of leaves wider than 32
     int smem_bytes;           // per frame (16-byte multiple)
     int gbytes;               // per frame global scratch (256-byte multiple)
 };
@@ -186,6 +187,7 @@ struct LParams {
     const int32_t *batch_dev;
     int fpc;
     int groups;                 // frame groups per CTA (1 or 2: the second starts half a program late)
+    int stagger;                // CTA b starts (b / grid) of a program late (spreads the SMs' op mix)
     int sync_mask;
     long long *op_cycles;       // profiling build: clock64 at the start of each op (CTA 0, frame slot 0), or null
     LLayout lay;

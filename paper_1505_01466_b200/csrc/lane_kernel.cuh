@@ -75,9 +75,10 @@ struct Fr {
     uint32_t lrb23;      // positions 2, 3
     uint32_t lflag;      // Rep: ones first; SPC: odd parity
     uint32_t dec;        // candidate chosen (0 .. 7)
+    uint32_t srcl;       // source lane of that decision
 
     __device__ __forceinline__ Fr(const LParams &p, unsigned char *s, unsigned char *g)
-        : P(p), sm(s), gs(g), lane(threadIdx.x & 31), pm(0.0), hard(0), lrb01(0), lrb23(0), lflag(0), dec(0) {
+        : P(p), sm(s), gs(g), lane(threadIdx.x & 31), pm(0.0), hard(0), lrb01(0), lrb23(0), lflag(0), dec(0), srcl(0) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) ia[i] = ib[i] = 0u;
     }
@@ -88,6 +89,11 @@ struct Fr {
 #endif
     }
     __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(sm + P.lay.ch_off); }
+    // hard-decision words of leaves wider than 32 (global scratch): word w of
+    // lane q's path at [w * 32 + q]
+    __device__ __forceinline__ uint32_t *hard_words() const {
+        return reinterpret_cast<uint32_t *>(gs + P.lay.hard_off);
+    }
     __device__ __forceinline__ uint32_t *beta_row(int s, int row) const {
         unsigned char *base = ((P.lay.b_gl >> s) & 1u) ? gs : sm;
         return reinterpret_cast<uint32_t *>(base + P.lay.b_off[s]) + row * P.lay.b_stride[s];
@@ -454,7 +460,7 @@ __device__ __forceinline__ void pw_sums_lane(const S &src, int m, float (&out)[N
 // listdec.py:362,375), hard-decision word(s), parity.  Returns the parity;
 // `hard` = the hard word when m <= 32.
 template <int K, class S>
-__device__ __forceinline__ int leaf_scan_lane(const S &src, int m, TopK<K> &tk, uint32_t &hard) {
+__device__ __forceinline__ int leaf_scan_lane(const S &src, int m, TopK<K> &tk, uint32_t &hard, uint32_t *hw) {
     tk.init();
     int par = 0;
     hard = 0u;
@@ -479,6 +485,7 @@ __device__ __forceinline__ int leaf_scan_lane(const S &src, int m, TopK<K> &tk, 
                 tc[j % NCH].push_scan(fabsf(v[j]), w0 + j);
             }
             hard = word;
+            if (m > 32) hw[(w0 >> 5) * 32] = word;
             par ^= __popc(word);
         }
         tk = tc[0];
@@ -486,6 +493,32 @@ __device__ __forceinline__ int leaf_scan_lane(const S &src, int m, TopK<K> &tk, 
         for (int h = 1; h < NCH; ++h)
 #pragma unroll
             for (int e = 0; e < K; ++e) tk.insert(tc[h].m[e], tc[h].i[e]);
+    } else if (K == 4 && m == 4) {
+        // SPC of size 4 (the default cap): every position is a least
+        // reliable one -- a stable 5-comparator sort of (|a|, index)
+        float q[4];
+        src.quad(0, q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            hard |= (q[e] < 0.f ? 1u : 0u) << e;
+            tk.m[e] = fabsf(q[e]);
+            tk.i[e] = e;
+        }
+        auto cx = [&](int a, int b) {  // (m, i) lexicographic: a before b
+            const bool sw = tk.m[b] < tk.m[a] || (tk.m[b] == tk.m[a] && tk.i[b] < tk.i[a]);
+            const float ma = tk.m[a], mb = tk.m[b];
+            const int ia = tk.i[a], ib = tk.i[b];
+            tk.m[a] = sw ? mb : ma;
+            tk.m[b] = sw ? ma : mb;
+            tk.i[a] = sw ? ib : ia;
+            tk.i[b] = sw ? ia : ib;
+        };
+        cx(0, 1);
+        cx(2, 3);
+        cx(0, 2);
+        cx(1, 3);
+        cx(1, 2);
+        par = __popc(hard);
     } else if (m >= 4) {
         float v[16];
 #pragma unroll
@@ -551,7 +584,7 @@ __device__ __forceinline__ void leaf_phase_a(Fr<T> &F, const LOp &o, int kind, l
     } else if (kind == K_R1) {  // listdec.py:360-372
         TopK<2> tk;
         uint32_t hard;
-        leaf_scan_lane<2>(src, m, tk, hard);
+        leaf_scan_lane<2>(src, m, tk, hard, F.hard_words() + F.lane);
         F.hard = hard;
         F.lrb01 = (uint32_t)tk.i[0] | ((uint32_t)tk.i[1] << 16);
         F.lrb23 = 0u;
@@ -566,7 +599,7 @@ __device__ __forceinline__ void leaf_phase_a(Fr<T> &F, const LOp &o, int kind, l
     } else {  // SPC, listdec.py:373-394
         TopK<4> tk;
         uint32_t hard;
-        const int par = leaf_scan_lane<4>(src, m, tk, hard);
+        const int par = leaf_scan_lane<4>(src, m, tk, hard, F.hard_words() + F.lane);
         const int odd = par & 1;
         F.hard = hard;
 #pragma unroll
@@ -575,37 +608,58 @@ __device__ __forceinline__ void leaf_phase_a(Fr<T> &F, const LOp &o, int kind, l
         F.lrb01 = (uint32_t)tk.i[0] | ((uint32_t)tk.i[1] << 16);
         F.lrb23 = (uint32_t)tk.i[2] | ((uint32_t)tk.i[3] << 16);
         F.lflag = odd;
-        // deltas sum the net flips in ascending position order
-        int rk[4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-            rk[x] = 0;
-#pragma unroll
-            for (int y = 0; y < 4; ++y) rk[x] += tk.i[y] < tk.i[x] ? 1 : 0;
-        }
+        // deltas: minus the sum of the net flips' magnitudes in ascending
+        // position order (Python's sum from 0: 0.0 + w is w exactly, and an
+        // empty flip set gives pm + -0.0 == pm).  rbit[x] = bit of LRB slot x
+        // in position-rank order; wr[r] = magnitude of the r-th by position.
+        uint32_t rbit[4];
         double wr[4];
+        if (m == 4) {  // the four positions are 0..3: rank = position
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            double v = 0.0;
+            for (int x = 0; x < 4; ++x) rbit[x] = 1u << tk.i[x];
 #pragma unroll
-            for (int x = 0; x < 4; ++x) v = rk[x] == r ? (double)tk.m[x] : v;
-            wr[r] = v;
+            for (int r = 0; r < 4; ++r) {
+                double v = 0.0;
+#pragma unroll
+                for (int x = 0; x < 4; ++x) v = tk.i[x] == r ? (double)tk.m[x] : v;
+                wr[r] = v;
+            }
+        } else {
+            int rk[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                rk[x] = 0;
+#pragma unroll
+                for (int y = 0; y < 4; ++y) rk[x] += tk.i[y] < tk.i[x] ? 1 : 0;
+                rbit[x] = 1u << rk[x];
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double v = 0.0;
+#pragma unroll
+                for (int x = 0; x < 4; ++x) v = rk[x] == r ? (double)tk.m[x] : v;
+                wr[r] = v;
+            }
         }
+        // flip sets in rank bits: ML {lrb0} if odd, then the pairs of
+        // _SPC_PAIRS (listdec.py:157) and all four, each XOR the ML set
+        const uint32_t ml = odd ? rbit[0] : 0u;
+        uint32_t fr[8];
+        fr[0] = ml;
+        fr[1] = (rbit[0] | rbit[1]) ^ ml;
+        fr[2] = (rbit[0] | rbit[2]) ^ ml;
+        fr[3] = (rbit[0] | rbit[3]) ^ ml;
+        fr[4] = (rbit[1] | rbit[2]) ^ ml;
+        fr[5] = (rbit[1] | rbit[3]) ^ ml;
+        fr[6] = (rbit[2] | rbit[3]) ^ ml;
+        fr[7] = 0xfu ^ ml;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            const int fm = lk_flip_mask(K_SPC, c, odd);
-            int fr = 0;
-#pragma unroll
-            for (int x = 0; x < 4; ++x) fr |= ((fm >> x) & 1) << rk[x];
             double acc = 0.0;
-            bool any = false;
 #pragma unroll
             for (int r = 0; r < 4; ++r)
-                if ((fr >> r) & 1) {
-                    acc = any ? acc + wr[r] : wr[r];
-                    any = true;
-                }
-            cd[c] = any ? -acc : 0.0;
+                if ((fr[c] >> r) & 1u) acc += wr[r];
+            cd[c] = -acc;
         }
     }
 #pragma unroll
@@ -725,28 +779,18 @@ __device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool 
 // ------------------------------------------------------- materialisation
 
 // word w (m >= 32) / the m-bit value (m < 32) of decision c of a path whose
-// leaf data is (hard, lrb, flag); `row` reads the leaf's LLRs again when the
-// hard decisions are wider than one word
-template <typename T, class S>
+// leaf data is (hard, lrb, flag); hw = the source path's hard words when the
+// leaf is wider than one word
 __device__ __forceinline__ uint32_t leaf_word(int kind, int m, int c, uint32_t hard, uint32_t l01, uint32_t l23,
-                                              uint32_t flag, const S &row, int w) {
+                                              uint32_t flag, const uint32_t *hw, int w) {
     const uint32_t fullw = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
     if (kind == K_R0) return 0u;
     if (kind == K_REP) {
         const bool ones = flag ? (c == 0) : (c == 1);
         return ones ? fullw : 0u;
     }
-    uint32_t v = hard;
-    if (m > 32) {
-        v = 0u;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            float q[4];
-            row.quad(w * 8 + j, q);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) v |= (q[e] < 0.f ? 1u : 0u) << (4 * j + e);
-        }
-    }
+    const uint32_t v0 = m > 32 ? hw[w * 32] : hard;
+    uint32_t v = v0;
     const int fm = lk_flip_mask(kind, c, (int)flag);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
@@ -761,17 +805,17 @@ __device__ __forceinline__ uint32_t leaf_word(int kind, int m, int c, uint32_t h
 // Combines t .. sE-1 in place (listdec.py:327-332):
 //   dst[E - 2^(s+1), E - 2^s) = slot_s[row_s] ^ dst[E - 2^s, E)
 template <typename T>
-__device__ __forceinline__ void write_chain(Fr<T> &F, const LOp &o, int kind, uint32_t *dst, int c, uint32_t hard,
-                                            uint32_t l01, uint32_t l23, uint32_t flag) {
+__device__ __forceinline__ void write_chain(Fr<T> &F, const LOp &o, int kind, uint32_t *dst, int p, int c,
+                                            uint32_t hard, uint32_t l01, uint32_t l23, uint32_t flag) {
     const int t = o.stage, sE = o.aux, m = 1 << t, E = 1 << sE;
-    const RowLd<T> row = leaf_src(F, o, t, F.ia);
+    const uint32_t *row = F.hard_words() + p;
     if (m >= 32) {
         for (int w = 0; w < (m >> 5); ++w)
-            dst[((E - m) >> 5) + w] = leaf_word<T>(kind, m, c, hard, l01, l23, flag, row, w);
+            dst[((E - m) >> 5) + w] = leaf_word(kind, m, c, hard, l01, l23, flag, row, w);
     } else {
         const int s_sub = sE < 5 ? sE : 5;
         const int W0 = E >= 32 ? E - 32 : 0;
-        uint32_t R = leaf_word<T>(kind, m, c, hard, l01, l23, flag, row, 0) << (E - m - W0);
+        uint32_t R = leaf_word(kind, m, c, hard, l01, l23, flag, row, 0) << (E - m - W0);
         for (int s = t; s < s_sub; ++s) {
             const uint32_t sl = F.beta_row(s, get8(F.ib, s))[0];
             const int seg = 1 << s;
@@ -817,7 +861,7 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
     if (kind == K_R0) {
         if (sE < P.n && valid) {
             uint32_t *dst = F.beta_row(sE, F.lane);
-            write_chain(F, o, K_R0, dst, 0, 0u, 0u, 0u, 0u);
+            write_chain(F, o, K_R0, dst, F.lane, 0, 0u, 0u, 0u, 0u);
             set8(F.ib, sE, F.lane);
         }
         F.dec = 0;
@@ -873,10 +917,11 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
     F.lrb23 = l23;
     F.lflag = flag;
     F.dec = (uint32_t)c;
+    F.srcl = (uint32_t)p;
     F.mark(2);
     if (live && sE < P.n) {
         uint32_t *dst = F.beta_row(sE, F.lane);
-        write_chain(F, o, kind, dst, c, hard, l01, l23, flag);
+        write_chain(F, o, kind, dst, p, c, hard, l01, l23, flag);
         set8(F.ib, sE, F.lane);
     }
 }
@@ -903,16 +948,16 @@ __device__ __forceinline__ void build_root(const Fr<T> &F, int kk, uint32_t *x) 
         ib[j] = __shfl_sync(FULL_MASK, F.ib[j], kk);
         ia[j] = __shfl_sync(FULL_MASK, F.ia[j], kk);
     }
-    // the final leaf's LLR row (only read for words of leaves wider than 32)
-    const RowLd<T> src = leaf_src(F, fo, t, ia);
+    // the final leaf's hard words (leaves wider than 32)
+    const uint32_t *src = F.hard_words() + __shfl_sync(FULL_MASK, F.srcl, kk);
     const int E = N;
     if (m >= 32) {
         for (int w = lane; w < (m >> 5); w += 32)
-            x[((E - m) >> 5) + w] = leaf_word<T>(kind, m, c, hard, l01, l23, flag, src, w);
+            x[((E - m) >> 5) + w] = leaf_word(kind, m, c, hard, l01, l23, flag, src, w);
     } else if (lane == 0) {
         const int s_sub = n < 5 ? n : 5;
         const int W0 = E >= 32 ? E - 32 : 0;
-        uint32_t R = leaf_word<T>(kind, m, c, hard, l01, l23, flag, src, 0) << (E - m - W0);
+        uint32_t R = leaf_word(kind, m, c, hard, l01, l23, flag, src, 0) << (E - m - W0);
         for (int s = t; s < s_sub; ++s) {
             const uint32_t sl = F.beta_row(s, get8(ib, s))[0];
             const int seg = 1 << s;
@@ -1130,6 +1175,7 @@ __global__ void __launch_bounds__(512, 1) k_lane(const __grid_constant__ LParams
     const int gsize = P.groups > 1 ? P.fpc / P.groups : P.fpc;
     const int gid = grp / gsize, gthreads = 32 * gsize;
     int o_start = (P.groups > 1 && gid == 1) ? P.n_ops / 2 : 0;
+    if (P.stagger) o_start = (o_start + (int)(((long long)blockIdx.x * P.n_ops) / gridDim.x)) % P.n_ops;
     long long f0 = (long long)blockIdx.x * P.fpc;
     while (f0 < batch) {
         const bool dummy = o_start > 0;

@@ -280,6 +280,15 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
             goff = align_up(goff + bytes, 256);
         }
     }
+    {
+        // hard words of Rate-1 / SPC leaves wider than 32 (read back by their survivors)
+        int mmax = 0;
+        for (int i = 0; i < n_ops; ++i)
+            if ((ops[i].kind == PB_OP_RATE1 || ops[i].kind == PB_OP_SPC) && ops[i].size > 32)
+                mmax = std::max(mmax, ops[i].size);
+        lay.hard_off = goff;
+        goff = align_up(goff + (mmax / 32) * 32 * 4, 256);
+    }
     lay.smem_bytes = align_up(off, 16);
     lay.gbytes = align_up(goff, 256);
     if (lay.smem_bytes > smem_cap) {
@@ -370,6 +379,7 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     lp->final_op = final_op;
     lp->fpc = fpc;
     lp->sync_mask = fpc > 1 ? env_int("PB_LANE_SYNC_MASK", 7) : -1;
+    lp->stagger = env_int("PB_LANE_STAGGER", 0);
     lp->groups = (fpc >= 4 && fpc % 2 == 0) ? std::max(1, std::min(2, env_int("PB_LANE_GROUPS", 1))) : 1;
     lp->lay = lay;
     std::copy(prog.begin(), prog.end(), lp->prog);
