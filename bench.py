@@ -156,6 +156,26 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def parse_opts(items):
+    """--opt key=value (repeatable) -> ListDecoder options (pb_options)."""
+    out = {}
+    for it in items or []:
+        k, _, v = it.partition("=")
+        out[k.strip()] = v.strip() if k.strip() == "kernel" else int(v)
+    return out
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -221,11 +241,13 @@ def run_reference(args):
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32" if mode == "f32" else "int8",
         "data": "synthetic (seeded BPSK-AWGN, reference per-frame Philox generator)",
-        "config": config_dict(args, spec, L, ebn0, mode, label, per_step),
+        "config": config_dict(args, spec, L, ebn0, mode, label, args.batch),
         "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": threads, "kind": "port",
-                         "sample": f"{per_step} frames/step x {args.steps} steps through "
-                                   f"oracle/libpolar_oracle.so (C restatement of "
-                                   f"polaris.listdec), {threads} threads"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"each step decodes a bounded sample of the workload's "
+                                   f"{args.batch}-frame batch: its first {per_step} frames "
+                                   f"(x {args.steps} steps) through oracle/libpolar_oracle.so (C "
+                                   f"restatement of polaris.listdec), {threads} threads"},
         "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -259,6 +281,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=6.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="decoder option key=value (pb_options: kernel, sync_every, ...)")
+    ap.add_argument("--no-latency", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -284,10 +309,11 @@ def main():
     pud = torch.empty(B, dtype=torch.int32, device=dev)
     invd = torch.empty(B, dtype=torch.uint8, device=dev)
     adaptive = args.config.endswith("_adaptive")
+    opts = parse_opts(args.opt)
     if adaptive:
-        dec = pb.AdaptiveDecoder(sch, L, mode=mode, device=local)
+        dec = pb.AdaptiveDecoder(sch, L, mode=mode, device=local, options=opts)
     else:
-        dec = pb.ListDecoder(sch, L, mode=mode, device=local)
+        dec = pb.ListDecoder(sch, L, mode=mode, device=local, options=opts)
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -329,6 +355,10 @@ def main():
     total_ms = float(tmax.item())
 
     # end to end through the public API: pinned host LLRs in, host results out
+    # (int8 mode: the fixed-point front end's int8 LLRs, a quarter of the bytes)
+    if mode == "int8":
+        llr_host = torch.from_numpy(pb.quantize_int8(frames.llrs)).pin_memory()
+    in_bytes = B * spec.N * (1 if mode == "int8" else 4)
     info_h = torch.empty((B, spec.k), dtype=torch.uint8).pin_memory()
     ok_h = torch.empty(B, dtype=torch.uint8).pin_memory()
     pm_h = torch.empty(B, dtype=torch.float64).pin_memory()
@@ -347,6 +377,34 @@ def main():
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e_t.item())
+
+    # single-frame latency (the paper's per-frame figure):
+    # one frame per launch, device-resident (CUDA events) and through decode()
+    latency = None
+    if rank == 0 and not args.no_latency:
+        one = llr_dev[:1].contiguous()
+        lat_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        dev_us, api_us = [], []
+        for i in range(60):
+            lat_ev[0].record(stream)
+            if adaptive:
+                dec.decode_device(one, info[:1], okd[:1], pmd[:1], pud[:1], invd[:1])
+            else:
+                dec.decode_device(one, info[:1], okd[:1], pmd[:1], pud[:1])
+            lat_ev[1].record(stream)
+            torch.cuda.synchronize(dev)
+            if i >= 10:
+                dev_us.append(1e3 * lat_ev[0].elapsed_time(lat_ev[1]))
+        host_one = frames.llrs[0] if mode == "f32" else pb.quantize_int8(frames.llrs[:1])[0]
+        for i in range(30):
+            t0 = time.perf_counter()
+            dec.decode(host_one)
+            if i >= 5:
+                api_us.append(1e6 * (time.perf_counter() - t0))
+        latency = {"frame_p50_us_device": statistics.median(dev_us),
+                   "frame_p50_us_e2e": statistics.median(api_us),
+                   "note": "one frame per launch; device: CUDA events around the decode kernel(s); "
+                           "e2e: ListDecoder.decode(llr) wall time incl. copies and launch"}
 
     if rank == 0:
         frames_all = B * world
@@ -386,7 +444,7 @@ def main():
             "fer": float(counters[1] / counters[0]), "ber": float(counters[2] / (counters[0] * spec.k)),
             "gpu_launches": int(launches),
             "e2e": {"value": frames_all * e2e_steps * spec.k / e2e_s / 1e9, "unit": "Gbit/s",
-                    "h2d_bytes_per_step": B * spec.N * 4,
+                    "h2d_bytes_per_step": in_bytes,
                     "d2h_bytes_per_step": B * (spec.k + 1 + 8 + 4 + (1 if adaptive else 0))},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Glane-op/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -395,12 +453,14 @@ def main():
                                       f"(sm_max_mhz, {peak_kind}); SURVEY 8(d) ALU-issue roofline",
                          "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / float(peaks.get("hbm_gbs", 6650.0))},
             "clocks": clocks.summary(),
+            "latency": latency,
+            "options": opts,
             "plan": json.loads((dec._list if adaptive else dec).plan),
         }
         if not args.no_cpu_baseline:
             rate, n, threads, dt = oracle_rate(sch, L, frames.llrs, mode, args.cpu_seconds, adaptive)
             line["cpu_baseline"] = {"value": rate / 1e9, "unit": "Gbit/s", "cores": threads,
-                                    "kind": "port",
+                                    "kind": "port", "cpu_model": cpu_model(),
                                     "sample": f"{n} frames of the same batch through "
                                               f"oracle/libpolar_oracle.so ({dt:.1f} s, "
                                               f"{threads} threads)"}

@@ -75,6 +75,25 @@ typedef struct pb_op {
 
 typedef struct pb_handle pb_handle;
 
+/* Explicit launch / planning options (no hidden global state: nothing is
+ * read from the environment).  Zero-initialise and set what you need; 0 in
+ * any field means "the measured default".  Pass NULL for all defaults. */
+typedef struct pb_options {
+    int32_t size;             /* sizeof(pb_options) (forward compatibility); 0 = this version */
+    int32_t kernel;           /* list kernel: 0 auto (lane-per-path kernel for L > 16 when its plan fits),
+                                 1 interpreted multi-shape kernel, 2 lane-per-path kernel (PB_EINVAL if it
+                                 cannot be planned) */
+    int32_t warps_per_frame;  /* interpreted kernel: warps per frame (1, 2, 4, 8; 0 = 1) */
+    int32_t frames_per_sm;    /* resident frames per SM target (0 = launch bound / 32, 16 for L > 16) */
+    int32_t sync_every;       /* CTA regroup period in ops (power of two; 0 = auto; -1 = never) */
+    int32_t recompute_stages; /* lane kernel: top stages recomputed from the channel (1 or 2; 0 = auto:
+                                 2 for float32, 1 for int8) */
+    int32_t chunk_frames;     /* host-buffer pipeline chunk in frames (0 = one wave of resident frames,
+                                 six for adaptive decoding) */
+    int32_t grid_sms;         /* use at most this many SMs (0 = all) */
+    int32_t l1_list_kernel;   /* 1: list size 1 through the list kernel instead of the single-path pass */
+} pb_options;
+
 /* Build a decoder for (code, schedule, list size) on a CUDA device.
  * Replaces ListDecoder.__init__ (listdec.py:171-185): validates the list size
  * (ValueError "list size X must be >= 1"), re-validates the op list against
@@ -85,6 +104,10 @@ typedef struct pb_handle pb_handle;
  * (identical results, ~30x faster than a one-path list decode). */
 int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
               int device, pb_handle **out);
+
+/* pb_create with explicit options (opts may be NULL = pb_create). */
+int pb_create_ex(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
+                 int device, const pb_options *opts, pb_handle **out);
 
 /* Decode `batch` frames.  Replaces ListDecoder.decode (listdec.py:289-308),
  * batched.  llr: [batch][N] of in_type.  Outputs (each may be NULL):

@@ -27,7 +27,7 @@ PB_OK, PB_EINVAL, PB_ECUDA, PB_EINTERNAL, PB_ENOMEM = 0, -1, -2, -3, -4
 PB_MODE_F32, PB_MODE_INT8 = 0, 1
 PB_IN_F32, PB_IN_I8 = 0, 1
 
-EXPORTS = ("pb_create", "pb_decode", "pb_decode_paths", "pb_decode_adaptive", "pb_fastssc",
+EXPORTS = ("pb_create", "pb_create_ex", "pb_decode", "pb_decode_paths", "pb_decode_adaptive", "pb_fastssc",
            "pb_generate_frames", "pb_count_errors",
            "pb_destroy", "pb_last_error",
            "pb_plan_json", "pb_launch_count", "pb_last_kernel_ms", "pb_version")
@@ -39,6 +39,29 @@ class PbCode(ctypes.Structure):
                 ("crc_width", ctypes.c_int32), ("crc_poly", ctypes.c_uint32),
                 ("crc_init", ctypes.c_uint32), ("crc_reflect", ctypes.c_int32),
                 ("crc_xor_out", ctypes.c_uint32)]
+
+
+class PbOptions(ctypes.Structure):
+    """pb_options (include/polar_b200.h): explicit planning / launch options,
+    0 = the measured default."""
+    _fields_ = [("size", ctypes.c_int32), ("kernel", ctypes.c_int32),
+                ("warps_per_frame", ctypes.c_int32), ("frames_per_sm", ctypes.c_int32),
+                ("sync_every", ctypes.c_int32), ("recompute_stages", ctypes.c_int32),
+                ("chunk_frames", ctypes.c_int32), ("grid_sms", ctypes.c_int32),
+                ("l1_list_kernel", ctypes.c_int32)]
+
+    @classmethod
+    def from_dict(cls, d):
+        o = cls()
+        o.size = ctypes.sizeof(cls)
+        names = {f for f, _ in cls._fields_} - {"size"}
+        for k, v in (d or {}).items():
+            if k not in names:
+                raise ValueError(f"unknown decoder option {k!r} (one of {sorted(names)})")
+            if k == "kernel" and isinstance(v, str):
+                v = {"auto": 0, "interpreted": 1, "lane": 2}[v]
+            setattr(o, k, int(v))
+        return o
 
 
 class PbOp(ctypes.Structure):
@@ -151,6 +174,9 @@ def lib():
     L.pb_create.restype = i32
     L.pb_create.argtypes = [ctypes.POINTER(PbCode), ctypes.POINTER(PbOp), i32, i32, i32, i32,
                             ctypes.POINTER(vp)]
+    L.pb_create_ex.restype = i32
+    L.pb_create_ex.argtypes = [ctypes.POINTER(PbCode), ctypes.POINTER(PbOp), i32, i32, i32, i32,
+                               ctypes.POINTER(PbOptions), ctypes.POINTER(vp)]
     L.pb_decode.restype = i32
     L.pb_decode.argtypes = [vp, vp, i32, i64, vp, vp, vp, vp, vp]
     L.pb_decode_paths.restype = i32

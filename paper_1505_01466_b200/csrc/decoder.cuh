@@ -186,8 +186,6 @@ struct LParams {
     const int32_t *frame_map;
     const int32_t *batch_dev;
     int fpc;
-    int groups;                 // frame groups per CTA (1 or 2: the second starts half a program late)
-    int stagger;                // CTA b starts (b / grid) of a program late (spreads the SMs' op mix)
     int sync_mask;
     long long *op_cycles;       // profiling build: clock64 at the start of each op (CTA 0, frame slot 0), or null
     LLayout lay;

@@ -1096,23 +1096,13 @@ __device__ __forceinline__ void load_channel_lane(const LParams &P, T *ch, long 
     }
 }
 
-// barrier over this frame's group of the CTA (all frames: bar 0; 2 groups:
-// named barriers 1 / 2)
-__device__ __forceinline__ void group_sync(int gid, int nthreads, bool whole) {
-    if (whole)
-        __syncthreads();
-    else
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + gid), "r"(nthreads) : "memory");
-}
-
 template <typename T>
-__device__ __forceinline__ void run_ops(Fr<T> &F, int &np, int o0, int o1, int gid, int gthreads) {
+__device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
     const LParams &P = F.P;
-    const bool whole = P.groups <= 1;
 #if PB_PROFILE
     const bool prof = P.op_cycles && blockIdx.x == 0 && threadIdx.x == 0;
 #endif
-    for (int oi = o0; oi < o1; ++oi) {
+    for (int oi = 0; oi < P.n_ops; ++oi) {
 #if PB_PROFILE
         if (prof) P.op_cycles[oi] = clock64();
         F.marks = prof ? P.op_cycles + P.n_ops + 1 + 4 * oi : nullptr;
@@ -1150,7 +1140,7 @@ __device__ __forceinline__ void run_ops(Fr<T> &F, int &np, int o0, int o1, int g
                 break;
         }
         if (P.sync_mask >= 0 && (oi & P.sync_mask) == 0)
-            group_sync(gid, gthreads, whole);  // regroup the frames (shared instruction fetch)
+            __syncthreads();  // regroup the CTA's frames (shared instruction fetch)
         else
             __syncwarp();
     }
@@ -1169,31 +1159,21 @@ __global__ void __launch_bounds__(512, 1) k_lane(const __grid_constant__ LParams
     unsigned char *sm = lk_smem + (size_t)grp * P.lay.smem_bytes;
     const long long stride = (long long)gridDim.x * P.fpc;
     const long long batch = P.batch_dev ? (long long)*P.batch_dev : P.batch;
-    // frame groups: with two, the second starts half a program late (its
-    // first pass runs the second half of the ops on a throwaway frame) so the
-    // groups' op mixes interleave on the SM; each group keeps its frames in step
-    const int gsize = P.groups > 1 ? P.fpc / P.groups : P.fpc;
-    const int gid = grp / gsize, gthreads = 32 * gsize;
-    int o_start = (P.groups > 1 && gid == 1) ? P.n_ops / 2 : 0;
-    if (P.stagger) o_start = (o_start + (int)(((long long)blockIdx.x * P.n_ops) / gridDim.x)) % P.n_ops;
-    long long f0 = (long long)blockIdx.x * P.fpc;
-    while (f0 < batch) {
-        const bool dummy = o_start > 0;
+    // (measured and dropped: a second frame group per CTA started half a
+    // program late, and CTAs started at staggered ops: +2 % / -2 % device
+    // rate, both costing a throwaway half frame per launch)
+    for (long long f0 = (long long)blockIdx.x * P.fpc; f0 < batch; f0 += stride) {
         // tail: idle slots decode the last frame again and write nothing
         const long long fi = f0 + grp < batch ? f0 + grp : batch - 1;
         const long long f = P.frame_map ? (long long)P.frame_map[fi] : fi;
-        const bool own = f0 + grp < batch && !dummy;
+        const bool own = f0 + grp < batch;
         Fr<T> F(P, sm, gs);
-        if (!dummy) load_channel_lane<T>(P, F.channel(), f, lane);
+        load_channel_lane<T>(P, F.channel(), f, lane);
         __syncwarp();
         int np = 1;
-        run_ops(F, np, o_start, P.n_ops, gid, gthreads);
+        run_ops(F, np);
         if (own) finalize(F, f, np);
-        if (P.fpc > 1) group_sync(gid, gthreads, P.groups <= 1);
-        if (dummy)
-            o_start = 0;
-        else
-            f0 += stride;
+        if (P.fpc > 1) __syncthreads();
     }
 }
 
@@ -1202,7 +1182,10 @@ template <typename T>
 cudaError_t lane_launch_t(const LParams *p, int grid, size_t smem, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k_lane<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_lane<T><<<grid, 32 * p->fpc, smem, st>>>(*p);
+    // a batch smaller than one CTA's frame slots runs only the warps it needs
+    // (single-frame latency: the frame's warp does not share the SM)
+    const int warps = grid == 1 && p->batch < p->fpc && !p->batch_dev ? (int)p->batch : p->fpc;
+    k_lane<T><<<grid, 32 * warps, smem, st>>>(*p);
     return cudaGetLastError();
 }
 template <typename T>

@@ -133,6 +133,7 @@ struct pb_handle {
     unsigned char *d_ssc_ch = nullptr;
     int32_t *d_fail = nullptr;   // adaptive: failing frame indices + per-chunk counts
     size_t d_fail_cap = 0;
+    int chunk_frames = 0;           // pb_options::chunk_frames
     // lane-per-path list kernel (lane_kernel.cuh), L in 17..32
     bool lane = false;
     pb::lk::LParams *lp = nullptr;  // host copy of the launch parameters (IO fields per call)
@@ -157,9 +158,30 @@ bool is_device_ptr(const void *p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
+// options of the handle being created (pb_options, zero = default)
+struct Opts {
+    int kernel = 0, warps = 0, fps = 0, sync_every = 0, recompute = 0, chunk = 0, grid_sms = 0, l1_list = 0;
+};
+Opts read_opts(const pb_options *o) {
+    Opts r;
+    if (!o) return r;
+    r.kernel = o->kernel;
+    r.warps = o->warps_per_frame;
+    r.fps = o->frames_per_sm;
+    r.sync_every = o->sync_every;
+    r.recompute = o->recompute_stages;
+    r.chunk = o->chunk_frames;
+    r.grid_sms = o->grid_sms;
+    r.l1_list = o->l1_list_kernel;
+    return r;
+}
+// sync_every (ops, power of two) -> the kernels' barrier mask; dflt = mask
+int sync_mask_of(int every, int dflt) {
+    if (every < 0) return -1;
+    if (every == 0) return dflt;
+    int p = 1;
+    while (p < every) p <<= 1;
+    return p - 1;
 }
 
 // grammar walk: node(lo, hi, side) := leaf | F node(lo,mid,0) G node(mid,hi,1) Combine
@@ -223,13 +245,14 @@ int align_up(int x, int a) { return (x + a - 1) / a * a; }
 // kernel is used) when the plan does not fit.
 static bool is_leaf_kind(int k) { return k == PB_OP_RATE0 || k == PB_OP_RATE1 || k == PB_OP_REP || k == PB_OP_SPC; }
 
-static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vector<pb::DOp> &dprog, std::string &why) {
+static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vector<pb::DOp> &dprog, const Opts &opt,
+                      std::string &why) {
     using namespace pb::lk;
     const int N = h->N, n = h->n, L = h->L, mode = h->mode;
     const int es = mode == PB_MODE_F32 ? 4 : 1;
     // measured (c3 L=32): float32 3.09 Gbit/s with n-2 recomputed vs 2.86 stored;
     // int8 3.53 stored vs 2.89 recomputed (small rows, costly conversions)
-    const int NV = n >= 2 ? std::max(1, std::min(2, env_int("PB_LANE_NV", mode == PB_MODE_F32 ? 2 : 1))) : 1;
+    const int NV = n >= 2 ? std::max(1, std::min(2, opt.recompute ? opt.recompute : (mode == PB_MODE_F32 ? 2 : 1))) : 1;
     auto virt = [&](int s) { return s < n && s >= n - NV; };
     if ((int)dprog.size() > kMaxOps) {
         why = "op program too long";
@@ -241,7 +264,7 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
             staged[ops[i].stage - 1] = true;
     LLayout lay{};
     const int smem_cap = 227 * 1024;
-    const int target_fps = std::max(1, env_int("PB_LANE_FPS", 16));
+    const int target_fps = std::max(1, opt.fps ? opt.fps : 16);
     const int budget = smem_cap / target_fps / 16 * 16;
     int off = 0, goff = 0;
     lay.ch_off = 0;
@@ -252,7 +275,7 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     off += 256;
     lay.root_off = off;
     off = align_up(off + std::max(1, N / 32) * 4, 16);
-    const int b_sm = env_int("PB_LANE_BETA_SM", 6);
+    const int b_sm = 6;  // beta slots 0..5 in shared memory (1 word per row)
     for (int s = 0; s < n; ++s) {
         const int words = std::max(1, (1 << s) / 32);
         lay.b_stride[s] = words > 1 ? words + 1 : 1;
@@ -378,9 +401,8 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     lp->n_ops = (int)prog.size();
     lp->final_op = final_op;
     lp->fpc = fpc;
-    lp->sync_mask = fpc > 1 ? env_int("PB_LANE_SYNC_MASK", 7) : -1;
-    lp->stagger = env_int("PB_LANE_STAGGER", 0);
-    lp->groups = (fpc >= 4 && fpc % 2 == 0) ? std::max(1, std::min(2, env_int("PB_LANE_GROUPS", 1))) : 1;
+    // regroup every 8 ops (measured c3 L=32: every 8 3.23, 32 3.09, 4 3.12, never 2.46 Gbit/s)
+    lp->sync_mask = fpc > 1 ? sync_mask_of(opt.sync_every, 7) : -1;
     lp->lay = lay;
     std::copy(prog.begin(), prog.end(), lp->prog);
     h->lp = lp;
@@ -409,7 +431,17 @@ int pb_version(void) { return PB_API_VERSION; }
 
 int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode, int device,
               pb_handle **out) {
+    return pb_create_ex(code, ops, n_ops, list_size, mode, device, nullptr, out);
+}
+
+int pb_create_ex(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode, int device,
+                 const pb_options *opts, pb_handle **out) {
     g_err.clear();
+    const Opts opt = read_opts(opts);
+    if (opt.kernel < 0 || opt.kernel > 2) return fail(PB_EINVAL, "pb_options.kernel must be 0, 1 or 2");
+    if (opt.warps != 0 && opt.warps != 1 && opt.warps != 2 && opt.warps != 4 && opt.warps != 8)
+        return fail(PB_EINVAL, "pb_options.warps_per_frame must be 1, 2, 4 or 8");
+    if (opt.recompute < 0 || opt.recompute > 2) return fail(PB_EINVAL, "pb_options.recompute_stages must be 0, 1 or 2");
     if (!out || !code || !ops) return fail(PB_EINVAL, "null argument");
     *out = nullptr;
     if (list_size < 1) return fail(PB_EINVAL, "list size " + std::to_string(list_size) + " must be >= 1");
@@ -437,6 +469,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     }
 
     pb_handle *h = new pb_handle();
+    h->chunk_frames = opt.chunk;
     h->device = device;
     h->mode = mode;
     h->L = list_size;
@@ -525,7 +558,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     // ---- storage plan
     const int es = mode == PB_MODE_F32 ? 4 : 1;
     // frame shape: W warps per frame, PPW (power of two) path slots per warp
-    int warps = env_int("PB_WARPS", 1);
+    int warps = opt.warps ? opt.warps : 1;
     auto shape_ppw = [&](int wv) {
         int p = 1;
         while (p * wv < L) p <<= 1;
@@ -550,7 +583,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     }
     const int smem_cap = 227 * 1024;
     // resident frames per SM: one warp each, up to the launch bound
-    const int target_fps = std::max(1, env_int("PB_FRAMES_PER_SM", pb::shape_max_threads(warps, ppw) / 32));
+    const int target_fps = std::max(1, opt.fps ? opt.fps : pb::shape_max_threads(warps, ppw) / 32);
     // Per-frame layout for a channel in shared memory or in global scratch.
     auto plan_layout = [&](bool chg, pb::FrameLayout &lay) {
         lay = pb::FrameLayout{};
@@ -564,7 +597,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         // (PB_BETA_GLOBAL_FROM) to leave shared memory to more frames
         // (measured: slots >= 6 global for c3 / c5 / int8 at 16 frames per SM;
         // the freed shared memory also grows the L1 that caches the global rows)
-        lay.b_gfrom = std::min(n, std::max(1, env_int("PB_BETA_GLOBAL_FROM", 6)));
+        lay.b_gfrom = std::min(n, 6);
         for (int s = 0; s < n; ++s) {
             int words = std::max(1, (1 << s) / 32);
             lay.b_stride[s] = words > 1 ? words + 1 : 1;
@@ -602,7 +635,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         lay.root_off = off;
         off = align_up(off + lay.root_words * 4, 16);
 
-        const int budget = std::max(off, env_int("PB_SMEM_BUDGET", smem_cap / target_fps - 1024));
+        const int budget = std::max(off, smem_cap / target_fps - 1024);
         // alpha stages s = 0 .. n-2 (n-1 is recomputed), lowest stages first into
         // shared memory, the rest into per-frame global scratch (L2-resident)
         int s_global = n - 1;
@@ -633,9 +666,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         plan_layout(false, ls);
         plan_layout(true, lg);
         auto fps_of = [&](const pb::FrameLayout &l) { return std::min(target_fps, smem_cap / std::max(1, l.smem_bytes)); };
-        const int chg_env = env_int("PB_CH_GLOBAL", -1);
         bool chg = fps_of(lg) > fps_of(ls) || (fps_of(lg) == fps_of(ls) && lg.a_gfrom > ls.a_gfrom);
-        if (chg_env >= 0) chg = chg_env != 0;
         chg = chg && pb_shape_supported(mode, warps, ppw, 1);
         h->chg = chg;
         lay = chg ? lg : ls;
@@ -652,7 +683,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     // leaf's LLRs) is skipped -- one op, one row store and one row load fewer
     // per leaf.  Stage n-1 parents are recomputed from the channel and
     // global-scratch parents keep their F / G.
-    if (mode == PB_MODE_INT8 && env_int("PB_FUSE_LEAF", 1) != 0) {
+    if (mode == PB_MODE_INT8) {
         for (size_t i = 1; i < h->prog.size(); ++i) {
             pb::DOp &d = h->prog[i], &pf = h->prog[i - 1];
             const bool leaf = d.kind == pb::DK_R0 || d.kind == pb::DK_REP || d.kind == pb::DK_R1 || d.kind == pb::DK_SPC;
@@ -683,7 +714,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         pr.prog_smem = 0;
         // measured (same-box A/B): +3 % c3 L=32, +4 % c5 L=16, +1 % int8
         // L=32 over a global-memory program; -4 % at 8 paths per warp (c3 L=8)
-        pr.prog_inline = (int)h->prog.size() <= pb::kInlineOps && env_int("PB_PROG_PARAM", ppw >= 16 ? 1 : 0) != 0;
+        pr.prog_inline = (int)h->prog.size() <= pb::kInlineOps && ppw >= 16;
         if (pr.prog_inline) std::copy(h->prog.begin(), h->prog.end(), pr.iprog);
     }
     cudaError_t e = cudaSetDevice(device);
@@ -692,7 +723,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         return cuda_fail(e, "cudaSetDevice");
     }
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
-    if (env_int("PB_GRID_SMS", 0) > 0) h->sms = std::min(h->sms, env_int("PB_GRID_SMS", 0));  // experiments
+    if (opt.grid_sms > 0) h->sms = std::min(h->sms, opt.grid_sms);
     e = pb_occupancy(mode, h->warps, h->ppw, h->chg, h->smem_frame, 1, &h->blocks_per_sm);
     if (e != cudaSuccess || h->blocks_per_sm < 1) {
         delete h;
@@ -705,8 +736,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     // (measured: no_instructions stalls 8.7% -> 16.5%, -25% throughput).
     // (A CTA barrier after every op to force lockstep measured slower.)
     {
-        const int fpc_env = env_int("PB_FPC", 0);
-        int fpc = std::min(fpc_env > 0 ? fpc_env : h->blocks_per_sm, pb::shape_max_threads(h->warps, h->ppw) / 32 / h->warps);  // launch bound
+        int fpc = std::min(h->blocks_per_sm, pb::shape_max_threads(h->warps, h->ppw) / 32 / h->warps);  // launch bound
         while (fpc > 1 && (size_t)fpc * h->smem_frame > (size_t)smem_cap) --fpc;
         int bps = 0;
         while (fpc > 1) {
@@ -719,16 +749,8 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         h->blocks_per_sm = bps;
     }
     h->grid = h->sms * h->blocks_per_sm;
-    // op program staged in shared memory (PB_PROG_SMEM=1): measured neutral at
-    // L=32 and -10 % at L=8 (less L1), so the program is read through L1 by default
-    if (env_int("PB_PROG_SMEM", 0) && h->blocks_per_sm == 1 &&
-        h->fpc * h->smem_frame + sizeof(pb::DOp) * h->prog.size() <= (size_t)smem_cap) {
-        int bps2 = 0;
-        const size_t tot = h->fpc * h->smem_frame + sizeof(pb::DOp) * h->prog.size();
-        if (pb_occupancy(mode, h->warps, h->ppw, h->chg, tot, h->fpc, &bps2) == cudaSuccess && bps2 >= 1)
-            h->prog_smem = sizeof(pb::DOp) * h->prog.size();
-        cudaGetLastError();
-    }
+    // (the op program is read through L1 / the constant bank; staging it in
+    // shared memory measured neutral at L=32 and -10 % at L=8)
 
     // ---- single-path pass plan (k_ssc): one warp per frame, up to
     // PB_SSC_MAXT/32 frames per CTA; the channel goes to global scratch when
@@ -754,11 +776,9 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
         };
         const int maxf = PB_SSC_MAXT / 32;
         const int fs = plan(false), fg = plan(true);
-        const int chg_env = env_int("PB_SSC_CH_GLOBAL", -1);
-        bool chg = std::min(maxf, smem_cap / std::max(1, fg)) > std::min(maxf, smem_cap / std::max(1, fs));
-        if (chg_env >= 0) chg = chg_env != 0;
+        const bool chg = std::min(maxf, smem_cap / std::max(1, fg)) > std::min(maxf, smem_cap / std::max(1, fs));
         const int off = plan(chg);
-        int sfpc = std::min(std::min(maxf, env_int("PB_SSC_FPC", maxf)), smem_cap / std::max(1, off));
+        int sfpc = std::min(maxf, smem_cap / std::max(1, off));
         int bps = 0;
         while (sfpc >= 1) {
             if (pb_occupancy_ssc(mode, sfpc, off, &bps) == cudaSuccess && bps >= 1) break;
@@ -771,7 +791,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
             h->ssc_grid = h->sms * bps;
             h->ssc_chg = chg;
         }
-        h->l1_ssc = h->ssc_ok && L == 1 && env_int("PB_L1_LIST", 0) == 0;
+        h->l1_ssc = h->ssc_ok && L == 1 && !opt.l1_list;
     }
 
     // ---- device tables
@@ -848,7 +868,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     pr.final_op = final_op;
     pr.gscratch = h->d_scratch;
     pr.op_cycles = nullptr;
-    pr.ablate = env_int("PB_ABLATE", 0);
+    pr.ablate = 0;
     pr.fpc = h->fpc;
     pr.prog_smem = h->prog_smem ? 1 : 0;
     // The CTA's frames drift apart op by op (data-dependent selection and
@@ -856,7 +876,7 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     // CTA barrier every 32 ops regroups them.  Measured: +30% for L >= 16
     // (c3 L=32 1.40 -> 1.82, int8 1.51 -> 1.99, c5 1.48 -> 1.93 Gbit/s), a
     // slight loss for the short per-op code of L <= 8.
-    pr.sync_mask = h->fpc > 1 ? env_int("PB_SYNC_MASK", h->ppw * h->warps >= 16 ? 31 : -1) : -1;
+    pr.sync_mask = h->fpc > 1 ? sync_mask_of(opt.sync_every, h->ppw * h->warps >= 16 ? 31 : -1) : -1;
 
     {
         pb::SscParams &sp = h->ssc;
@@ -873,8 +893,18 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
     }
 
     std::string lane_why = "list size <= 16";
-    if (L > 16 && h->warps == 1 && env_int("PB_LANE", 1) != 0) plan_lane(h, ops, n_ops, h->prog, lane_why);
-    if (env_int("PB_LANE", 1) == 0) lane_why = "disabled";
+    if (opt.kernel == 1) {
+        lane_why = "interpreted kernel requested";
+    } else if ((L > 16 || opt.kernel == 2) && h->warps == 1) {
+        plan_lane(h, ops, n_ops, h->prog, opt, lane_why);
+    } else if (h->warps != 1) {
+        lane_why = "several warps per frame requested";
+    }
+    if (opt.kernel == 2 && !h->lane) {
+        const std::string why = lane_why;
+        pb_destroy(h);
+        return fail(PB_EINVAL, "lane-per-path kernel unavailable: " + why);
+    }
 
     char buf[1024];
     snprintf(buf, sizeof buf,
@@ -1221,7 +1251,9 @@ int decode_impl(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8
     // (adaptive decoding: 6 waves, so each chunk's list pass over its few
     // CRC failures amortises its launch and its grid-wide occupancy)
     const long long chunk = std::max<long long>(
-        1, env_int("PB_CHUNK_FRAMES", std::max(2048, (adaptive ? 6 : 1) * h->grid * h->fpc)));
+        1, h->chunk_frames > 0 ? (long long)h->chunk_frames
+                               : (long long)std::max(2048, (adaptive ? 6 : 1) * (h->lane ? h->lane_grid * h->lane_fpc
+                                                                                       : h->grid * h->fpc)));
     if (!dev_in && batch > chunk)
         return decode_pipelined(h, h->base, llr, in_type, in_es, batch, chunk, info_out, crc_ok, pm_out, paths_used,
                                 invoked, adaptive, st);

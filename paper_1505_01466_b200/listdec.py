@@ -176,10 +176,16 @@ class ListDecoder:
         as int8), saturating G, integer metrics (BASELINE config 4).
     device : int
         CUDA device ordinal.
+    options : dict, optional
+        Explicit planning / launch options (``pb_options`` of the C ABI):
+        ``kernel`` ("auto" | "interpreted" | "lane"), ``warps_per_frame``,
+        ``frames_per_sm``, ``sync_every``, ``recompute_stages``,
+        ``chunk_frames``, ``grid_sms``, ``l1_list_kernel``; omitted = the
+        measured defaults.  Nothing is read from the environment.
     """
 
     def __init__(self, schedule: Schedule, list_size: int, *, mode: str = "f32",
-                 device: int = 0):
+                 device: int = 0, options: dict | None = None):
         if list_size < 1:
             raise ValueError(f"list size {list_size} must be >= 1")
         if mode not in ("f32", "int8"):
@@ -202,10 +208,12 @@ class ListDecoder:
         ops = (_native.PbOp * max(1, len(arr)))()
         for i, row in enumerate(arr.tolist()):
             ops[i] = _native.PbOp(*row)
+        self.options = dict(options or {})
+        opts = _native.PbOptions.from_dict(self.options)
         handle = ctypes.c_void_p()
-        rc = lib.pb_create(ctypes.byref(code), ops, len(arr), self.list_size,
-                           _native.PB_MODE_F32 if mode == "f32" else _native.PB_MODE_INT8,
-                           self.device, ctypes.byref(handle))
+        rc = lib.pb_create_ex(ctypes.byref(code), ops, len(arr), self.list_size,
+                              _native.PB_MODE_F32 if mode == "f32" else _native.PB_MODE_INT8,
+                              self.device, ctypes.byref(opts), ctypes.byref(handle))
         _native.check(rc, "pb_create")
         self._h = handle
 
@@ -380,12 +388,12 @@ class AdaptiveDecoder:
     """
 
     def __init__(self, schedule: Schedule, list_size: int, *, mode: str = "f32",
-                 device: int = 0):
+                 device: int = 0, options: dict | None = None):
         if schedule.spec.crc is None:
             raise ValueError("adaptive decoding needs a CRC in the code spec")
         self.schedule = schedule
         self.list_size = list_size
-        self._list = ListDecoder(schedule, list_size, mode=mode, device=device)
+        self._list = ListDecoder(schedule, list_size, mode=mode, device=device, options=options)
         self.spec = schedule.spec
 
     @property

@@ -10,7 +10,7 @@ recorded outputs and the CPU oracle.
   host buffers (single and pipelined chunks) and device tensors.
 * ``ListDecoder(schedule, 1)`` routes through k_ssc with the list decoder's
   leaf rules: bit-exact against the oracle's L=1 list decode and against the
-  list kernel itself (PB_L1_LIST=1).
+  list kernel itself (options l1_list_kernel=1).
 """
 
 import os
@@ -112,11 +112,8 @@ def test_adaptive_pipelined_and_device_paths_agree():
     fb = pb.generate_frames(spec, 2.0, seed=5, start=0, count=6000)
     dec = pb.AdaptiveDecoder(sch, 8)
     whole = dec.decode_batch(fb.llrs)
-    os.environ["PB_CHUNK_FRAMES"] = "1000"
-    try:
-        chunked = dec.decode_batch(torch.from_numpy(fb.llrs).pin_memory())
-    finally:
-        del os.environ["PB_CHUNK_FRAMES"]
+    chunked = pb.AdaptiveDecoder(sch, 8, options={"chunk_frames": 1000}).decode_batch(
+        torch.from_numpy(fb.llrs).pin_memory())
     _same(chunked, whole, "pipelined")
     assert np.array_equal(chunked.invoked_list, whole.invoked_list)
     x = torch.from_numpy(fb.llrs).cuda()
@@ -152,10 +149,6 @@ def test_list_of_one_through_ssc_vs_oracle_and_list_kernel(code, mode):
     got = dec.decode_batch(feed)
     ref = oracle.decode_batch(sch, 1, feed.astype(np.float32), int8=(mode == "int8"), threads=4)
     _same(got, ref, "ssc L=1 vs oracle")
-    os.environ["PB_L1_LIST"] = "1"
-    try:
-        lk = pb.ListDecoder(sch, 1, mode=mode)
-    finally:
-        del os.environ["PB_L1_LIST"]
+    lk = pb.ListDecoder(sch, 1, mode=mode, options={"l1_list_kernel": 1})
     assert '"l1_decodes": 0' in lk.plan
     _same(lk.decode_batch(feed), got, "list kernel L=1 vs ssc")

@@ -127,12 +127,11 @@ def test_several_handles_coexist(c1):
     assert plan["L"] == 8 and plan["smem_per_frame"] > 0
 
 
-@pytest.mark.parametrize("warps", ["1", "2", "4", "8"])
-def test_warp_shapes_agree(c1, warps, monkeypatch):
+@pytest.mark.parametrize("warps", [1, 2, 4, 8])
+def test_warp_shapes_agree(c1, warps):
     spec, sch, fb = c1
-    monkeypatch.setenv("PB_WARPS", warps)
     for L in (8, 32):
-        d = pb.ListDecoder(sch, L)
+        d = pb.ListDecoder(sch, L, options={"warps_per_frame": warps})
         r = d.decode_batch(fb.llrs[:96])
         o = oracle.decode_batch(sch, L, fb.llrs[:96])
         assert np.array_equal(r.info_bits, o.info_bits)
@@ -140,14 +139,13 @@ def test_warp_shapes_agree(c1, warps, monkeypatch):
 
 
 @pytest.mark.parametrize("pinned", [False, True])
-def test_chunked_host_pipeline_matches_device_call(c1, monkeypatch, pinned):
-    """Host-buffer batches above PB_CHUNK_FRAMES run chunked over two streams;
+def test_chunked_host_pipeline_matches_device_call(c1, pinned):
+    """Host-buffer batches above the chunk size run chunked over two streams;
     results must equal the single-launch call, ragged tail included."""
     import torch
     spec, sch, fb = c1
-    dec = pb.ListDecoder(sch, 4)
-    ref = dec.decode_batch(fb.llrs)                 # below the chunk size: one launch
-    monkeypatch.setenv("PB_CHUNK_FRAMES", "70")   # 300 frames -> 5 chunks, last one ragged
+    ref = pb.ListDecoder(sch, 4).decode_batch(fb.llrs)   # below the chunk size: one launch
+    dec = pb.ListDecoder(sch, 4, options={"chunk_frames": 70})  # 300 frames -> 5 chunks, last ragged
     llr = torch.from_numpy(fb.llrs).pin_memory() if pinned else fb.llrs
     launches = dec.launches
     got = dec.decode_batch(llr)
@@ -157,7 +155,7 @@ def test_chunked_host_pipeline_matches_device_call(c1, monkeypatch, pinned):
         assert np.array_equal(np.asarray(a), np.asarray(b))
 
 
-def test_pinned_pipeline_with_global_scratch_matches_device_call(monkeypatch):
+def test_pinned_pipeline_with_global_scratch_matches_device_call():
     """pinned host buffers in AND out, several chunks, a
     config whose frames use global scratch (c3 L=32): the chunks' kernels
     must not share the handle's scratch concurrently."""
@@ -175,7 +173,7 @@ def test_pinned_pipeline_with_global_scratch_matches_device_call(monkeypatch):
     dpu = torch.empty(B, dtype=torch.int32, device="cuda")
     dec.decode_device(x, dinfo, dok, dpm, dpu)
     torch.cuda.synchronize()
-    monkeypatch.setenv("PB_CHUNK_FRAMES", "700")   # 5 chunks, ragged tail
+    dec = pb.ListDecoder(sch, 32, options={"chunk_frames": 700})   # 5 chunks, ragged tail
     llr_h = torch.from_numpy(fb.llrs).pin_memory()
     out = pb.BatchResult(torch.empty((B, k), dtype=torch.uint8).pin_memory(),
                          torch.empty(B, dtype=torch.uint8).pin_memory(),
@@ -232,3 +230,34 @@ def test_output_buffers_are_validated(c1):
         dec.decode_device(x, torch.empty((B, k), dtype=torch.uint8))
     with pytest.raises(ValueError, match="paths_used"):
         dec.decode_device(x, paths_used=torch.empty(B, dtype=torch.int64, device="cuda"))
+
+
+@pytest.mark.parametrize("cfg", [(2048, 1691, 32, "f32"), (2048, 1691, 32, "int8"), (1024, 828, 20, "f32"),
+                                 (8192, 6112, 24, "f32")], ids=str)
+def test_lane_kernel_and_interpreted_kernel_are_twins(cfg):
+    """The lane-per-path kernel (default for L > 16) and the interpreted
+    multi-shape kernel decode identically (both bit-exact vs the oracle)."""
+    import json
+    N, k, L, mode = cfg
+    spec = pb.CodeSpec.from_design_ebn0(N, k, pb.CRC32, 3.5)
+    sch = pb.build_schedule(spec)
+    fb = pb.generate_frames(spec, 3.0, seed=N + L, start=0, count=600 if N <= 2048 else 160)
+    lane = pb.ListDecoder(sch, L, mode=mode, options={"kernel": "lane"})
+    interp = pb.ListDecoder(sch, L, mode=mode, options={"kernel": "interpreted"})
+    assert json.loads(lane.plan)["lane_kernel"] is not None
+    assert json.loads(interp.plan)["lane_kernel"] is None
+    a, b = lane.decode_batch(fb.llrs), interp.decode_batch(fb.llrs)
+    for x, y in ((a.info_bits, b.info_bits), (a.crc_ok, b.crc_ok), (a.chosen_pm, b.chosen_pm),
+                 (a.paths_used, b.paths_used)):
+        assert np.array_equal(x, y)
+    for opt in ({"recompute_stages": 1}, {"sync_every": -1}, {"frames_per_sm": 8}):
+        c = pb.ListDecoder(sch, L, mode=mode, options=dict(opt, kernel="lane")).decode_batch(fb.llrs[:200])
+        assert np.array_equal(c.info_bits, a.info_bits[:200]) and np.array_equal(c.chosen_pm, a.chosen_pm[:200])
+
+
+def test_bad_options_are_rejected(c1):
+    spec, sch, fb = c1
+    with pytest.raises(ValueError, match="unknown decoder option"):
+        pb.ListDecoder(sch, 4, options={"warps": 2})
+    with pytest.raises(ValueError, match="warps_per_frame"):
+        pb.ListDecoder(sch, 4, options={"warps_per_frame": 3})
