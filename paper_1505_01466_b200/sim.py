@@ -106,72 +106,109 @@ class DeviceFrames:
         _native.check(rc, "pb_count_errors")
 
 
-def _point(dec, schedule, adaptive, snr, min_errors, max_frames, seed, workers, chunk_size, frames,
+class _Worker:
+    """One device's decoder and buffers for super-batches of B frames."""
+
+    def __init__(self, dec, spec, adaptive, B, chunks_per_batch, frames, mode):
+        import torch
+        self.dec, self.spec, self.adaptive = dec, spec, adaptive
+        base = dec._list if adaptive else dec
+        self.dev = torch.device("cuda", base.device)
+        dev = self.dev
+        k = spec.k
+        if frames == "device":
+            self.src = DeviceFrames(base)
+            self.llr = torch.empty((B, spec.N), dtype=torch.int8 if mode == "int8" else torch.float32, device=dev)
+            self.pay = torch.empty((B, self.src.kw), dtype=torch.int32, device=dev)
+            self.counts = torch.zeros((chunks_per_batch, 3), dtype=torch.int64, device=dev)
+        self.info = torch.empty((B, k), dtype=torch.uint8, device=dev)
+        self.ok = torch.empty(B, dtype=torch.uint8, device=dev)
+        self.pm = torch.empty(B, dtype=torch.float64, device=dev)
+        self.pu = torch.empty(B, dtype=torch.int32, device=dev)
+        self.inv = torch.empty(B, dtype=torch.uint8, device=dev)
+        with torch.cuda.device(dev):
+            self.stream = torch.cuda.Stream(dev)
+            self.e0, self.e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def run(self, snr, seed, start, n, chunk_size, frames, workers, mode):
+        """Decode frames start..start+n-1; per-chunk (frames, frame errors,
+        bit errors), per-frame invoked flags (adaptive), device ms."""
+        import torch
+        nch = -(-n // chunk_size)
+        with torch.cuda.device(self.dev), torch.cuda.stream(self.stream):
+            if frames == "device":
+                self.src.generate(seed, snr, start, n, self.llr, self.pay)
+                x = self.llr[:n]
+            else:
+                fb = generate_frames(self.spec, snr, seed, start, n, workers=workers)
+                feed = fb.llrs if mode == "f32" else quantize_int8(fb.llrs)
+                x = torch.from_numpy(feed).to(self.dev, non_blocking=False)
+            self.e0.record()
+            if self.adaptive:
+                self.dec.decode_device(x, self.info[:n], self.ok[:n], self.pm[:n], self.pu[:n], self.inv[:n])
+            else:
+                self.dec.decode_device(x, self.info[:n], self.ok[:n], self.pm[:n], self.pu[:n])
+            self.e1.record()
+            if frames == "device":
+                self.counts.zero_()
+                self.src.count(self.info, self.pay, n, chunk_size, self.counts)
+                per = self.counts[:nch].cpu().numpy()
+            else:
+                got = self.info[:n].cpu().numpy()
+                bad = np.count_nonzero(got != fb.payloads, axis=1)
+                per = np.zeros((nch, 3), np.int64)
+                for c in range(nch):
+                    b = bad[c * chunk_size:(c + 1) * chunk_size]
+                    per[c] = (b.size, np.count_nonzero(b), b.sum())
+            invc = self.inv[:n].cpu().numpy() if self.adaptive else None
+            self.stream.synchronize()
+        return per, invc, self.e0.elapsed_time(self.e1)
+
+
+def _point(decs, schedule, adaptive, snr, min_errors, max_frames, seed, workers, chunk_size, frames,
            batch, mode) -> SimRecord:
-    import torch
+    """One sweep point over one or several devices: each round decodes one
+    super-batch per device (consecutive frame ranges, in parallel), then
+    absorbs the chunks in frame order with the reference's stop rule -- the
+    counts do not depend on the number of devices."""
+    from concurrent.futures import ThreadPoolExecutor
     spec = schedule.spec
     k = spec.k
     tot = dict(frames=0, ferr=0, berr=0, inv=0)
     dev_ms = 0.0
     chunks_per_batch = max(1, batch // chunk_size)
     B = chunks_per_batch * chunk_size
-    base = dec._list if adaptive else dec
-    dev = torch.device("cuda", base.device)
-    if frames == "device":
-        src = DeviceFrames(base)
-        llr = torch.empty((B, spec.N), dtype=torch.int8 if mode == "int8" else torch.float32, device=dev)
-        pay = torch.empty((B, src.kw), dtype=torch.int32, device=dev)
-        counts = torch.zeros((chunks_per_batch, 3), dtype=torch.int64, device=dev)
-    info = torch.empty((B, k), dtype=torch.uint8, device=dev)
-    ok = torch.empty(B, dtype=torch.uint8, device=dev)
-    pm = torch.empty(B, dtype=torch.float64, device=dev)
-    pu = torch.empty(B, dtype=torch.int32, device=dev)
-    inv = torch.empty(B, dtype=torch.uint8, device=dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ws = [_Worker(d, spec, adaptive, B, chunks_per_batch, frames, mode) for d in decs]
     start, done = 0, False
-    while not done and start < max_frames:
-        n = min(B, max_frames - start)
-        nch = -(-n // chunk_size)
-        if frames == "device":
-            src.generate(seed, snr, start, n, llr, pay)
-            x = llr[:n]
-        else:
-            fb = generate_frames(spec, snr, seed, start, n, workers=workers)
-            feed = fb.llrs if mode == "f32" else quantize_int8(fb.llrs)
-            x = torch.from_numpy(feed).to(dev)
-        e0.record()
-        if adaptive:
-            dec.decode_device(x, info[:n], ok[:n], pm[:n], pu[:n], inv[:n])
-        else:
-            dec.decode_device(x, info[:n], ok[:n], pm[:n], pu[:n])
-        e1.record()
-        if frames == "device":
-            counts.zero_()
-            src.count(info, pay, n, chunk_size, counts)
-            per = counts[:nch].cpu().numpy()
-        else:
-            got = info[:n].cpu().numpy()
-            bad = np.count_nonzero(got != fb.payloads, axis=1)
-            per = np.zeros((nch, 3), np.int64)
-            for c in range(nch):
-                b = bad[c * chunk_size:(c + 1) * chunk_size]
-                per[c] = (b.size, np.count_nonzero(b), b.sum())
-        invc = inv[:n].cpu().numpy() if adaptive else None
-        torch.cuda.synchronize(dev)
-        batch_ms = e0.elapsed_time(e1)
-        decoded = 0
-        for c in range(nch):  # absorb chunks in order (sim.py:236-262)
-            tot["frames"] += int(per[c, 0])
-            tot["ferr"] += int(per[c, 1])
-            tot["berr"] += int(per[c, 2])
-            if adaptive:
-                tot["inv"] += int(invc[c * chunk_size:(c + 1) * chunk_size].sum())
-            decoded += int(per[c, 0])
-            if (min_errors > 0 and tot["ferr"] >= min_errors) or tot["frames"] >= max_frames:
-                done = True
-                break
-        dev_ms += batch_ms * decoded / n  # chunks past the stop point are not charged
-        start += n
+    with ThreadPoolExecutor(len(ws)) as pool:
+        while not done and start < max_frames:
+            jobs = []
+            for w in ws:
+                if start >= max_frames:
+                    break
+                n = min(B, max_frames - start)
+                jobs.append((n, pool.submit(w.run, snr, seed, start, n, chunk_size, frames, workers, mode)))
+                start += n
+            round_ms = 0.0
+            for n, fut in jobs:
+                per, invc, batch_ms = fut.result()
+                if done:
+                    continue
+                decoded = 0
+                for c in range(len(per)):  # absorb chunks in order (sim.py:236-262)
+                    tot["frames"] += int(per[c, 0])
+                    tot["ferr"] += int(per[c, 1])
+                    tot["berr"] += int(per[c, 2])
+                    if adaptive:
+                        tot["inv"] += int(invc[c * chunk_size:(c + 1) * chunk_size].sum())
+                    decoded += int(per[c, 0])
+                    if (min_errors > 0 and tot["ferr"] >= min_errors) or tot["frames"] >= max_frames:
+                        done = True
+                        break
+                # devices run in parallel: a round costs its slowest device;
+                # chunks past the stop point are not charged
+                round_ms = max(round_ms, batch_ms * decoded / n)
+            dev_ms += round_ms
     fr = tot["frames"]
     lat = dev_ms * 1e3 / fr if fr else 0.0
     return SimRecord(snr_db=snr, frames=fr, frame_errors=tot["ferr"], bit_errors=tot["berr"],
@@ -185,21 +222,24 @@ def _point(dec, schedule, adaptive, snr, min_errors, max_frames, seed, workers, 
 def run_sweep(schedule: Schedule, list_size: int, snr_dbs, *, adaptive: bool = False,
               min_errors: int = 100, max_frames: int = 1_000_000, seed: int = 0,
               workers: int = 1, chunk_size: int = 256, frames: str = "host",
-              batch: int = 65536, mode: str = "f32", device: int = 0) -> list[SimRecord]:
+              batch: int = 65536, mode: str = "f32", device: int = 0,
+              devices=None) -> list[SimRecord]:
     """FER/BER over SNR points (reference ``sim.py:283-302``), decoded on the GPU.
 
     Same stop rule and chunk accounting as the reference; ``workers`` sets the
     host frame-generation processes (``frames="host"``).  ``batch`` frames
-    (rounded down to whole chunks) are decoded per GPU launch."""
+    (rounded down to whole chunks) are decoded per GPU launch.  ``devices``
+    (a list of CUDA ordinals) shards each round of super-batches over
+    several GPUs -- the analogue of the reference's process pool
+    (``sim.py:235-258``); the counts are identical for any device list."""
     if min_errors < 0 or max_frames < 1:
         raise ValueError("min_errors must be >= 0 and max_frames >= 1")
     if chunk_size < 1:
         raise ValueError(f"chunk_size {chunk_size} must be >= 1")
     if frames not in ("host", "device"):
         raise ValueError(f"frames must be 'host' or 'device', got {frames!r}")
-    if adaptive:
-        dec = AdaptiveDecoder(schedule, list_size, mode=mode, device=device)
-    else:
-        dec = ListDecoder(schedule, list_size, mode=mode, device=device)
-    return [_point(dec, schedule, adaptive, float(s), min_errors, max_frames, seed, workers, chunk_size,
+    devs = list(devices) if devices else [device]
+    make = AdaptiveDecoder if adaptive else ListDecoder
+    decs = [make(schedule, list_size, mode=mode, device=d) for d in devs]
+    return [_point(decs, schedule, adaptive, float(s), min_errors, max_frames, seed, workers, chunk_size,
                    frames, batch, mode) for s in snr_dbs]

@@ -50,14 +50,17 @@ def test_gpu_decode_simulate_bench(tmp_path, capsys):
     with open(tmp_path / "llr.txt", "w") as fh:
         for x in fb.llrs:
             fh.write(" ".join(repr(float(v)) for v in x) + "\n")
+    from oracle import oracle
+    sch = pb.build_schedule(spec)
+    parsed = pb.clamp_llr(np.stack(cli.read_llr_lines(tmp_path / "llr.txt")))
     for extra in ([], ["--adaptive"]):
         assert cli.main(["decode", "--spec", str(spec_p), "--list", "8", "--in", str(tmp_path / "llr.txt"),
                          "--out", str(tmp_path / "dec.txt"), *extra]) == 0
         got = np.stack(cli.read_bit_lines(tmp_path / "dec.txt"))
-        exp = pb.ListDecoder(pb.build_schedule(spec), 8).decode_batch(fb.llrs.astype(np.float64))
         assert got.shape == (20, 120)
-        if not extra:
-            assert np.array_equal(got, exp.info_bits)
+        # the CPU oracle (restatement of the reference, pinned to its fixtures)
+        exp = (oracle.adaptive_batch(sch, 8, parsed) if extra else oracle.decode_batch(sch, 8, parsed))
+        assert np.array_equal(got, exp.info_bits), extra
     assert cli.main(["simulate", "--spec", str(spec_p), "--list", "4", "--snr", "1:2:1", "--min-errors", "5",
                      "--max-frames", "2000", "--out", str(tmp_path / "s.csv")]) == 0
     lines = (tmp_path / "s.csv").read_text().splitlines()

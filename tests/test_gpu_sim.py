@@ -20,13 +20,16 @@ SWEEPS = json.load(open(os.path.join(golden_cases.HERE, "reference_adaptive.json
 
 
 @pytest.mark.parametrize("sw", SWEEPS, ids=[s["name"] for s in SWEEPS])
-@pytest.mark.parametrize("batch", [64 * 1024, 100])
-def test_run_sweep_counts_match_reference(sw, batch):
+@pytest.mark.parametrize("batch,devices", [(64 * 1024, None), (100, None), (300, [0, 0, 0])])
+def test_run_sweep_counts_match_reference(sw, batch, devices):
+    """Counts equal the reference's run_sweep fixtures for any super-batch
+    size and device list ([0, 0, 0]: three decoders sharding each round, the
+    multi-GPU path exercised on one GPU)."""
     spec = pb.CodeSpec.construct(sw["N"], sw["k"], pb.CrcConfig(**sw["crc"]), sw["eps"])
     sch = pb.build_schedule(spec)
     recs = pb.run_sweep(sch, sw["L"], sw["snrs"], adaptive=sw["adaptive"], min_errors=sw["min_errors"],
                         max_frames=sw["max_frames"], seed=sw["seed"], chunk_size=sw["chunk_size"],
-                        batch=batch)
+                        batch=batch, devices=devices)
     for got, exp in zip(recs, sw["records"]):
         assert (got.frames, got.frame_errors, got.bit_errors) == \
             (exp["frames"], exp["frame_errors"], exp["bit_errors"])
@@ -115,3 +118,12 @@ def test_device_frames_sweep_runs_and_is_monotone():
     ad = pb.run_sweep(sch, 4, [2.0], adaptive=True, min_errors=0, max_frames=20000, seed=5,
                       frames="device", batch=8192)
     assert 0 < ad[0].invoked_list_fraction < 1
+
+
+def test_device_frames_sweep_sharded_over_devices_is_split_invariant():
+    spec = pb.CodeSpec.from_design_ebn0(1024, 828, pb.CRC32, 4.0)
+    sch = pb.build_schedule(spec)
+    a = pb.run_sweep(sch, 8, [3.0], min_errors=0, max_frames=20000, frames="device", batch=4096, seed=3)
+    b = pb.run_sweep(sch, 8, [3.0], min_errors=0, max_frames=20000, frames="device", batch=4096, seed=3,
+                     devices=[0, 0])
+    assert (a[0].frames, a[0].frame_errors, a[0].bit_errors) == (b[0].frames, b[0].frame_errors, b[0].bit_errors)
