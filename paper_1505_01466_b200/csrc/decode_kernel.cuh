@@ -16,9 +16,9 @@
 //              listdec.py:360-394)
 //   selection  warp 0, lane = source path: candidate metrics as orderable
 //              int64 keys, each lane's candidates a sorted column; the L-th
-//              best key from warp-shuffle bitonic sorts of the columns (early
-//              exit once no column entry can enter), exact ties resolved by
-//              (source, cand) prefix counts -- listdec.py:63-100
+//              best key from a k-way merge of the columns (REDUX max / min,
+//              select_phase_c), exact ties resolved by (source, cand) prefix
+//              counts -- listdec.py:63-100
 //   materialise survivors copy their source's row-index vectors (lazy copy,
 //              listdec.py:103-143,397-434), write the leaf word and run the
 //              leaf's chain of Combines in place (listdec.py:327-332)
@@ -862,20 +862,6 @@ __device__ __forceinline__ long long shfl_ll(long long v, int src) {
     const int lo = __shfl_sync(FULL_MASK, (int)(v & 0xffffffff), src);
     const int hi = __shfl_sync(FULL_MASK, (int)(v >> 32), src);
     return ((long long)hi << 32) | (unsigned)lo;
-}
-__device__ __forceinline__ void bitonic_sort(long long &v, int Wd, bool desc, int lane) {
-    for (int k = 2; k <= Wd; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            const long long o = shfl_xor_ll(v, j);
-            const bool want_max = (((lane & j) == 0) == (((lane & k) == 0) == desc));
-            v = (want_max == (o > v)) ? o : v;
-        }
-}
-__device__ __forceinline__ void bitonic_merge_desc(long long &v, int Wd, int lane) {
-    for (int j = Wd >> 1; j > 0; j >>= 1) {
-        const long long o = shfl_xor_ll(v, j);
-        v = (((lane & j) == 0) == (o > v)) ? o : v;
-    }
 }
 // exclusive warp prefix sum of v in [0, 15]: one ballot per bit, independent
 __device__ __forceinline__ int excl_scan4(int v, int lane) {

@@ -6,10 +6,14 @@
 //     (its "chain"), and the active-path count before/after every op is
 //     resolved statically (it does not depend on the data)
 //   * builds the CRC tables: per-u-position syndrome rows (codes.py:127-156 as
-//     an affine GF(2) map) transformed into each leaf's local codeword
-//     coordinates, so a path's CRC state is one uint32 updated per leaf
+//     an affine GF(2) map) transformed into the codeword domain (x = u G_N),
+//     as nibble tables: a survivor's CRC check is one XOR pass over its root
+//     codeword at the end of the frame
 //   * plans the per-frame storage (shared memory vs global scratch per alpha
-//     stage), sizes the persistent grid, stages host buffers, times launches.
+//     stage) for the interpreted kernel and the lane-per-path kernel
+//     (plan_lane), sizes the persistent grids, stages host buffers, orders
+//     launches that share a handle's scratch, times launches.  Every knob is
+//     an explicit pb_options field (no environment reads).
 #include <cuda_runtime.h>
 
 #include <algorithm>

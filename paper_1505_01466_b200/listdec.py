@@ -92,7 +92,8 @@ def select_candidates(pools, list_size: int):
     helper with the reference's semantics: the ``list_size`` best
     (source, candidate) pairs by updated metric, ties to the earlier source
     then candidate, returned in (source, candidate) order.  The GPU performs
-    the same choice with warp-shuffle bitonic sorts."""
+    the same choice with a warp-wide k-way merge of per-path sorted
+    candidate columns (lane_kernel.cuh select_mask)."""
     if list_size < 1:
         raise ValueError(f"list size {list_size} must be >= 1")
     flat = []
