@@ -26,6 +26,10 @@
 #ifndef PB_LANE_V2SPEC
 #define PB_LANE_V2SPEC 1
 #endif
+// a survivor's chain rows of at least this many words use the unrolled form
+#ifndef PB_CHAIN_CLOSED_MIN
+#define PB_CHAIN_CLOSED_MIN 1000000
+#endif
 
 namespace pb {
 namespace lk {
@@ -801,49 +805,110 @@ __device__ __forceinline__ uint32_t leaf_word(int kind, int m, int c, uint32_t h
     return v;
 }
 
-// Leaf word of this lane's survivor into slot sE's row, then the chain of
-// Combines t .. sE-1 in place (listdec.py:327-332):
-//   dst[E - 2^(s+1), E - 2^s) = slot_s[row_s] ^ dst[E - 2^s, E)
+// The slot-sE row a leaf's chain of Combines produces (listdec.py:327-332):
+// level by level dst[E - 2^(s+1), E - 2^s) = slot_s[row_s] ^ dst[E - 2^s, E),
+// i.e. unrolled, bit j of the row is
+//   leaf[j mod m] ^ XOR_{s in [t, sE), bit s of j clear} slot_s[j mod 2^s].
+// The levels below 32 bits only depend on j mod 32: one register pattern R
+// (computed level by level); the word levels make word w
+//   base(w) ^ XOR_{s >= 5, bit (s-5) of w clear} slot_s[w mod 2^(s-5)]
+// with base = R (leaf narrower than a word) or the leaf word w mod (m/32).
+// No word depends on another, so a block's loads (every level) are in flight
+// together instead of one memory round trip per level.  Words w0, w0 + step,
+// ... of the row; ib = the path's beta rows.
 template <typename T>
-__device__ __forceinline__ void write_chain(Fr<T> &F, const LOp &o, int kind, uint32_t *dst, int p, int c,
-                                            uint32_t hard, uint32_t l01, uint32_t l23, uint32_t flag) {
-    const int t = o.stage, sE = o.aux, m = 1 << t, E = 1 << sE;
-    const uint32_t *row = F.hard_words() + p;
-    if (m >= 32) {
-        for (int w = 0; w < (m >> 5); ++w)
-            dst[((E - m) >> 5) + w] = leaf_word(kind, m, c, hard, l01, l23, flag, row, w);
-    } else {
+__device__ __forceinline__ void chain_row(const Fr<T> &F, int kind, int t, int sE, const uint32_t (&ib)[4],
+                                          uint32_t *dst, const uint32_t *hw, int c, uint32_t hard, uint32_t l01,
+                                          uint32_t l23, uint32_t flag, int w0, int step) {
+    const int m = 1 << t, E = 1 << sE;
+    uint32_t R = 0u;
+    if (m < 32) {
         const int s_sub = sE < 5 ? sE : 5;
         const int W0 = E >= 32 ? E - 32 : 0;
-        uint32_t R = leaf_word(kind, m, c, hard, l01, l23, flag, row, 0) << (E - m - W0);
+        R = leaf_word(kind, m, c, hard, l01, l23, flag, hw, 0) << (E - m - W0);
         for (int s = t; s < s_sub; ++s) {
-            const uint32_t sl = F.beta_row(s, get8(F.ib, s))[0];
+            const uint32_t sl = F.beta_row(s, get8(ib, s))[0];
             const int seg = 1 << s;
             R |= ((sl ^ (R >> (E - seg - W0))) & ((1u << seg) - 1u)) << (E - 2 * seg - W0);
         }
-        if (E >= 32)
-            dst[(E >> 5) - 1] = R;
-        else
-            dst[0] = R & ((1u << E) - 1u);
-    }
-    for (int s = t > 5 ? t : 5; s < sE; ++s) {
-        const int seg = 1 << s, nw = seg >> 5;
-        const uint32_t *sl = F.beta_row(s, get8(F.ib, s));
-        uint32_t *da = dst + ((E - 2 * seg) >> 5);
-        const uint32_t *db = dst + ((E - seg) >> 5);
-        int w = 0;
-        for (; w + 4 <= nw; w += 4) {
-            uint32_t a[4], b[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                a[u] = sl[w + u];
-                b[u] = db[w + u];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) da[w + u] = a[u] ^ b[u];
+        if (E <= 32) {
+            if (w0 == 0) dst[0] = E == 32 ? R : (R & ((1u << E) - 1u));
+            return;
         }
-        for (; w < nw; ++w) da[w] = sl[w] ^ db[w];
     }
+    const int s0 = t > 5 ? t : 5;
+    const int nw = E >> 5, lw = m >= 32 ? (m >> 5) - 1 : 0;
+    if (step == 1 && (nw < PB_CHAIN_CLOSED_MIN || sE - s0 > 6)) {
+        // short rows (and very deep chains): level by level, each level's
+        // words from the one below (the recursion as written)
+        if (m >= 32) {
+            for (int w = 0; w < (m >> 5); ++w)
+                dst[((E - m) >> 5) + w] = leaf_word(kind, m, c, hard, l01, l23, flag, hw, w);
+        } else {
+            dst[nw - 1] = R;
+        }
+        for (int s = s0; s < sE; ++s) {
+            const int seg = 1 << s, nws = seg >> 5;
+            const uint32_t *sl = F.beta_row(s, get8(ib, s));
+            uint32_t *da = dst + ((E - 2 * seg) >> 5);
+            const uint32_t *db = dst + ((E - seg) >> 5);
+            int w = 0;
+            for (; w + 4 <= nws; w += 4) {
+                uint32_t a[4], b[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    a[u] = sl[w + u];
+                    b[u] = db[w + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) da[w + u] = a[u] ^ b[u];
+            }
+            for (; w < nws; ++w) da[w] = sl[w] ^ db[w];
+        }
+        return;
+    }
+    constexpr int NL = 6;  // word levels handled unrolled (N <= 2048: all of them)
+    const uint32_t *sl[NL];
+#pragma unroll
+    for (int i = 0; i < NL; ++i) sl[i] = s0 + i < sE ? F.beta_row(s0 + i, get8(ib, s0 + i)) : nullptr;
+    for (int wb = w0; wb < nw; wb += 8 * step) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int w = wb + u * step;
+            v[u] = m >= 32 ? (w < nw ? leaf_word(kind, m, c, hard, l01, l23, flag, hw, w & lw) : 0u) : R;
+        }
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+            if (s0 + i < sE) {
+                const int sh = s0 + i - 5, msk = (1 << sh) - 1;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int w = wb + u * step;
+                    if (w < nw && !((w >> sh) & 1)) v[u] ^= sl[i][w & msk];
+                }
+            }
+        }
+        for (int s = s0 + NL; s < sE; ++s) {  // deeper chains (N > 2048, warp mode)
+            const uint32_t *q = F.beta_row(s, get8(ib, s));
+            const int sh = s - 5, msk = (1 << sh) - 1;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int w = wb + u * step;
+                if (w < nw && !((w >> sh) & 1)) v[u] ^= q[w & msk];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (wb + u * step < nw) dst[wb + u * step] = v[u];
+    }
+}
+
+// Leaf word of this lane's survivor and its chain into slot sE's own row
+template <typename T>
+__device__ __forceinline__ void write_chain(Fr<T> &F, const LOp &o, int kind, uint32_t *dst, int p, int c,
+                                            uint32_t hard, uint32_t l01, uint32_t l23, uint32_t flag) {
+    chain_row(F, kind, o.stage, o.aux, F.ib, dst, F.hard_words() + p, c, hard, l01, l23, flag, 0, 1);
 }
 
 template <typename T>
@@ -934,7 +999,7 @@ template <typename T>
 __device__ __forceinline__ void build_root(const Fr<T> &F, int kk, uint32_t *x) {
     const LParams &P = F.P;
     const LOp fo = P.prog[P.final_op];
-    const int N = P.N, n = P.n, t = fo.stage, m = 1 << t, lane = F.lane;
+    const int n = P.n, t = fo.stage, lane = F.lane;
     int kind = fo.kind;
     if (kind == K_R1 && t == 0) kind = K_REP;
     const int c = (int)__shfl_sync(FULL_MASK, F.dec, kk);
@@ -942,40 +1007,14 @@ __device__ __forceinline__ void build_root(const Fr<T> &F, int kk, uint32_t *x) 
     const uint32_t l01 = __shfl_sync(FULL_MASK, F.lrb01, kk);
     const uint32_t l23 = __shfl_sync(FULL_MASK, F.lrb23, kk);
     const uint32_t flag = __shfl_sync(FULL_MASK, F.lflag, kk);
-    uint32_t ib[4], ia[4];
+    uint32_t ib[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        ib[j] = __shfl_sync(FULL_MASK, F.ib[j], kk);
-        ia[j] = __shfl_sync(FULL_MASK, F.ia[j], kk);
-    }
+    for (int j = 0; j < 4; ++j) ib[j] = __shfl_sync(FULL_MASK, F.ib[j], kk);
     // the final leaf's hard words (leaves wider than 32)
     const uint32_t *src = F.hard_words() + __shfl_sync(FULL_MASK, F.srcl, kk);
-    const int E = N;
-    if (m >= 32) {
-        for (int w = lane; w < (m >> 5); w += 32)
-            x[((E - m) >> 5) + w] = leaf_word(kind, m, c, hard, l01, l23, flag, src, w);
-    } else if (lane == 0) {
-        const int s_sub = n < 5 ? n : 5;
-        const int W0 = E >= 32 ? E - 32 : 0;
-        uint32_t R = leaf_word(kind, m, c, hard, l01, l23, flag, src, 0) << (E - m - W0);
-        for (int s = t; s < s_sub; ++s) {
-            const uint32_t sl = F.beta_row(s, get8(ib, s))[0];
-            const int seg = 1 << s;
-            R |= ((sl ^ (R >> (E - seg - W0))) & ((1u << seg) - 1u)) << (E - 2 * seg - W0);
-        }
-        if (E >= 32)
-            x[(E >> 5) - 1] = R;
-        else
-            x[0] = R & ((1u << E) - 1u);
-    }
+    // lanes over the root's words (the chain ends at the root: E = N)
+    chain_row(F, kind, t, n, ib, x, src, c, hard, l01, l23, flag, lane, 32);
     __syncwarp();
-    for (int s = t > 5 ? t : 5; s < n; ++s) {
-        const int seg = 1 << s, nw = seg >> 5;
-        const uint32_t *sl = F.beta_row(s, get8(ib, s));
-        const int a = (E - 2 * seg) >> 5, b = (E - seg) >> 5;
-        for (int w = lane; w < nw; w += 32) x[a + w] = sl[w] ^ x[b + w];
-        __syncwarp();
-    }
 }
 
 __device__ __forceinline__ uint32_t syndrome(const LParams &P, const uint32_t *x, int lane) {
