@@ -92,6 +92,9 @@ typedef struct pb_options {
                                  six for adaptive decoding) */
     int32_t grid_sms;         /* use at most this many SMs (0 = all) */
     int32_t l1_list_kernel;   /* 1: list size 1 through the list kernel instead of the single-path pass */
+    int32_t fuse;             /* lane kernel op fusion: 0 auto (everything measured faster), -1 none, else a
+                                 bit set: 1 = a leaf reads f / g of its parent's row (its own row is never
+                                 stored), 2 = an F is computed by the op producing its input row */
 } pb_options;
 
 /* Build a decoder for (code, schedule, list size) on a CUDA device.

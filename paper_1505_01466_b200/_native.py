@@ -48,7 +48,7 @@ class PbOptions(ctypes.Structure):
                 ("warps_per_frame", ctypes.c_int32), ("frames_per_sm", ctypes.c_int32),
                 ("sync_every", ctypes.c_int32), ("recompute_stages", ctypes.c_int32),
                 ("chunk_frames", ctypes.c_int32), ("grid_sms", ctypes.c_int32),
-                ("l1_list_kernel", ctypes.c_int32)]
+                ("l1_list_kernel", ctypes.c_int32), ("fuse", ctypes.c_int32)]
 
     @classmethod
     def from_dict(cls, d):

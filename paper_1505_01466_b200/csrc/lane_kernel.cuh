@@ -269,11 +269,51 @@ __device__ __forceinline__ V2Ld<T> make_v2(const Fr<T> &F, const LOp &o) {
     return V2Ld<T>{F.channel(), F.beta_row(n - 1, get8(F.ib, n - 1)), F.beta_row(n - 2, get8(F.ib, n - 2)),
                    F.P.N >> 2, (o.flags & LF_V1G) != 0, (o.flags & LF_V2G) != 0};
 }
-// a leaf's LLRs: its stage's stored row (stages n-1 / n-2 are stored for
-// leaves: the F / G before such a leaf writes them, runtime.cu) or the channel
+// A leaf's LLRs.  Plain: its stage's stored row (leaves under a recomputed
+// stage read the staging row the F / G before them wrote, runtime.cu) or the
+// channel (a root leaf).  Fused (LF_FUSE_F / LF_FUSE_G): the F / G that would
+// have produced the leaf's row is folded into the read -- the leaf reads the
+// two halves of its parent's row (stage t + 1) and applies f, or g with the
+// path's left-sibling bits (beta slot t); the row of stage t is never stored
+// (listdec.py:317-326 followed by :334-394 on the same values).
 template <typename T>
-__device__ __forceinline__ RowLd<T> leaf_src(const Fr<T> &F, const LOp &o, int t, const uint32_t (&ia)[4]) {
-    return o.src == S_CH ? RowLd<T>{F.channel(), 4} : RowLd<T>{F.a_row(t, get8(ia, t)), 128};
+struct LeafLd {
+    const T *p;          // the row read: stage t (plain) or t + 1 (fused)
+    int qs;              // quad stride in elements (128 stored rows, 4 channel)
+    int mode;            // 0 plain, 1 f, 2 g
+    int m;               // leaf size
+    const uint32_t *bw;  // g: beta row of slot t
+    __device__ __forceinline__ void quad(int x, float (&v)[4]) const {
+        if (mode == 0) {
+            V4<T>::ld(p + x * qs, v);
+            return;
+        }
+        float a[4], b[4];
+        V4<T>::ld(p + x * qs, a);
+        V4<T>::ld(p + (x + (m >> 2)) * qs, b);
+        if (mode == 2) {
+            const unsigned bits = bw[x >> 3] >> ((x & 7) * 4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = g_op_bits<T>(a[j], b[j], bits, j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = f_op(a[j], b[j]);
+        }
+    }
+    __device__ __forceinline__ float el(int i) const { return Elem<T>::ld(p + (i >> 2) * qs + (i & 3)); }
+    __device__ __forceinline__ float get(int i) const {
+        if (mode == 0) return el(i);
+        const float a = el(i), b = el(i + m);
+        return mode == 2 ? g_op<T>(a, b, (bw[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
+    }
+};
+template <typename T>
+__device__ __forceinline__ LeafLd<T> leaf_src(const Fr<T> &F, const LOp &o, int t, const uint32_t (&ia)[4]) {
+    const int mode = (o.flags >> LF_FUSE_SHIFT) & 3;
+    const int ps = mode ? t + 1 : t;
+    const uint32_t *bw = mode == 2 ? F.beta_row(t, get8(F.ib, t)) : nullptr;
+    if (o.src == S_CH) return LeafLd<T>{F.channel(), 4, mode, 1 << t, bw};
+    return LeafLd<T>{F.a_row(ps, get8(ia, ps)), 128, mode, 1 << t, bw};
 }
 
 // ---------------------------------------------------------------- F / G
@@ -567,7 +607,7 @@ __device__ __forceinline__ int lk_flip_mask(int kind, int c, int odd) {
 template <typename T>
 __device__ __forceinline__ void leaf_phase_a(Fr<T> &F, const LOp &o, int kind, long long (&key)[8]) {
     const int t = o.stage, m = 1 << t;
-    const RowLd<T> src = leaf_src(F, o, t, F.ia);
+    const LeafLd<T> src = leaf_src(F, o, t, F.ia);
     if (kind == K_R0) {  // listdec.py:340-346
         float r[1];
         pw_sums_lane<1>(src, m, r);

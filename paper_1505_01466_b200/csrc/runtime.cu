@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -164,7 +165,7 @@ bool is_device_ptr(const void *p) {
 
 // options of the handle being created (pb_options, zero = default)
 struct Opts {
-    int kernel = 0, warps = 0, fps = 0, sync_every = 0, recompute = 0, chunk = 0, grid_sms = 0, l1_list = 0;
+    int kernel = 0, warps = 0, fps = 0, sync_every = 0, recompute = 0, chunk = 0, grid_sms = 0, l1_list = 0, fuse = 0;
 };
 Opts read_opts(const pb_options *o) {
     Opts r;
@@ -177,6 +178,8 @@ Opts read_opts(const pb_options *o) {
     r.chunk = o->chunk_frames;
     r.grid_sms = o->grid_sms;
     r.l1_list = o->l1_list_kernel;
+    // fields added after the first version: present when the caller's struct is long enough
+    if (o->size == 0 || o->size >= (int)(offsetof(pb_options, fuse) + sizeof(int32_t))) r.fuse = o->fuse;
     return r;
 }
 // sync_every (ops, power of two) -> the kernels' barrier mask; dflt = mask
@@ -262,9 +265,18 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
         why = "op program too long";
         return false;
     }
+    // op fusion (pb_options.fuse): bit 0 = leaves read f / g of their parent's row
+    const int fuse = opt.fuse < 0 ? 0 : (opt.fuse == 0 ? 1 : opt.fuse);
+    // a leaf folds the F / G before it into its reads when that op reads a
+    // stored row or the channel (not a recomputed stage)
+    auto leaf_fusable = [&](int i) {
+        return (fuse & 1) && i + 1 < n_ops && (ops[i].kind == PB_OP_F || ops[i].kind == PB_OP_G) &&
+               is_leaf_kind(ops[i + 1].kind) && (ops[i].stage == n || !virt(ops[i].stage));
+    };
     bool staged[pb::kMaxLog] = {};
     for (int i = 0; i + 1 < n_ops; ++i)
-        if ((ops[i].kind == PB_OP_F || ops[i].kind == PB_OP_G) && virt(ops[i].stage - 1) && is_leaf_kind(ops[i + 1].kind))
+        if ((ops[i].kind == PB_OP_F || ops[i].kind == PB_OP_G) && virt(ops[i].stage - 1) &&
+            is_leaf_kind(ops[i + 1].kind) && !leaf_fusable(i))
             staged[ops[i].stage - 1] = true;
     LLayout lay{};
     const int smem_cap = 227 * 1024;
@@ -333,6 +345,7 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     std::vector<LOp> prog;
     int di = 0, final_op = -1;
     bool v1g = false, v2g = false;
+    uint8_t pend_fuse = 0, pend_src = 0;
     for (int i = 0; i < n_ops; ++i) {
         const pb_op &op = ops[i];
         if (op.kind == PB_OP_COMBINE) continue;
@@ -343,6 +356,11 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
             if (s == n) v1g = op.kind == PB_OP_G;
             if (NV == 2 && s == n - 1) v2g = op.kind == PB_OP_G;
             const bool out_virtual = virt(s - 1);
+            if (leaf_fusable(i)) {  // the leaf after it reads f / g of this op's source
+                pend_fuse = op.kind == PB_OP_F ? LF_FUSE_F : LF_FUSE_G;
+                pend_src = src_of(s);
+                continue;
+            }
             if (out_virtual && !staged[s - 1]) continue;  // a mode switch only
             if (out_virtual && !(i + 1 < n_ops && is_leaf_kind(ops[i + 1].kind))) continue;
             LOp l{};
@@ -361,9 +379,10 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
         l.pin = (uint8_t)d.pin;
         l.pout = (uint8_t)d.pout;
         l.ncand = (uint8_t)(d.kind == pb::DK_R0 ? 0 : d.ncand);
-        l.src = op.stage == n ? S_CH : (virt(op.stage) ? S_GL : src_of(op.stage));
+        l.src = pend_fuse ? pend_src : op.stage == n ? S_CH : (virt(op.stage) ? S_GL : src_of(op.stage));
         l.aux = (uint8_t)d.target;
-        l.flags = (uint8_t)((d.select ? LF_SELECT : 0) | (v1g ? LF_V1G : 0) | (v2g ? LF_V2G : 0));
+        l.flags = (uint8_t)((d.select ? LF_SELECT : 0) | (v1g ? LF_V1G : 0) | (v2g ? LF_V2G : 0) | pend_fuse);
+        pend_fuse = 0;
         final_op = (int)prog.size();
         prog.push_back(l);
         // skip the Combines the leaf absorbed (the interpreted program did too)

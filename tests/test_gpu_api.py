@@ -250,7 +250,8 @@ def test_lane_kernel_and_interpreted_kernel_are_twins(cfg):
     for x, y in ((a.info_bits, b.info_bits), (a.crc_ok, b.crc_ok), (a.chosen_pm, b.chosen_pm),
                  (a.paths_used, b.paths_used)):
         assert np.array_equal(x, y)
-    for opt in ({"recompute_stages": 1}, {"sync_every": -1}, {"frames_per_sm": 8}):
+    for opt in ({"recompute_stages": 1}, {"sync_every": -1}, {"frames_per_sm": 8}, {"fuse": -1}, {"fuse": 1},
+                {"fuse": 1, "recompute_stages": 1}):
         c = pb.ListDecoder(sch, L, mode=mode, options=dict(opt, kernel="lane")).decode_batch(fb.llrs[:200])
         assert np.array_equal(c.info_bits, a.info_bits[:200]) and np.array_equal(c.chosen_pm, a.chosen_pm[:200])
 

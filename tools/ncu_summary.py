@@ -54,6 +54,26 @@ def main():
         "lts_bytes_per_frame": (f("lts__t_bytes.sum") or 0) / frames,
         "stalls_pct": {k: round(100 * v / tot, 1) for k, v in sorted(st.items(), key=lambda t: -t[1])[:8]},
     }
+    # north-star counters: pipe utilisation, issue slots, shared-memory and L2 / DRAM throughput vs peak
+    want = re.compile(r"^(sm__inst_executed_pipe_\w+\.avg\.pct_of_peak_sustained_active"
+                      r"|sm__pipe_\w+_cycles_active\.avg\.pct_of_peak_sustained_active"
+                      r"|sm__inst_issued\.avg\.pct_of_peak_sustained_active"
+                      r"|sm__inst_executed\.avg\.per_cycle_(active|elapsed)"
+                      r"|smsp__inst_executed\.avg\.per_cycle_active"
+                      r"|l1tex__data_pipe_lsu_wavefronts_mem_shared\.\w+\.pct_of_peak_sustained_elapsed"
+                      r"|l1tex__data_pipe_lsu_wavefronts_mem_shared\.sum"
+                      r"|l1tex__throughput\.avg\.pct_of_peak_sustained_active"
+                      r"|lts__throughput\.avg\.pct_of_peak_sustained_elapsed"
+                      r"|dram__throughput\.avg\.pct_of_peak_sustained_elapsed"
+                      r"|gpu__dram_throughput\.avg\.pct_of_peak_sustained_elapsed"
+                      r"|sm__throughput\.avg\.pct_of_peak_sustained_elapsed"
+                      r"|lts__t_sector_hit_rate\.pct|l1tex__t_sector_hit_rate\.pct"
+                      r"|smsp__thread_inst_executed_per_inst_executed\.ratio"
+                      r"|sm__cycles_active\.avg|sm__cycles_elapsed\.avg"
+                      r"|launch__occupancy_limit_\w+|sm__maximum_warps_per_active_cycle_pct"
+                      r"|smsp__warps_eligible\.avg\.per_cycle_active|smsp__warps_active\.avg\.per_cycle_active"
+                      r"|launch__shared_mem_per_block_dynamic|local_(load|store)\w*|smsp__inst_executed_op_local\w+\.sum)$")
+    out["counters"] = {k: (f(k) if f(k) is not None else d[k]) for k in sorted(d) if want.match(k)}
     # per-function instruction attribution (innermost source line)
     rows = list(csv.reader(io.StringIO(ncu(rep, "--page", "source", "--csv", "--print-source", "cuda,sass"))))
     src = open(KSRC).read().split("\n")
