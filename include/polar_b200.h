@@ -95,6 +95,12 @@ typedef struct pb_options {
     int32_t fuse;             /* lane kernel op fusion: 0 auto (everything measured faster), -1 none, else a
                                  bit set: 1 = a leaf reads f / g of its parent's row (its own row is never
                                  stored), 2 = an F is computed by the op producing its input row */
+    int32_t specialize;       /* lane kernel compiled per code (NVRTC, cubin cached next to the library): every
+                                 distinct op of the schedule becomes one instantiation with stage, placements,
+                                 offsets and path counts as constants -- the paper's unrolled decoder.
+                                 0 auto (on; the generic kernel runs if NVRTC is unavailable), -1 off
+                                 (generic kernel), 1 on (PB_ECUDA if it cannot be built), 3 = on with leaf
+                                 Combine-chain targets read at run time (fewer variants) */
 } pb_options;
 
 /* Build a decoder for (code, schedule, list size) on a CUDA device.
@@ -111,6 +117,18 @@ int pb_create(const pb_code *code, const pb_op *ops, int n_ops, int list_size, i
 /* pb_create with explicit options (opts may be NULL = pb_create). */
 int pb_create_ex(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
                  int device, const pb_options *opts, pb_handle **out);
+
+/* The per-code specialised lane kernel (pb_options.specialize) without a
+ * device.  pb_jit_source: the generated translation unit (buf may be NULL;
+ * *needed = bytes incl. the terminator, *n_variants = distinct op bodies).
+ * pb_jit_prebuild: compile it with NVRTC into the cubin cache next to the
+ * library (the build step does this for the BASELINE configurations, so a GPU
+ * box never compiles them).  PB_EINVAL when the lane kernel cannot be planned
+ * for the code, PB_ECUDA when NVRTC is unavailable or the compilation fails. */
+int pb_jit_source(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
+                  const pb_options *opts, char *buf, int64_t cap, int64_t *needed, int32_t *n_variants);
+int pb_jit_prebuild(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
+                    const pb_options *opts, int32_t *cache_hit, double *compile_s);
 
 /* Decode `batch` frames.  Replaces ListDecoder.decode (listdec.py:289-308),
  * batched.  llr: [batch][N] of in_type.  Outputs (each may be NULL):

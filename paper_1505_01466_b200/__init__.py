@@ -16,8 +16,8 @@ from .schedule import (NodeKind, NodeOp, Schedule, ScheduleConfig, build_schedul
 from .channel import (LLR_CLAMP, ChannelConfig, clamp_llr, frame_rng, generate_frames,
                       quantize_int8, transmit)
 from .listdec import (AdaptiveBatchResult, AdaptiveDecoder, BatchResult, DecodeResult,
-                      ListDecoder, PathOutcome, adaptive_decode, decode, schedule_op_rows,
-                      select_candidates)
+                      ListDecoder, PathOutcome, adaptive_decode, decode, prebuild_specialised,
+                      schedule_op_rows, select_candidates, set_default_options, specialised_source)
 from .fastssc import execute_schedule
 from .sim import CSV_FIELDS, DeviceFrames, SimRecord, run_sweep, write_csv
 
@@ -35,5 +35,5 @@ __all__ = [
     "AdaptiveBatchResult", "AdaptiveDecoder", "BatchResult", "DecodeResult", "ListDecoder",
     "PathOutcome", "adaptive_decode", "decode", "execute_schedule", "schedule_op_rows",
     "CSV_FIELDS", "DeviceFrames", "SimRecord", "run_sweep", "write_csv",
-    "select_candidates", "__version__",
+    "select_candidates", "set_default_options", "specialised_source", "prebuild_specialised", "__version__",
 ]

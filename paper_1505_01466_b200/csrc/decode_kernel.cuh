@@ -32,14 +32,8 @@
 #include <math.h>
 #include <stdint.h>
 #else
-typedef signed char int8_t;
-typedef unsigned char uint8_t;
-typedef short int16_t;
-typedef unsigned short uint16_t;
-typedef int int32_t;
-typedef unsigned int uint32_t;
-typedef long long int64_t;
-typedef unsigned long long uint64_t;
+#define INT_MAX 2147483647
+#define INT_MIN (-2147483647 - 1)
 #define LLONG_MIN (-9223372036854775807LL - 1)
 #define LLONG_MAX 9223372036854775807LL
 #define INFINITY __int_as_float(0x7f800000)

@@ -3,6 +3,16 @@
 #pragma once
 #ifndef __CUDACC_RTC__
 #include <stdint.h>
+#else  // NVRTC (the per-code specialised lane kernel, jit.cpp): no host headers
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef short int16_t;
+typedef unsigned short uint16_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+typedef unsigned long size_t;
 #endif
 
 namespace pb {
@@ -191,6 +201,13 @@ struct LParams {
     long long *op_cycles;       // profiling build: clock64 at the start of each op (CTA 0, frame slot 0), or null
     LLayout lay;
     LOp prog[kMaxOps];
+    uint16_t vid[kMaxOps];      // specialised build (jit.cpp): op i runs variant vid[i] of PB_JIT_OPS
+};
+// per-code constants of the specialised build (kJit in the generated source)
+struct JitCode {
+    int N, n, k, L, has_crc;
+    uint32_t crc_const;
+    int n_ops, final_op;
 };
 }  // namespace lk
 

@@ -31,8 +31,46 @@
 #define PB_CHAIN_CLOSED_MIN 1000000
 #endif
 
+// Per-code specialised build (PB_JIT, csrc/jit.cpp): the generated translation
+// unit defines, before including this header,
+//   __device__ constexpr LLayout kLay   the frame's storage plan
+//   __device__ constexpr JitCode kJit   N, n, k, L, CRC constants, op counts
+//   PB_JIT_OPS(X)                        X(id, kind, stage, pin, pout, ncand, src, aux, flags)
+//                                        one line per distinct op of the schedule (-1 = read at run time)
+// so stages, row placements (shared vs global), offsets, path counts and
+// selection shapes are compile-time constants in every op body -- the
+// paper's unrolled decoder (arXiv 1505.01466 sec. IV: node functions
+// specialised on size and position, schedule.py:159-206), with the op
+// sequence kept as a table of variant ids instead of straight-line code so
+// the SM's warps share the instruction cache.  Without PB_JIT the same
+// bodies read everything at run time (the generic kernel: the correctness
+// twin and the fallback when NVRTC is unavailable).
+#ifdef PB_JIT
+#define LK_LAY(P) (::pb::lk::kLay)
+#define LK_C(P, f) (::pb::lk::kJit.f)
+#else
+#define LK_LAY(P) ((P).lay)
+#define LK_C(P, f) ((P).f)
+#endif
+
 namespace pb {
 namespace lk {
+
+// An op as the bodies see it: each field a compile-time constant (>= 0) or
+// read from the runtime LOp (-1).
+template <int KIND = -1, int STAGE = -1, int PIN = -1, int POUT = -1, int NCAND = -1, int SRC = -1, int AUX = -1,
+          int FLAGS = -1>
+struct Op {
+    LOp o;
+    __device__ __forceinline__ int kind() const { return KIND >= 0 ? KIND : (int)o.kind; }
+    __device__ __forceinline__ int stage() const { return STAGE >= 0 ? STAGE : (int)o.stage; }
+    __device__ __forceinline__ int pin() const { return PIN >= 0 ? PIN : (int)o.pin; }
+    __device__ __forceinline__ int pout() const { return POUT >= 0 ? POUT : (int)o.pout; }
+    __device__ __forceinline__ int ncand() const { return NCAND >= 0 ? NCAND : (int)o.ncand; }
+    __device__ __forceinline__ int src() const { return SRC >= 0 ? SRC : (int)o.src; }
+    __device__ __forceinline__ int aux() const { return AUX >= 0 ? AUX : (int)o.aux; }
+    __device__ __forceinline__ int flags() const { return FLAGS >= 0 ? FLAGS : (int)o.flags; }
+};
 
 __device__ __forceinline__ int get8(const uint32_t (&w)[4], int s) {
     const int j = s >> 2;
@@ -92,24 +130,24 @@ struct Fr {
         if (marks) marks[k] = clock64();
 #endif
     }
-    __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(sm + P.lay.ch_off); }
+    __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(sm + LK_LAY(P).ch_off); }
     // hard-decision words of leaves wider than 32 (global scratch): word w of
     // lane q's path at [w * 32 + q]
     __device__ __forceinline__ uint32_t *hard_words() const {
-        return reinterpret_cast<uint32_t *>(gs + P.lay.hard_off);
+        return reinterpret_cast<uint32_t *>(gs + LK_LAY(P).hard_off);
     }
     __device__ __forceinline__ uint32_t *beta_row(int s, int row) const {
-        unsigned char *base = ((P.lay.b_gl >> s) & 1u) ? gs : sm;
-        return reinterpret_cast<uint32_t *>(base + P.lay.b_off[s]) + row * P.lay.b_stride[s];
+        unsigned char *base = ((LK_LAY(P).b_gl >> s) & 1u) ? gs : sm;
+        return reinterpret_cast<uint32_t *>(base + LK_LAY(P).b_off[s]) + row * LK_LAY(P).b_stride[s];
     }
     // stored alpha row r of stage s: quad x at element x * 128 (32 rows x 4)
     __device__ __forceinline__ T *a_row(int s, int r) const {
-        unsigned char *base = ((P.lay.a_gl >> s) & 1u) ? gs : sm;
-        return reinterpret_cast<T *>(base + P.lay.a_off[s]) + r * 4;
+        unsigned char *base = ((LK_LAY(P).a_gl >> s) & 1u) ? gs : sm;
+        return reinterpret_cast<T *>(base + LK_LAY(P).a_off[s]) + r * 4;
     }
     template <int WHERE>
     __device__ __forceinline__ T *a_row_t(int s, int r) const {
-        return reinterpret_cast<T *>((WHERE == S_GL ? gs : sm) + P.lay.a_off[s]) + r * 4;
+        return reinterpret_cast<T *>((WHERE == S_GL ? gs : sm) + LK_LAY(P).a_off[s]) + r * 4;
     }
 };
 
@@ -259,15 +297,15 @@ struct V2Ld {
     }
 };
 template <typename T>
-__device__ __forceinline__ V1Ld<T> make_v1(const Fr<T> &F, const LOp &o) {
-    const int n = F.P.n;
-    return V1Ld<T>{F.channel(), F.beta_row(n - 1, get8(F.ib, n - 1)), F.P.N >> 1, (o.flags & LF_V1G) != 0};
+__device__ __forceinline__ V1Ld<T> make_v1(const Fr<T> &F, int flags) {
+    const int n = LK_C(F.P, n);
+    return V1Ld<T>{F.channel(), F.beta_row(n - 1, get8(F.ib, n - 1)), LK_C(F.P, N) >> 1, (flags & LF_V1G) != 0};
 }
 template <typename T>
-__device__ __forceinline__ V2Ld<T> make_v2(const Fr<T> &F, const LOp &o) {
-    const int n = F.P.n;
+__device__ __forceinline__ V2Ld<T> make_v2(const Fr<T> &F, int flags) {
+    const int n = LK_C(F.P, n);
     return V2Ld<T>{F.channel(), F.beta_row(n - 1, get8(F.ib, n - 1)), F.beta_row(n - 2, get8(F.ib, n - 2)),
-                   F.P.N >> 2, (o.flags & LF_V1G) != 0, (o.flags & LF_V2G) != 0};
+                   LK_C(F.P, N) >> 2, (flags & LF_V1G) != 0, (flags & LF_V2G) != 0};
 }
 // A leaf's LLRs.  Plain: its stage's stored row (leaves under a recomputed
 // stage read the staging row the F / G before them wrote, runtime.cu) or the
@@ -307,12 +345,12 @@ struct LeafLd {
         return mode == 2 ? g_op<T>(a, b, (bw[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
     }
 };
-template <typename T>
-__device__ __forceinline__ LeafLd<T> leaf_src(const Fr<T> &F, const LOp &o, int t, const uint32_t (&ia)[4]) {
-    const int mode = (o.flags >> LF_FUSE_SHIFT) & 3;
+template <typename T, class OP>
+__device__ __forceinline__ LeafLd<T> leaf_src(const Fr<T> &F, const OP &o, int t, const uint32_t (&ia)[4]) {
+    const int mode = (o.flags() >> LF_FUSE_SHIFT) & 3;
     const int ps = mode ? t + 1 : t;
     const uint32_t *bw = mode == 2 ? F.beta_row(t, get8(F.ib, t)) : nullptr;
-    if (o.src == S_CH) return LeafLd<T>{F.channel(), 4, mode, 1 << t, bw};
+    if (o.src() == S_CH) return LeafLd<T>{F.channel(), 4, mode, 1 << t, bw};
     return LeafLd<T>{F.a_row(ps, get8(ia, ps)), 128, mode, 1 << t, bw};
 }
 
@@ -390,16 +428,16 @@ __device__ __forceinline__ void fg_body_v(const S &src, T *dst, const uint32_t *
 }
 
 // F / G of stage s into the path's own row of stage s-1 (listdec.py:317-326)
-template <typename T, bool IS_G, int SRC, int DST>
-__device__ __forceinline__ void fg_op(Fr<T> &F, const LOp &o) {
-    const int s = o.stage, h = 1 << (s - 1);
-    if (F.lane < o.pin) {
+template <typename T, bool IS_G, int SRC, int DST, class OP>
+__device__ __forceinline__ void fg_op(Fr<T> &F, const OP &o) {
+    const int s = o.stage(), h = 1 << (s - 1);
+    if (F.lane < o.pin()) {
         T *dst = F.template a_row_t<DST>(s - 1, F.lane);
         const uint32_t *bw = IS_G ? F.beta_row(s - 1, get8(F.ib, s - 1)) : nullptr;
         if (SRC == S_V2) {
             // the recomputed stages' F / G modes are fixed for the whole op:
             // one loop per mode pair, no per-quad branches
-            const V2Ld<T> v = make_v2(F, o);
+            const V2Ld<T> v = make_v2(F, o.flags());
             if (h < 32) {
                 fg_body<T, IS_G, 2>(v, dst, bw, h);
             } else if (!PB_LANE_V2SPEC) {
@@ -411,7 +449,7 @@ __device__ __forceinline__ void fg_op(Fr<T> &F, const LOp &o) {
                 default: fg_body_v<T, IS_G, 2>(V2Ld<T, 3>{v.ch, v.b1, v.b2, v.q, true, true}, dst, bw, h); break;
             }
         } else if (SRC == S_V1) {
-            const V1Ld<T> v = make_v1(F, o);
+            const V1Ld<T> v = make_v1(F, o.flags());
             if (h < 32)
                 fg_body<T, IS_G, 4>(v, dst, bw, h);
             else if (v.g_)
@@ -604,9 +642,9 @@ __device__ __forceinline__ int lk_flip_mask(int kind, int c, int odd) {
 // Phase A of a leaf for this lane's path: Rate-0 adds to the metric;
 // forking leaves produce candidate keys okey(pm + delta) in candidate order
 // and the leaf data the survivors will need.  Returns false for Rate-0.
-template <typename T>
-__device__ __forceinline__ void leaf_phase_a(Fr<T> &F, const LOp &o, int kind, long long (&key)[8]) {
-    const int t = o.stage, m = 1 << t;
+template <typename T, class OP>
+__device__ __forceinline__ void leaf_phase_a(Fr<T> &F, const OP &o, int kind, long long (&key)[8]) {
+    const int t = o.stage(), m = 1 << t;
     const LeafLd<T> src = leaf_src(F, o, t, F.ia);
     if (kind == K_R0) {  // listdec.py:340-346
         float r[1];
@@ -945,26 +983,26 @@ __device__ __forceinline__ void chain_row(const Fr<T> &F, int kind, int t, int s
 }
 
 // Leaf word of this lane's survivor and its chain into slot sE's own row
-template <typename T>
-__device__ __forceinline__ void write_chain(Fr<T> &F, const LOp &o, int kind, uint32_t *dst, int p, int c,
+template <typename T, class OP>
+__device__ __forceinline__ void write_chain(Fr<T> &F, const OP &o, int kind, uint32_t *dst, int p, int c,
                                             uint32_t hard, uint32_t l01, uint32_t l23, uint32_t flag) {
-    chain_row(F, kind, o.stage, o.aux, F.ib, dst, F.hard_words() + p, c, hard, l01, l23, flag, 0, 1);
+    chain_row(F, kind, o.stage(), o.aux(), F.ib, dst, F.hard_words() + p, c, hard, l01, l23, flag, 0, 1);
 }
 
-template <typename T>
-__device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
+template <typename T, class OP>
+__device__ __forceinline__ void leaf_op(Fr<T> &F, const OP &o) {
     const LParams &P = F.P;
-    const int t = o.stage;
-    int kind = o.kind;
+    const int t = o.stage();
+    int kind = o.kind();
     if (kind == K_R1 && t == 0) kind = K_REP;  // listdec.py:347
-    const bool valid = F.lane < o.pin;
+    const bool valid = F.lane < o.pin();
     long long key[8];
     if (valid) leaf_phase_a(F, o, kind, key);
     __syncwarp();
     F.mark(0);
-    const int sE = o.aux;
+    const int sE = o.aux();
     if (kind == K_R0) {
-        if (sE < P.n && valid) {
+        if (sE < LK_C(P, n) && valid) {
             uint32_t *dst = F.beta_row(sE, F.lane);
             write_chain(F, o, K_R0, dst, F.lane, 0, 0u, 0u, 0u, 0u);
             set8(F.ib, sE, F.lane);
@@ -973,20 +1011,20 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
         return;
     }
     unsigned mask;
-    const int C = o.ncand;
-    if (!(o.flags & LF_SELECT)) {
+    const int C = o.ncand();
+    if (!(o.flags() & LF_SELECT)) {
         mask = valid ? (1u << C) - 1u : 0u;
     } else if (C == 2) {
-        mask = select_mask<2>(key, valid, P.L, F.lane);
+        mask = select_mask<2>(key, valid, LK_C(P, L), F.lane);
     } else if (C == 4) {
-        mask = select_mask<4>(key, valid, P.L, F.lane);
+        mask = select_mask<4>(key, valid, LK_C(P, L), F.lane);
     } else {
-        mask = select_mask<8>(key, valid, P.L, F.lane);
+        mask = select_mask<8>(key, valid, LK_C(P, L), F.lane);
     }
     F.mark(1);
     // survivors in (source, cand) order: this lane's go to slots off ..
-    uint8_t *asg = F.sm + P.lay.asg_off;
-    double *met = reinterpret_cast<double *>(F.sm + P.lay.met_off);
+    uint8_t *asg = F.sm + LK_LAY(P).asg_off;
+    double *met = reinterpret_cast<double *>(F.sm + LK_LAY(P).met_off);
     int k = excl_scan4(__popc(mask), F.lane);
     while (mask) {
         const int c = __ffs(mask) - 1;
@@ -996,7 +1034,7 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
         ++k;
     }
     __syncwarp();
-    const bool live = F.lane < o.pout;
+    const bool live = F.lane < o.pout();
     int p = F.lane, c = 0;
     double pmn = F.pm;
     if (live) {
@@ -1024,7 +1062,7 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
     F.dec = (uint32_t)c;
     F.srcl = (uint32_t)p;
     F.mark(2);
-    if (live && sE < P.n) {
+    if (live && sE < LK_C(P, n)) {
         uint32_t *dst = F.beta_row(sE, F.lane);
         write_chain(F, o, kind, dst, p, c, hard, l01, l23, flag);
         set8(F.ib, sE, F.lane);
@@ -1038,8 +1076,8 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const LOp &o) {
 template <typename T>
 __device__ __forceinline__ void build_root(const Fr<T> &F, int kk, uint32_t *x) {
     const LParams &P = F.P;
-    const LOp fo = P.prog[P.final_op];
-    const int n = P.n, t = fo.stage, lane = F.lane;
+    const LOp fo = P.prog[LK_C(P, final_op)];
+    const int n = LK_C(P, n), t = fo.stage, lane = F.lane;
     int kind = fo.kind;
     if (kind == K_R1 && t == 0) kind = K_REP;
     const int c = (int)__shfl_sync(FULL_MASK, F.dec, kk);
@@ -1058,7 +1096,7 @@ __device__ __forceinline__ void build_root(const Fr<T> &F, int kk, uint32_t *x) 
 }
 
 __device__ __forceinline__ uint32_t syndrome(const LParams &P, const uint32_t *x, int lane) {
-    const int N = P.N, nw = N >= 32 ? N >> 5 : 1;
+    const int N = LK_C(P, N), nw = N >= 32 ? N >> 5 : 1;
     uint32_t s = 0u;
     for (int w = lane; w < nw; w += 32) {
         uint32_t v = x[w];
@@ -1081,18 +1119,18 @@ __device__ __forceinline__ void finalize(Fr<T> &F, long long f, int np) {
     const int lane = F.lane;
     const bool live = lane < np;
     const double pmk = live ? F.pm : -INFINITY;
-    uint32_t *u = reinterpret_cast<uint32_t *>(F.sm + P.lay.root_off);
-    const int rw = P.N >= 32 ? P.N >> 5 : 1;
+    uint32_t *u = reinterpret_cast<uint32_t *>(F.sm + LK_LAY(P).root_off);
+    const int rw = LK_C(P, N) >= 32 ? LK_C(P, N) >> 5 : 1;
     if (P.path_cw) {  // decode_paths: every survivor's codeword, metric and CRC flag
         for (int kk = 0; kk < np; ++kk) {
-            uint32_t *dst = P.path_cw + ((size_t)f * P.L + kk) * rw;
-            if (P.N < 32 && lane == 0) dst[0] = 0u;
+            uint32_t *dst = P.path_cw + ((size_t)f * LK_C(P, L) + kk) * rw;
+            if (LK_C(P, N) < 32 && lane == 0) dst[0] = 0u;
             __syncwarp();
             build_root(F, kk, dst);
             const uint32_t syn = syndrome(P, dst, lane);
-            if (lane == 0) P.path_crc[(size_t)f * P.L + kk] = P.has_crc && syn == P.crc_const;
+            if (lane == 0) P.path_crc[(size_t)f * LK_C(P, L) + kk] = LK_C(P, has_crc) && syn == LK_C(P, crc_const);
         }
-        if (live) P.path_pm[(size_t)f * P.L + lane] = pmk;
+        if (live) P.path_pm[(size_t)f * LK_C(P, L) + lane] = pmk;
         __syncwarp();
     }
     unsigned tried = 0u;
@@ -1112,34 +1150,34 @@ __device__ __forceinline__ void finalize(Fr<T> &F, long long f, int np) {
         }
         if (first < 0) first = bk;
         tried |= 1u << bk;
-        if (!P.has_crc) {
+        if (!LK_C(P, has_crc)) {
             wnr = bk;
             wpm = bm;
             break;
         }
-        if (P.N < 32 && lane == 0) u[0] = 0u;
+        if (LK_C(P, N) < 32 && lane == 0) u[0] = 0u;
         __syncwarp();
         build_root(F, bk, u);
-        if (syndrome(P, u, lane) == P.crc_const) {
+        if (syndrome(P, u, lane) == LK_C(P, crc_const)) {
             wnr = bk;
             wpm = bm;
             break;
         }
     }
-    const bool wok = wnr >= 0 && P.has_crc;
+    const bool wok = wnr >= 0 && LK_C(P, has_crc);
     if (wnr < 0) {
         wnr = first;
         wpm = __shfl_sync(FULL_MASK, pmk, first & 31);
     }
     if (P.info_out) {
         if (!wok) {
-            if (P.N < 32 && lane == 0) u[0] = 0u;
+            if (LK_C(P, N) < 32 && lane == 0) u[0] = 0u;
             __syncwarp();
             build_root(F, wnr, u);
         }
-        polar_transform_words(u, P.N, lane);
-        uint8_t *out = P.info_out + (size_t)f * P.k;
-        for (int i = lane; i < P.k; i += 32) {
+        polar_transform_words(u, LK_C(P, N), lane);
+        uint8_t *out = P.info_out + (size_t)f * LK_C(P, k);
+        for (int i = lane; i < LK_C(P, k); i += 32) {
             const uint32_t pos = __ldg(P.info_pos + i);
             out[i] = (uint8_t)((u[pos >> 5] >> (pos & 31)) & 1u);
         }
@@ -1156,7 +1194,7 @@ __device__ __forceinline__ void finalize(Fr<T> &F, long long f, int np) {
 
 template <typename T>
 __device__ __forceinline__ void load_channel_lane(const LParams &P, T *ch, long long f, int lane) {
-    const int N = P.N;
+    const int N = LK_C(P, N);
     if (P.in_type == PB_IN_I8) {
         const int8_t *src = reinterpret_cast<const int8_t *>(P.llr) + (size_t)f * N;
         for (int i = lane; i < N; i += 32) ch[i] = (T)src[i];
@@ -1175,23 +1213,21 @@ __device__ __forceinline__ void load_channel_lane(const LParams &P, T *ch, long 
     }
 }
 
-template <typename T>
-__device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
-    const LParams &P = F.P;
-#if PB_PROFILE
-    const bool prof = P.op_cycles && blockIdx.x == 0 && threadIdx.x == 0;
-#endif
-    for (int oi = 0; oi < P.n_ops; ++oi) {
-#if PB_PROFILE
-        if (prof) P.op_cycles[oi] = clock64();
-        F.marks = prof ? P.op_cycles + P.n_ops + 1 + 4 * oi : nullptr;
-#endif
-        LOp o;
-        {
-            const uint2 raw = reinterpret_cast<const uint2 *>(P.prog)[oi];  // one 8-byte constant load
-            o = *reinterpret_cast<const LOp *>(&raw);
+// One op.  Compile-time kind (the specialised build): exactly the body the
+// op needs is instantiated; run-time kind: a jump over the (F / G, source,
+// destination) placements that occur and the leaf body.
+template <typename T, int K, int S, int PI, int PO, int NC, int SR, int AX, int FL>
+__device__ __forceinline__ void exec_op(Fr<T> &F, const Op<K, S, PI, PO, NC, SR, AX, FL> &o, int &np) {
+    if constexpr (K >= 0) {
+        if constexpr (K <= K_G) {
+            static_assert(SR >= 0 && AX >= 0, "a compile-time F / G needs compile-time placements");
+            fg_op<T, K == K_G, SR, AX == S_GL ? S_GL : S_SM>(F, o);
+        } else if constexpr (K != K_NOP) {
+            leaf_op(F, o);
+            np = o.pout();
         }
-        const int sel = o.kind <= K_G ? (o.kind * 16 + o.src * 2 + (o.aux == S_GL ? 1 : 0)) : -1;
+    } else {
+        const int sel = o.kind() <= K_G ? (o.kind() * 16 + o.src() * 2 + (o.aux() == S_GL ? 1 : 0)) : -1;
         switch (sel) {
             // F: (source, destination) placements that occur (channel and
             // stage n-1 sources only write stages read by a leaf)
@@ -1212,30 +1248,61 @@ __device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
             case 1 * 16 + S_V2 * 2 + 0: fg_op<T, true, S_V2, S_SM>(F, o); break;
             case 1 * 16 + S_V2 * 2 + 1: fg_op<T, true, S_V2, S_GL>(F, o); break;
             default:
-                if (o.kind != K_NOP) {
+                if (o.kind() != K_NOP) {
                     leaf_op(F, o);
-                    np = o.pout;
+                    np = o.pout();
                 }
                 break;
         }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
+    const LParams &P = F.P;
+#if PB_PROFILE
+    const bool prof = P.op_cycles && blockIdx.x == 0 && threadIdx.x == 0;
+#endif
+    for (int oi = 0; oi < LK_C(P, n_ops); ++oi) {
+#if PB_PROFILE
+        if (prof) P.op_cycles[oi] = clock64();
+        F.marks = prof ? P.op_cycles + LK_C(P, n_ops) + 1 + 4 * oi : nullptr;
+#endif
+        LOp o;
+        {
+            const uint2 raw = reinterpret_cast<const uint2 *>(P.prog)[oi];  // one 8-byte constant load
+            o = *reinterpret_cast<const LOp *>(&raw);
+        }
+#ifdef PB_JIT
+        // the op's variant: its body with the schedule's constants folded in
+        switch (P.vid[oi]) {
+#define PB_JIT_CASE(id, K, S, PI, PO, NC, SR, AX, FL) \
+    case id: exec_op<T>(F, Op<K, S, PI, PO, NC, SR, AX, FL>{o}, np); break;
+            PB_JIT_OPS(PB_JIT_CASE)
+#undef PB_JIT_CASE
+            default: break;
+        }
+#else
+        exec_op<T>(F, Op<>{o}, np);
+#endif
         if (P.sync_mask >= 0 && (oi & P.sync_mask) == 0)
             __syncthreads();  // regroup the CTA's frames (shared instruction fetch)
         else
             __syncwarp();
     }
 #if PB_PROFILE
-    if (prof) P.op_cycles[P.n_ops] = clock64();
+    if (prof) P.op_cycles[LK_C(P, n_ops)] = clock64();
 #endif
 }
 
 // Persistent frame loop: a CTA holds P.fpc frames (one warp each).
 template <typename T>
-__global__ void __launch_bounds__(512, 1) k_lane(const __grid_constant__ LParams P) {
+__device__ __forceinline__ void lane_body(const LParams &P) {
     extern __shared__ __align__(16) unsigned char lk_smem[];
     const int grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long slot = (long long)blockIdx.x * P.fpc + grp;
-    unsigned char *gs = P.gscratch ? P.gscratch + (size_t)slot * P.lay.gbytes : nullptr;
-    unsigned char *sm = lk_smem + (size_t)grp * P.lay.smem_bytes;
+    unsigned char *gs = P.gscratch ? P.gscratch + (size_t)slot * LK_LAY(P).gbytes : nullptr;
+    unsigned char *sm = lk_smem + (size_t)grp * LK_LAY(P).smem_bytes;
     const long long stride = (long long)gridDim.x * P.fpc;
     const long long batch = P.batch_dev ? (long long)*P.batch_dev : P.batch;
     // (measured and dropped: a second frame group per CTA started half a
@@ -1256,7 +1323,14 @@ __global__ void __launch_bounds__(512, 1) k_lane(const __grid_constant__ LParams
     }
 }
 
-#ifndef __CUDACC_RTC__
+#ifndef PB_JIT
+template <typename T>
+__global__ void __launch_bounds__(512, 1) k_lane(const __grid_constant__ LParams P) {
+    lane_body<T>(P);
+}
+#endif
+
+#if !defined(__CUDACC_RTC__) && !defined(PB_JIT)
 template <typename T>
 cudaError_t lane_launch_t(const LParams *p, int grid, size_t smem, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k_lane<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

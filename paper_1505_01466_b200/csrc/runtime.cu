@@ -27,6 +27,7 @@
 
 #include "../../include/polar_b200.h"
 #include "decoder.cuh"
+#include "jit.h"
 
 #ifndef PB_PROFILE
 #define PB_PROFILE 0
@@ -145,6 +146,8 @@ struct pb_handle {
     int lane_fpc = 0, lane_grid = 0;
     size_t lane_smem = 0;           // per CTA
     unsigned char *d_lane_scratch = nullptr;
+    pb::jit::Kernel *jk = nullptr;  // the lane kernel specialised for this code (jit.cu), or null: generic
+    std::string jit_info;           // plan_json fragment about the specialised kernel
     // on-device frame generation: all K info positions, payload syndrome rows
     uint32_t *d_info_all = nullptr, *d_hu = nullptr;
     int crc_w = 0;
@@ -165,7 +168,7 @@ bool is_device_ptr(const void *p) {
 
 // options of the handle being created (pb_options, zero = default)
 struct Opts {
-    int kernel = 0, warps = 0, fps = 0, sync_every = 0, recompute = 0, chunk = 0, grid_sms = 0, l1_list = 0, fuse = 0;
+    int kernel = 0, warps = 0, fps = 0, sync_every = 0, recompute = 0, chunk = 0, grid_sms = 0, l1_list = 0, fuse = 0, specialize = 0;
 };
 Opts read_opts(const pb_options *o) {
     Opts r;
@@ -180,6 +183,7 @@ Opts read_opts(const pb_options *o) {
     r.l1_list = o->l1_list_kernel;
     // fields added after the first version: present when the caller's struct is long enough
     if (o->size == 0 || o->size >= (int)(offsetof(pb_options, fuse) + sizeof(int32_t))) r.fuse = o->fuse;
+    if (o->size == 0 || o->size >= (int)(offsetof(pb_options, specialize) + sizeof(int32_t))) r.specialize = o->specialize;
     return r;
 }
 // sync_every (ops, power of two) -> the kernels' barrier mask; dflt = mask
@@ -252,10 +256,17 @@ int align_up(int x, int a) { return (x + a - 1) / a * a; }
 // kernel is used) when the plan does not fit.
 static bool is_leaf_kind(int k) { return k == PB_OP_RATE0 || k == PB_OP_RATE1 || k == PB_OP_REP || k == PB_OP_SPC; }
 
-static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vector<pb::DOp> &dprog, const Opts &opt,
-                      std::string &why) {
+struct LanePlan {
+    pb::lk::LLayout lay{};
+    std::vector<pb::lk::LOp> prog;
+    int final_op = -1;
+};
+
+// Pure host part: storage layout and the lowered program (no device).
+static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_ops, const std::vector<pb::DOp> &dprog,
+                       const Opts &opt, LanePlan &out, std::string &why) {
     using namespace pb::lk;
-    const int N = h->N, n = h->n, L = h->L, mode = h->mode;
+    (void)L;
     const int es = mode == PB_MODE_F32 ? 4 : 1;
     // measured (c3 L=32): float32 3.09 Gbit/s with n-2 recomputed vs 2.86 stored;
     // int8 3.53 stored vs 2.89 recomputed (small rows, costly conversions)
@@ -400,6 +411,22 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
         why = "op program too long";
         return false;
     }
+    out.lay = lay;
+    out.prog = prog;
+    out.final_op = final_op;
+    return true;
+}
+
+static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vector<pb::DOp> &dprog, const Opts &opt,
+                      std::string &why) {
+    using namespace pb::lk;
+    const int N = h->N, n = h->n, L = h->L, mode = h->mode;
+    const int smem_cap = 227 * 1024;
+    LanePlan pl;
+    if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, opt, pl, why)) return false;
+    const LLayout &lay = pl.lay;
+    const std::vector<LOp> &prog = pl.prog;
+    const int final_op = pl.final_op;
     int fpc = std::min(16, smem_cap / std::max(16, lay.smem_bytes));
     int bps = 0;
     while (fpc >= 1) {
@@ -444,6 +471,134 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     }
     lp->gscratch = h->d_lane_scratch;
     h->lane = true;
+    // ---- the kernel specialised for this code (jit.cu); the generic kernel otherwise
+    if (opt.specialize >= 0) {
+        pb::jit::Spec sp;
+        sp.N = N, sp.n = n, sp.k = h->k, sp.L = L, sp.mode = mode;
+        sp.has_crc = lp->has_crc, sp.crc_const = lp->crc_const;
+        sp.lay = lay, sp.prog = prog, sp.final_op = final_op;
+        sp.policy = opt.specialize == 0 ? pb::jit::POL_FULL : opt.specialize;
+        std::vector<uint16_t> vid;
+        int nvar = 0;
+        const std::string src = pb::jit::generate(sp, vid, &nvar);
+        std::string err;
+        bool hit = false;
+        double secs = 0.0;
+        h->jk = pb::jit::acquire(src, true, err, &hit, &secs);
+        char jb[512];
+        if (h->jk && pb::jit::occupancy(h->jk, 32 * fpc, h->lane_smem) >= 1) {
+            std::copy(vid.begin(), vid.end(), lp->vid);
+            snprintf(jb, sizeof jb, "\"specialised\": {\"variants\": %d, \"registers\": %d, \"cache_hit\": %s, "
+                     "\"compile_s\": %.1f}", nvar, pb::jit::registers(h->jk), hit ? "true" : "false", secs);
+            h->jit_info = jb;
+        } else {
+            if (h->jk) err = "the specialised kernel does not fit one CTA per SM";
+            pb::jit::release(h->jk);
+            h->jk = nullptr;
+            if (opt.specialize > 0) {
+                why = "specialised kernel unavailable: " + err;
+                h->lane = false;
+                return false;
+            }
+            std::string e2;
+            for (char c : err.substr(0, 300)) e2 += (c == '"' || c == '\\' || c == '\n') ? ' ' : c;
+            h->jit_info = "\"specialised\": null, \"specialised_why\": \"" + e2 + "\"";
+        }
+    } else {
+        h->jit_info = "\"specialised\": null, \"specialised_why\": \"not requested\"";
+    }
+    return true;
+}
+
+// CRC syndrome rows per u position (affine map of codes.py:127-156) and the
+// constant a passing codeword's syndrome equals.  Pure host code.
+static void crc_rows(const pb_code *code, const std::vector<int> &info, int N, std::vector<uint32_t> &Hu,
+                     uint32_t &crc_const) {
+    const int w = code->crc_width;
+    Hu.assign(N, 0u);
+    crc_const = 0;
+    if (w) {
+        Crc crc{w, code->crc_poly, code->crc_init, code->crc_xor_out, code->crc_reflect != 0};
+        const int k = code->k;
+        uint32_t v = crc.step(0u, 1);  // injection of one input bit
+        for (int j = k - 1; j >= 0; --j) {
+            Hu[info[j]] = crc.append_word(v);
+            v = crc.step(v, 0);
+        }
+        uint32_t reg = crc.start();
+        for (int j = 0; j < k; ++j) reg = crc.step(reg, 0);
+        crc_const = crc.append_word(reg ^ crc.xor_out);
+        for (int j = 0; j < w; ++j) Hu[info[k + j]] = 1u << j;
+    }
+
+}
+
+// Lower the reference's op list (schedule.py:44-58) to the device program:
+// Combines are absorbed by the leaf before them, every op carries its path
+// counts.  Pure host code (no device).
+static bool lower_program(const pb_op *ops, int n_ops, int n, int L, std::vector<pb::DOp> &prog, int &final_op,
+                          int &max_hard, std::string &err) {
+    int P = 1, vstate = pb::VM_F, leaf_off = 0;
+    final_op = -1;
+    max_hard = 1;
+    for (int i = 0; i < n_ops; ++i) {
+        const pb_op &op = ops[i];
+        pb::DOp d{};
+        if (op.kind == PB_OP_F || op.kind == PB_OP_G) {
+            if (op.stage == n) {
+                vstate = op.kind == PB_OP_F ? pb::VM_F : pb::VM_G;
+                d.kind = pb::DK_NOP;
+            } else {
+                d.kind = op.kind == PB_OP_F ? pb::DK_F : pb::DK_G;
+                d.vmode = op.stage == n - 1 ? (int8_t)vstate : (int8_t)pb::VM_NONE;
+            }
+            d.stage = (int8_t)op.stage;
+            d.pin = (int8_t)P;
+            d.pout = (int8_t)P;
+            prog.push_back(d);
+            continue;
+        }
+        if (op.kind == PB_OP_COMBINE) {
+            err = "invalid schedule: Combine not preceded by a right-child leaf";
+            return false;
+        }
+        const int t = op.stage, m = op.size;
+        const int C = n_cands(op.kind, m, L);
+        d.kind = op.kind == PB_OP_RATE0 ? pb::DK_R0
+                 : op.kind == PB_OP_REP ? pb::DK_REP
+                 : op.kind == PB_OP_RATE1 ? pb::DK_R1
+                                          : pb::DK_SPC;
+        d.stage = (int8_t)t;
+        d.pin = (int8_t)P;
+        d.ncand = (int8_t)C;
+        const int pout = op.kind == PB_OP_RATE0 ? P : std::min(L, P * C);
+        d.pout = (int8_t)pout;
+        d.select = (int8_t)(op.kind != PB_OP_RATE0 && P * C > L);
+        d.vmode = t == n - 1 ? (int8_t)vstate : (int8_t)pb::VM_NONE;
+        d.off = leaf_off;
+        if ((op.kind == PB_OP_RATE1 && m > 1) || op.kind == PB_OP_SPC) max_hard = std::max(max_hard, m);
+        // chain of Combines absorbed by this leaf
+        int target = t;
+        if (op.side == 1) {
+            int j = i + 1;
+            for (;;) {
+                if (j >= n_ops || ops[j].kind != PB_OP_COMBINE || ops[j].stage != target + 1) {
+                    err = "invalid schedule: broken Combine chain";
+                    return false;
+                }
+                target = ops[j].stage;
+                int sd = ops[j].side;
+                ++j;
+                if (sd == 0 || target == n) break;
+            }
+            i = j - 1;
+        }
+        d.target = (int8_t)target;
+        leaf_off += m;
+        P = pout;
+        final_op = (int)prog.size();
+        prog.push_back(d);
+    }
     return true;
 }
 
@@ -501,82 +656,19 @@ int pb_create_ex(const pb_code *code, const pb_op *ops, int n_ops, int list_size
     h->k = code->k;
     const int L = list_size;
 
-    // ---- CRC syndrome rows per u position (affine map of codes.py:127-156)
-    std::vector<uint32_t> Hu(N, 0u);
+    // ---- CRC syndrome rows per u position
+    std::vector<uint32_t> Hu;
     uint32_t crc_const = 0;
-    if (w) {
-        Crc crc{w, code->crc_poly, code->crc_init, code->crc_xor_out, code->crc_reflect != 0};
-        const int k = code->k;
-        uint32_t v = crc.step(0u, 1);  // injection of one input bit
-        for (int j = k - 1; j >= 0; --j) {
-            Hu[info[j]] = crc.append_word(v);
-            v = crc.step(v, 0);
-        }
-        uint32_t reg = crc.start();
-        for (int j = 0; j < k; ++j) reg = crc.step(reg, 0);
-        crc_const = crc.append_word(reg ^ crc.xor_out);
-        for (int j = 0; j < w; ++j) Hu[info[k + j]] = 1u << j;
-    }
+    crc_rows(code, info, N, Hu, crc_const);
 
     // ---- lower the schedule
-    int P = 1, vstate = pb::VM_F, leaf_off = 0, final_op = -1, max_hard = 1;
-    for (int i = 0; i < n_ops; ++i) {
-        const pb_op &op = ops[i];
-        pb::DOp d{};
-        if (op.kind == PB_OP_F || op.kind == PB_OP_G) {
-            if (op.stage == n) {
-                vstate = op.kind == PB_OP_F ? pb::VM_F : pb::VM_G;
-                d.kind = pb::DK_NOP;
-            } else {
-                d.kind = op.kind == PB_OP_F ? pb::DK_F : pb::DK_G;
-                d.vmode = op.stage == n - 1 ? (int8_t)vstate : (int8_t)pb::VM_NONE;
-            }
-            d.stage = (int8_t)op.stage;
-            d.pin = (int8_t)P;
-            d.pout = (int8_t)P;
-            h->prog.push_back(d);
-            continue;
-        }
-        if (op.kind == PB_OP_COMBINE) {
+    int final_op = -1, max_hard = 1;
+    {
+        std::string err;
+        if (!lower_program(ops, n_ops, n, L, h->prog, final_op, max_hard, err)) {
             delete h;
-            return fail(PB_EINVAL, "invalid schedule: Combine not preceded by a right-child leaf");
+            return fail(PB_EINVAL, err);
         }
-        const int t = op.stage, m = op.size;
-        const int C = n_cands(op.kind, m, L);
-        d.kind = op.kind == PB_OP_RATE0 ? pb::DK_R0
-                 : op.kind == PB_OP_REP ? pb::DK_REP
-                 : op.kind == PB_OP_RATE1 ? pb::DK_R1
-                                          : pb::DK_SPC;
-        d.stage = (int8_t)t;
-        d.pin = (int8_t)P;
-        d.ncand = (int8_t)C;
-        const int pout = op.kind == PB_OP_RATE0 ? P : std::min(L, P * C);
-        d.pout = (int8_t)pout;
-        d.select = (int8_t)(op.kind != PB_OP_RATE0 && P * C > L);
-        d.vmode = t == n - 1 ? (int8_t)vstate : (int8_t)pb::VM_NONE;
-        d.off = leaf_off;
-        if ((op.kind == PB_OP_RATE1 && m > 1) || op.kind == PB_OP_SPC) max_hard = std::max(max_hard, m);
-        // chain of Combines absorbed by this leaf
-        int target = t;
-        if (op.side == 1) {
-            int j = i + 1;
-            for (;;) {
-                if (j >= n_ops || ops[j].kind != PB_OP_COMBINE || ops[j].stage != target + 1) {
-                    delete h;
-                    return fail(PB_EINVAL, "invalid schedule: broken Combine chain");
-                }
-                target = ops[j].stage;
-                int sd = ops[j].side;
-                ++j;
-                if (sd == 0 || target == n) break;
-            }
-            i = j - 1;
-        }
-        d.target = (int8_t)target;
-        leaf_off += m;
-        P = pout;
-        final_op = (int)h->prog.size();
-        h->prog.push_back(d);
     }
     // ---- storage plan
     const int es = mode == PB_MODE_F32 ? 4 : 1;
@@ -923,6 +1015,11 @@ int pb_create_ex(const pb_code *code, const pb_op *ops, int n_ops, int list_size
     } else if (h->warps != 1) {
         lane_why = "several warps per frame requested";
     }
+    if (!h->lane && opt.specialize > 0 && lane_why.rfind("specialised kernel unavailable", 0) == 0) {
+        const std::string why = lane_why;
+        pb_destroy(h);
+        return fail(PB_ECUDA, why);
+    }
     if (opt.kernel == 2 && !h->lane) {
         const std::string why = lane_why;
         pb_destroy(h);
@@ -946,15 +1043,89 @@ int pb_create_ex(const pb_code *code, const pb_op *ops, int n_ops, int list_size
         if (h->lane)
             snprintf(lb, sizeof lb,
                      ", \"lane_kernel\": {\"ops\": %d, \"smem_per_frame\": %d, \"global_scratch_per_frame\": %d, "
-                     "\"frames_per_cta\": %d, \"grid\": %d, \"alpha_global_mask\": %u, \"beta_global_mask\": %u}}",
+                     "\"frames_per_cta\": %d, \"grid\": %d, \"alpha_global_mask\": %u, \"beta_global_mask\": %u, ",
                      h->lp->n_ops, h->lp->lay.smem_bytes, h->lp->lay.gbytes, h->lane_fpc, h->lane_grid, h->lp->lay.a_gl,
                      h->lp->lay.b_gl);
         else
             snprintf(lb, sizeof lb, ", \"lane_kernel\": null, \"lane_kernel_why\": \"%s\"}", lane_why.c_str());
         h->plan_json.pop_back();
         h->plan_json += lb;
+        if (h->lane) h->plan_json += h->jit_info + "}}";
     }
     *out = h;
+    return PB_OK;
+}
+
+// ---- the specialised lane kernel without a device: its generated source
+// (tests, inspection) and a cache prebuild (build step; NVRTC needs no GPU)
+static int jit_spec_of(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
+                       const pb_options *opts, pb::jit::Spec &sp) {
+    const Opts opt = read_opts(opts);
+    if (!code || !ops || !code->frozen_mask) return fail(PB_EINVAL, "null argument");
+    if (list_size < 1 || list_size > pb::kMaxL) return fail(PB_EINVAL, "list size out of range");
+    if (mode != PB_MODE_F32 && mode != PB_MODE_INT8) return fail(PB_EINVAL, "unknown mode");
+    const int N = code->N;
+    if (N < 2 || (N & (N - 1)) || N > (1 << pb::kMaxLog)) return fail(PB_EINVAL, "bad block length");
+    int n = 0;
+    while ((1 << n) < N) ++n;
+    std::vector<int> info;
+    for (int i = 0; i < N; ++i)
+        if (!code->frozen_mask[i]) info.push_back(i);
+    if (code->k < 1 || code->k + code->crc_width != (int)info.size())
+        return fail(PB_EINVAL, "payload + CRC does not match the unfrozen positions");
+    {
+        int pos = 0;
+        std::string err;
+        if (!walk(ops, n_ops, pos, 0, N, 0, err) || pos != n_ops) return fail(PB_EINVAL, "invalid schedule: " + err);
+    }
+    std::vector<uint32_t> Hu;
+    uint32_t crc_const = 0;
+    crc_rows(code, info, N, Hu, crc_const);
+    std::vector<pb::DOp> dprog;
+    int final_op = -1, max_hard = 1;
+    std::string err;
+    if (!lower_program(ops, n_ops, n, list_size, dprog, final_op, max_hard, err)) return fail(PB_EINVAL, err);
+    LanePlan pl;
+    if (!lane_lower(N, n, list_size, mode, ops, n_ops, dprog, opt, pl, err))
+        return fail(PB_EINVAL, "lane-per-path kernel unavailable: " + err);
+    sp.N = N, sp.n = n, sp.k = code->k, sp.L = list_size, sp.mode = mode;
+    sp.has_crc = code->crc_width != 0, sp.crc_const = crc_const;
+    sp.lay = pl.lay, sp.prog = pl.prog, sp.final_op = pl.final_op;
+    sp.policy = opt.specialize <= 0 ? pb::jit::POL_FULL : opt.specialize;
+    return PB_OK;
+}
+
+int pb_jit_source(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
+                  const pb_options *opts, char *buf, int64_t cap, int64_t *needed, int32_t *n_variants) {
+    g_err.clear();
+    pb::jit::Spec sp;
+    if (int rc = jit_spec_of(code, ops, n_ops, list_size, mode, opts, sp)) return rc;
+    std::vector<uint16_t> vid;
+    int nv = 0;
+    const std::string src = pb::jit::generate(sp, vid, &nv);
+    if (needed) *needed = (int64_t)src.size() + 1;
+    if (n_variants) *n_variants = nv;
+    if (buf && cap > 0) {
+        const size_t c = std::min<size_t>((size_t)cap - 1, src.size());
+        std::memcpy(buf, src.data(), c);
+        buf[c] = 0;
+    }
+    return PB_OK;
+}
+
+int pb_jit_prebuild(const pb_code *code, const pb_op *ops, int n_ops, int list_size, int mode,
+                    const pb_options *opts, int32_t *cache_hit, double *compile_s) {
+    g_err.clear();
+    pb::jit::Spec sp;
+    if (int rc = jit_spec_of(code, ops, n_ops, list_size, mode, opts, sp)) return rc;
+    std::vector<uint16_t> vid;
+    const std::string src = pb::jit::generate(sp, vid, nullptr);
+    std::string err;
+    bool hit = false;
+    double secs = 0.0;
+    if (!pb::jit::acquire(src, false, err, &hit, &secs)) return fail(PB_ECUDA, err);
+    if (cache_hit) *cache_hit = hit;
+    if (compile_s) *compile_s = secs;
     return PB_OK;
 }
 
@@ -979,6 +1150,7 @@ int pb_destroy(pb_handle *h) {
     if (h->evs) cudaEventDestroy(h->evs);
     if (h->ev_busy) cudaEventDestroy(h->ev_busy);
     cudaFree(h->d_lane_scratch);
+    pb::jit::release(h->jk);
     delete h->lp;
     delete h;
     return PB_OK;
@@ -1048,6 +1220,17 @@ int scratch_acquire(pb_handle *h, cudaStream_t st) {
     if (h->busy_recorded) PB_CUDA(cudaStreamWaitEvent(st, h->ev_busy, 0));
     return PB_OK;
 }
+// the lane kernel: the per-code specialised build when the handle has one
+cudaError_t lane_launch(pb_handle *h, const pb::lk::LParams *lp, int grid, cudaStream_t st) {
+    if (!h->jk) return pb_lane_launch(lp, h->mode, grid, h->lane_smem, st);
+    // a batch smaller than one CTA's frame slots runs only the warps it needs (as lane_launch_t)
+    const int warps = grid == 1 && lp->batch < lp->fpc && !lp->batch_dev ? (int)lp->batch : lp->fpc;
+    std::string err;
+    const cudaError_t e = pb::jit::launch(h->jk, lp, grid, 32 * warps, h->lane_smem, st, err);
+    if (e != cudaSuccess) g_err = err;
+    return e;
+}
+
 int scratch_release(pb_handle *h, cudaStream_t st) {
     PB_CUDA(cudaEventRecord(h->ev_busy, st));
     h->busy_recorded = true;
@@ -1104,7 +1287,7 @@ int run_kernels_unordered(pb_handle *h, const pb::Params &base, int in_type, con
         lp->batch_dev = adaptive ? j.fail_count : nullptr;
         lp->op_cycles = nullptr;
         const int grid = (int)std::min<long long>(h->lane_grid, (j.batch + h->lane_fpc - 1) / h->lane_fpc);
-        cudaError_t e = pb_lane_launch(lp, h->mode, grid, h->lane_smem, st);
+        cudaError_t e = lane_launch(h, lp, grid, st);
         if (e != cudaSuccess) return cuda_fail(e, "lane decode kernel launch");
         h->launches += 1;
         return PB_OK;
@@ -1226,7 +1409,7 @@ int launch(pb_handle *h, pb::Params &pr, cudaStream_t st) {
         lp->batch_dev = nullptr;
         lp->op_cycles = pr.op_cycles;
         grid = (int)std::min<long long>(h->lane_grid, (pr.batch + h->lane_fpc - 1) / h->lane_fpc);
-        e = pb_lane_launch(lp, h->mode, grid, h->lane_smem, st);
+        e = lane_launch(h, lp, grid, st);
     } else {
         e = pb_launch_decode(&pr, h->mode, h->warps, h->ppw, h->chg, grid, h->smem_frame * h->fpc + h->prog_smem, st);
     }

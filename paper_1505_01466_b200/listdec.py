@@ -161,6 +161,69 @@ def _addr(a):
     return ctypes.c_void_p(a.ctypes.data)
 
 
+# Process-wide defaults merged under every decoder's explicit ``options``
+# (explicit Python state, nothing read from the environment): a test session
+# or a service sets e.g. ``set_default_options(specialize=-1)`` once.
+_DEFAULT_OPTIONS: dict = {}
+
+
+def set_default_options(**options) -> dict:
+    """Replace the process-wide default decoder options; returns the previous ones."""
+    global _DEFAULT_OPTIONS
+    _native.PbOptions.from_dict(options)  # validates the names
+    prev, _DEFAULT_OPTIONS = _DEFAULT_OPTIONS, dict(options)
+    return prev
+
+
+def _marshal_code(schedule: Schedule):
+    """(PbCode, PbOp array, op count, keep-alive) of a schedule for the C ABI."""
+    spec = schedule.spec
+    mask = np.ascontiguousarray(spec.frozen_mask, dtype=np.uint8)
+    crc = spec.crc
+    code = _native.PbCode(
+        spec.N, spec.k, mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+        0 if crc is None else crc.width, 0 if crc is None else crc.polynomial,
+        0 if crc is None else crc.init, 0 if crc is None else int(crc.reflect),
+        0 if crc is None else crc.xor_out)
+    arr = schedule_op_rows(schedule)
+    ops = (_native.PbOp * max(1, len(arr)))()
+    for i, row in enumerate(arr.tolist()):
+        ops[i] = _native.PbOp(*row)
+    return code, ops, len(arr), mask
+
+
+def specialised_source(schedule: Schedule, list_size: int, *, mode: str = "f32",
+                       options: dict | None = None) -> tuple[str, int]:
+    """The translation unit generated for this code's specialised lane kernel
+    (``pb_jit_source``; no GPU needed) and its number of distinct op bodies."""
+    lib = _native.lib()
+    code, ops, n, _keep = _marshal_code(schedule)
+    opts = _native.PbOptions.from_dict({**_DEFAULT_OPTIONS, **(options or {})})
+    need, nvar = ctypes.c_int64(), ctypes.c_int32()
+    m = _native.PB_MODE_INT8 if mode == "int8" else _native.PB_MODE_F32
+    _native.check(lib.pb_jit_source(ctypes.byref(code), ops, n, int(list_size), m, ctypes.byref(opts), None, 0,
+                                    ctypes.byref(need), ctypes.byref(nvar)), "pb_jit_source")
+    buf = ctypes.create_string_buffer(need.value)
+    _native.check(lib.pb_jit_source(ctypes.byref(code), ops, n, int(list_size), m, ctypes.byref(opts), buf,
+                                    need.value, None, None), "pb_jit_source")
+    return buf.value.decode(), int(nvar.value)
+
+
+def prebuild_specialised(schedule: Schedule, list_size: int, *, mode: str = "f32",
+                         options: dict | None = None) -> tuple[bool, float]:
+    """Compile this code's specialised lane kernel into the cubin cache next
+    to the library (``pb_jit_prebuild``; NVRTC needs no GPU).  Returns
+    (already cached, compile seconds)."""
+    lib = _native.lib()
+    code, ops, n, _keep = _marshal_code(schedule)
+    opts = _native.PbOptions.from_dict({**_DEFAULT_OPTIONS, **(options or {})})
+    hit, secs = ctypes.c_int32(), ctypes.c_double()
+    m = _native.PB_MODE_INT8 if mode == "int8" else _native.PB_MODE_F32
+    _native.check(lib.pb_jit_prebuild(ctypes.byref(code), ops, n, int(list_size), m, ctypes.byref(opts),
+                                      ctypes.byref(hit), ctypes.byref(secs)), "pb_jit_prebuild")
+    return bool(hit.value), float(secs.value)
+
+
 class ListDecoder:
     """List decoder over one schedule, reusable across frames
     (reference ``listdec.py:160-185``).
@@ -181,8 +244,10 @@ class ListDecoder:
         Explicit planning / launch options (``pb_options`` of the C ABI):
         ``kernel`` ("auto" | "interpreted" | "lane"), ``warps_per_frame``,
         ``frames_per_sm``, ``sync_every``, ``recompute_stages``,
-        ``chunk_frames``, ``grid_sms``, ``l1_list_kernel``; omitted = the
-        measured defaults.  Nothing is read from the environment.
+        ``chunk_frames``, ``grid_sms``, ``l1_list_kernel``, ``fuse``,
+        ``specialize`` (the lane kernel compiled per code with NVRTC: 0 auto /
+        -1 off / 1 required); omitted = the measured defaults, merged over
+        ``set_default_options``.  Nothing is read from the environment.
     """
 
     def __init__(self, schedule: Schedule, list_size: int, *, mode: str = "f32",
@@ -197,22 +262,11 @@ class ListDecoder:
         self.mode = mode
         self.device = int(device)
         lib = _native.lib()
-        spec = self.spec
-        self._mask = np.ascontiguousarray(spec.frozen_mask, dtype=np.uint8)
-        crc = spec.crc
-        code = _native.PbCode(
-            spec.N, spec.k, self._mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
-            0 if crc is None else crc.width, 0 if crc is None else crc.polynomial,
-            0 if crc is None else crc.init, 0 if crc is None else int(crc.reflect),
-            0 if crc is None else crc.xor_out)
-        arr = schedule_op_rows(schedule)
-        ops = (_native.PbOp * max(1, len(arr)))()
-        for i, row in enumerate(arr.tolist()):
-            ops[i] = _native.PbOp(*row)
-        self.options = dict(options or {})
+        code, ops, n_ops, self._mask = _marshal_code(schedule)
+        self.options = {**_DEFAULT_OPTIONS, **(options or {})}
         opts = _native.PbOptions.from_dict(self.options)
         handle = ctypes.c_void_p()
-        rc = lib.pb_create_ex(ctypes.byref(code), ops, len(arr), self.list_size,
+        rc = lib.pb_create_ex(ctypes.byref(code), ops, n_ops, self.list_size,
                               _native.PB_MODE_F32 if mode == "f32" else _native.PB_MODE_INT8,
                               self.device, ctypes.byref(opts), ctypes.byref(handle))
         _native.check(rc, "pb_create")
