@@ -94,7 +94,8 @@ typedef struct pb_options {
     int32_t l1_list_kernel;   /* 1: list size 1 through the list kernel instead of the single-path pass */
     int32_t fuse;             /* lane kernel op fusion: 0 auto (everything measured faster), -1 none, else a
                                  bit set: 1 = a leaf reads f / g of its parent's row (its own row is never
-                                 stored), 2 = an F is computed by the op producing its input row */
+                                 stored), 2 = an F is computed by the op producing its input row, 4 = a
+                                 global-scratch stage is discarded from the L2 after its last read */
     int32_t specialize;       /* lane kernel compiled per code (NVRTC, cubin cached next to the library): every
                                  distinct op of the schedule becomes one instantiation with stage, placements,
                                  offsets and path counts as constants -- the paper's unrolled decoder.

@@ -147,7 +147,10 @@ enum : uint8_t { K_F = 0, K_G = 1, K_R0 = 2, K_REP = 3, K_R1 = 4, K_SPC = 5, K_N
 // scratch, recomputed stage n-1 (f / g of the channel halves), recomputed
 // stage n-2, or the channel itself (a root leaf)
 enum : uint8_t { S_SM = 0, S_GL = 1, S_V1 = 2, S_V2 = 3, S_CH = 4 };
-enum : uint8_t { LF_SELECT = 1, LF_V1G = 2, LF_V2G = 4, LF_FUSE_F = 8, LF_FUSE_G = 16 };
+enum : uint8_t { LF_SELECT = 1, LF_V1G = 2, LF_V2G = 4, LF_FUSE_F = 8, LF_FUSE_G = 16,
+                 // this op is the last reader of the global-scratch stage it reads: the stage's
+                 // lines are discarded from the L2 afterwards (dead until rewritten: no write-back)
+                 LF_LAST = 32 };
 constexpr int LF_FUSE_SHIFT = 3;  // (flags >> 3) & 3: 0 plain leaf, 1 / 2 the F / G before it folded into its reads
 
 struct __align__(8) LOp {
@@ -158,7 +161,7 @@ struct __align__(8) LOp {
     uint8_t ncand;   // leaf: candidates per path (2 / 4 / 8; 0 for Rate-0)
     uint8_t src;     // S_*: where the input stage lives (a fused leaf: its parent's stage)
     uint8_t aux;     // F / G: S_SM / S_GL of the output stage; leaf: chain target slot (n = root)
-    uint8_t flags;   // LF_*: selection needed; recomputed stages' F / G modes
+    uint8_t flags;   // LF_*: selection needed; recomputed stages' F / G modes; fused F / G; LF_LAST
 };
 static_assert(sizeof(LOp) == 8, "LOp is one 8-byte load");
 

@@ -145,6 +145,16 @@ struct Fr {
         unsigned char *base = ((LK_LAY(P).a_gl >> s) & 1u) ? gs : sm;
         return reinterpret_cast<T *>(base + LK_LAY(P).a_off[s]) + r * 4;
     }
+    // The stored stage s (global scratch) is dead once its last reader is
+    // done: every later access is a full rewrite (each F / G covers the whole
+    // stage for all paths).  Dropping its lines from the L2 keeps them from
+    // being written back to DRAM and from pushing live rows out.
+    __device__ __forceinline__ void discard_stage(int s) const {
+        const int bytes = 32 * (s < 2 ? 4 : 1 << s) * (int)sizeof(T);
+        unsigned char *base = gs + LK_LAY(P).a_off[s];
+        for (int off = lane * 128; off < bytes; off += 32 * 128)
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + off) : "memory");
+    }
     template <int WHERE>
     __device__ __forceinline__ T *a_row_t(int s, int r) const {
         return reinterpret_cast<T *>((WHERE == S_GL ? gs : sm) + LK_LAY(P).a_off[s]) + r * 4;
@@ -462,6 +472,10 @@ __device__ __forceinline__ void fg_op(Fr<T> &F, const OP &o) {
             const RowLd<T> src{F.template a_row_t<SRC>(s, get8(F.ia, s)), 128};
             fg_body<T, IS_G, SRC == S_GL ? 8 : 4>(src, dst, bw, h);
         }
+    }
+    if (SRC == S_GL && (o.flags() & LF_LAST)) {
+        __syncwarp();
+        F.discard_stage(s);
     }
     set8(F.ia, s - 1, F.lane);
 }
@@ -999,6 +1013,7 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const OP &o) {
     long long key[8];
     if (valid) leaf_phase_a(F, o, kind, key);
     __syncwarp();
+    if ((o.flags() & LF_LAST) && o.src() == S_GL) F.discard_stage((o.flags() >> LF_FUSE_SHIFT) & 3 ? t + 1 : t);
     F.mark(0);
     const int sE = o.aux();
     if (kind == K_R0) {

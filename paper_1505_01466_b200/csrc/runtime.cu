@@ -276,8 +276,9 @@ static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_op
         why = "op program too long";
         return false;
     }
-    // op fusion (pb_options.fuse): bit 0 = leaves read f / g of their parent's row
-    const int fuse = opt.fuse < 0 ? 0 : (opt.fuse == 0 ? 1 : opt.fuse);
+    // op fusion (pb_options.fuse): bit 0 = leaves read f / g of their parent's row,
+    // bit 2 = dead global-scratch stages are discarded from the L2 after their last read
+    const int fuse = opt.fuse < 0 ? 0 : (opt.fuse == 0 ? 1 | 4 : opt.fuse);
     // a leaf folds the F / G before it into its reads when that op reads a
     // stored row or the channel (not a recomputed stage)
     auto leaf_fusable = [&](int i) {
@@ -380,7 +381,7 @@ static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_op
             l.pin = l.pout = (uint8_t)d.pin;
             l.src = src_of(s);
             l.aux = ((lay.a_gl >> (s - 1)) & 1u) ? S_GL : S_SM;
-            l.flags = flags;
+            l.flags = flags | ((fuse & 4) && op.kind == PB_OP_G && l.src == S_GL ? LF_LAST : 0);
             prog.push_back(l);
             continue;
         }
@@ -393,6 +394,8 @@ static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_op
         l.src = pend_fuse ? pend_src : op.stage == n ? S_CH : (virt(op.stage) ? S_GL : src_of(op.stage));
         l.aux = (uint8_t)d.target;
         l.flags = (uint8_t)((d.select ? LF_SELECT : 0) | (v1g ? LF_V1G : 0) | (v2g ? LF_V2G : 0) | pend_fuse);
+        // last reader of a global-scratch stage: a leaf reading its own row, or g of its parent's
+        if ((fuse & 4) && l.src == S_GL && pend_fuse != LF_FUSE_F) l.flags |= LF_LAST;
         pend_fuse = 0;
         final_op = (int)prog.size();
         prog.push_back(l);
