@@ -21,10 +21,18 @@ struct Spec {
     std::vector<lk::LOp> prog;
     int final_op = -1;
     int policy = 1;  // pb_options.specialize (> 0)
+    int fpc = 16;    // frames (warps) per CTA the kernel is compiled for: __launch_bounds__(32 * fpc, 1)
 };
 
 // policy bits beyond 1 (= everything compile-time)
-enum : int { POL_FULL = 1, POL_RT_TARGET = 2 /* leaf chain targets read at run time: fewer variants */ };
+enum : int {
+    POL_FULL = 1,
+    POL_RT_TARGET = 2,     // leaf chain targets read at run time: fewer variants
+    POL_CHAIN_LEVELS = 4,  // Combine chains level by level (default: the unrolled form, all loads independent:
+                           // c3 L=32 4.49 -> 4.62 Gbit/s)
+    POL_SCAN_PIPE2 = 8,    // wide-leaf scans software-pipelined over blocks of 2 quads
+    POL_SCAN_PIPE4 = 16,   // ... of 4 quads
+};
 
 // The generated translation unit and, per op, the variant id the kernel
 // switches on (LParams::vid).

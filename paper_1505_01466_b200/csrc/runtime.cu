@@ -382,6 +382,21 @@ static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_op
             l.src = src_of(s);
             l.aux = ((lay.a_gl >> (s - 1)) & 1u) ? S_GL : S_SM;
             l.flags = flags | ((fuse & 4) && op.kind == PB_OP_G && l.src == S_GL ? LF_LAST : 0);
+            // the F ops right below it (a left descent) join it (specialised build only)
+            if ((fuse & 2) && !out_virtual && ((fuse & 8) || (l.src != S_V1 && l.src != S_V2))) {
+                int D = 0;
+                while (D < ((fuse & 16) ? 2 : 1) && i + 1 + D < n_ops && ops[i + 1 + D].kind == PB_OP_F && ops[i + 1 + D].stage == s - 1 - D &&
+                       !leaf_fusable(i + 1 + D) && (1 << (s - 1)) >= (4 << (D + 1)))
+                    ++D;
+                if (D) {
+                    l.kind = op.kind == PB_OP_F ? K_FM : K_GM;
+                    l.ncand = (uint8_t)D;
+                    l.aux = 0;
+                    for (int q = 0; q <= D; ++q) l.aux |= ((lay.a_gl >> (s - 1 - q)) & 1u) << q;
+                    i += D;
+                    di += D;
+                }
+            }
             prog.push_back(l);
             continue;
         }
@@ -420,27 +435,92 @@ static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_op
     return true;
 }
 
+// The specialised kernel's input (jit.cu) for one code and option set: its own
+// lowering (the fusions only the specialised build implements), the frames per
+// CTA it is compiled for (its launch bound).  Pure host code, shared by
+// pb_create_ex and the device-free pb_jit_source / pb_jit_prebuild.
+static const int kLaneSmemCap = 227 * 1024;
+static bool make_jit_spec(int N, int n, int k, int L, int mode, int has_crc, uint32_t crc_const, const pb_op *ops,
+                          int n_ops, const std::vector<pb::DOp> &dprog, const Opts &opt, pb::jit::Spec &sp,
+                          LanePlan &pl, std::string &why) {
+    Opts jo = opt;
+    // auto: fused leaves + dead-stage discards.  The multi-level F / G (bits 2, 8, 16; only this build
+    // implements it) measured neutral to slower at c3 L=32 (4.48 vs 4.32-4.48 Gbit/s): off by default
+    if (opt.fuse == 0) jo.fuse = 1 | 4;
+    if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, jo, pl, why)) return false;
+    const int fps = std::max(1, std::min(32, opt.fps ? opt.fps : 16));
+    sp.N = N, sp.n = n, sp.k = k, sp.L = L, sp.mode = mode;
+    sp.has_crc = has_crc, sp.crc_const = crc_const;
+    sp.lay = pl.lay, sp.prog = pl.prog, sp.final_op = pl.final_op;
+    // auto / 1: everything compile-time, unrolled chains, wide-leaf scans pipelined over 2-quad blocks
+    // (c3 L=32: 4.61 -> 4.65 Gbit/s; 4-quad blocks 4.62); other values: explicit policy bits (jit.h)
+    sp.policy = opt.specialize <= 1 ? (pb::jit::POL_FULL | pb::jit::POL_SCAN_PIPE2) : opt.specialize;
+    sp.fpc = std::max(1, std::min(fps, kLaneSmemCap / std::max(16, pl.lay.smem_bytes)));
+    return true;
+}
+
 static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vector<pb::DOp> &dprog, const Opts &opt,
                       std::string &why) {
     using namespace pb::lk;
     const int N = h->N, n = h->n, L = h->L, mode = h->mode;
-    const int smem_cap = 227 * 1024;
     LanePlan pl;
-    if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, opt, pl, why)) return false;
+    int fpc = 0, bps = 0, nvar = 0;
+    std::vector<uint16_t> vid;
+    std::string jit_err = "not requested";
+    // ---- the kernel specialised for this code (jit.cu) ...
+    if (opt.specialize >= 0) {
+        pb::jit::Spec sp;
+        LanePlan jp;
+        std::string jwhy;
+        if (make_jit_spec(N, n, h->k, L, mode, h->base.has_crc, h->base.crc_const, ops, n_ops, dprog, opt, sp, jp,
+                          jwhy)) {
+            const std::string src = pb::jit::generate(sp, vid, &nvar);
+            bool hit = false;
+            double secs = 0.0;
+            h->jk = pb::jit::acquire(src, true, jit_err, &hit, &secs);
+            if (h->jk && pb::jit::occupancy(h->jk, 32 * sp.fpc, (size_t)sp.fpc * jp.lay.smem_bytes) >= 1) {
+                pl = jp;
+                fpc = sp.fpc;
+                bps = 1;
+                char jb[512];
+                snprintf(jb, sizeof jb, "\"specialised\": {\"variants\": %d, \"registers\": %d, \"cache_hit\": %s, "
+                         "\"compile_s\": %.1f}", nvar, pb::jit::registers(h->jk), hit ? "true" : "false", secs);
+                h->jit_info = jb;
+            } else {
+                if (h->jk) jit_err = "the specialised kernel does not fit one CTA per SM";
+                pb::jit::release(h->jk);
+                h->jk = nullptr;
+            }
+        } else {
+            jit_err = jwhy;
+        }
+        if (!h->jk && opt.specialize > 0) {
+            why = "specialised kernel unavailable: " + jit_err;
+            return false;
+        }
+    }
+    // ---- ... or the generic kernel (compiled for 16 frames per CTA)
+    if (!h->jk) {
+        Opts go = opt;
+        go.fps = std::min(16, opt.fps ? opt.fps : 16);
+        if (go.fuse > 0) go.fuse &= ~2;  // multi-level F / G: specialised build only
+        if (go.fuse == 0 && opt.fuse > 0) go.fuse = -1;
+        if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, go, pl, why)) return false;
+        fpc = std::min(go.fps, kLaneSmemCap / std::max(16, pl.lay.smem_bytes));
+        while (fpc >= 1) {
+            if (pb_lane_occupancy(mode, (size_t)fpc * pl.lay.smem_bytes, fpc, &bps) == cudaSuccess && bps >= 1) break;
+            cudaGetLastError();
+            --fpc;
+        }
+        if (fpc < 1) {
+            why = "no resident CTA";
+            return false;
+        }
+        std::string e2;
+        for (char c : jit_err.substr(0, 300)) e2 += (c == '"' || c == '\\' || c == '\n') ? ' ' : c;
+        h->jit_info = "\"specialised\": null, \"specialised_why\": \"" + e2 + "\"";
+    }
     const LLayout &lay = pl.lay;
-    const std::vector<LOp> &prog = pl.prog;
-    const int final_op = pl.final_op;
-    int fpc = std::min(16, smem_cap / std::max(16, lay.smem_bytes));
-    int bps = 0;
-    while (fpc >= 1) {
-        if (pb_lane_occupancy(mode, (size_t)fpc * lay.smem_bytes, fpc, &bps) == cudaSuccess && bps >= 1) break;
-        cudaGetLastError();
-        --fpc;
-    }
-    if (fpc < 1) {
-        why = "no resident CTA";
-        return false;
-    }
     LParams *lp = new LParams();
     std::memset(lp, 0, sizeof(LParams));
     lp->xsyn4 = h->d_xsyn4;
@@ -451,13 +531,16 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     lp->L = L;
     lp->has_crc = h->base.has_crc;
     lp->crc_const = h->base.crc_const;
-    lp->n_ops = (int)prog.size();
-    lp->final_op = final_op;
+    lp->n_ops = (int)pl.prog.size();
+    lp->final_op = pl.final_op;
     lp->fpc = fpc;
-    // regroup every 8 ops (measured c3 L=32: every 8 3.23, 32 3.09, 4 3.12, never 2.46 Gbit/s)
-    lp->sync_mask = fpc > 1 ? sync_mask_of(opt.sync_every, 7) : -1;
+    // CTA regroup period in ops.  Generic kernel: every 8 (measured c3 L=32: every 8 3.23, 32 3.09,
+    // 4 3.12, never 2.46 Gbit/s); the specialised kernel has fewer, longer ops: every 32 (every 4
+    // 4.19, 8 4.31, 16 4.42, 32 4.48, never 3.98 Gbit/s)
+    lp->sync_mask = fpc > 1 ? sync_mask_of(opt.sync_every, h->jk ? 31 : 7) : -1;
     lp->lay = lay;
-    std::copy(prog.begin(), prog.end(), lp->prog);
+    std::copy(pl.prog.begin(), pl.prog.end(), lp->prog);
+    if (h->jk) std::copy(vid.begin(), vid.end(), lp->vid);
     h->lp = lp;
     h->lane_fpc = fpc;
     h->lane_grid = h->sms * bps;
@@ -468,48 +551,14 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
             cudaGetLastError();
             delete lp;
             h->lp = nullptr;
+            pb::jit::release(h->jk);
+            h->jk = nullptr;
             why = "scratch allocation failed";
             return false;
         }
     }
     lp->gscratch = h->d_lane_scratch;
     h->lane = true;
-    // ---- the kernel specialised for this code (jit.cu); the generic kernel otherwise
-    if (opt.specialize >= 0) {
-        pb::jit::Spec sp;
-        sp.N = N, sp.n = n, sp.k = h->k, sp.L = L, sp.mode = mode;
-        sp.has_crc = lp->has_crc, sp.crc_const = lp->crc_const;
-        sp.lay = lay, sp.prog = prog, sp.final_op = final_op;
-        sp.policy = opt.specialize == 0 ? pb::jit::POL_FULL : opt.specialize;
-        std::vector<uint16_t> vid;
-        int nvar = 0;
-        const std::string src = pb::jit::generate(sp, vid, &nvar);
-        std::string err;
-        bool hit = false;
-        double secs = 0.0;
-        h->jk = pb::jit::acquire(src, true, err, &hit, &secs);
-        char jb[512];
-        if (h->jk && pb::jit::occupancy(h->jk, 32 * fpc, h->lane_smem) >= 1) {
-            std::copy(vid.begin(), vid.end(), lp->vid);
-            snprintf(jb, sizeof jb, "\"specialised\": {\"variants\": %d, \"registers\": %d, \"cache_hit\": %s, "
-                     "\"compile_s\": %.1f}", nvar, pb::jit::registers(h->jk), hit ? "true" : "false", secs);
-            h->jit_info = jb;
-        } else {
-            if (h->jk) err = "the specialised kernel does not fit one CTA per SM";
-            pb::jit::release(h->jk);
-            h->jk = nullptr;
-            if (opt.specialize > 0) {
-                why = "specialised kernel unavailable: " + err;
-                h->lane = false;
-                return false;
-            }
-            std::string e2;
-            for (char c : err.substr(0, 300)) e2 += (c == '"' || c == '\\' || c == '\n') ? ' ' : c;
-            h->jit_info = "\"specialised\": null, \"specialised_why\": \"" + e2 + "\"";
-        }
-    } else {
-        h->jit_info = "\"specialised\": null, \"specialised_why\": \"not requested\"";
-    }
     return true;
 }
 
@@ -1089,12 +1138,9 @@ static int jit_spec_of(const pb_code *code, const pb_op *ops, int n_ops, int lis
     std::string err;
     if (!lower_program(ops, n_ops, n, list_size, dprog, final_op, max_hard, err)) return fail(PB_EINVAL, err);
     LanePlan pl;
-    if (!lane_lower(N, n, list_size, mode, ops, n_ops, dprog, opt, pl, err))
+    if (!make_jit_spec(N, n, code->k, list_size, mode, code->crc_width != 0, crc_const, ops, n_ops, dprog, opt, sp, pl,
+                       err))
         return fail(PB_EINVAL, "lane-per-path kernel unavailable: " + err);
-    sp.N = N, sp.n = n, sp.k = code->k, sp.L = list_size, sp.mode = mode;
-    sp.has_crc = code->crc_width != 0, sp.crc_const = crc_const;
-    sp.lay = pl.lay, sp.prog = pl.prog, sp.final_op = pl.final_op;
-    sp.policy = opt.specialize <= 0 ? pb::jit::POL_FULL : opt.specialize;
     return PB_OK;
 }
 

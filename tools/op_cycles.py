@@ -17,7 +17,7 @@ lib.pb_profile_ops.restype = ctypes.c_int
 lib.pb_profile_ops.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
 n = lib.pb_device_op_count(dec._h)
-fb = pb.generate_frames(spec, ebn0, seed=1, start=0, count=4096)
+fb = pb.generate_frames(spec, ebn0, seed=1, start=0, count=int(os.environ.get('OPC_FRAMES', 4096)))
 llr = np.ascontiguousarray(fb.llrs)
 cyc4 = np.zeros((n, 12), np.int64); kinds = np.zeros(n, np.int8); stages = np.zeros(n, np.int8)
 rc = lib.pb_profile_ops(dec._h, llr.ctypes.data, 0, len(llr), cyc4.ctypes.data, kinds.ctypes.data, stages.ctypes.data)
@@ -25,7 +25,7 @@ _native.check(rc, 'pb_profile_ops')
 if os.environ.get('OPC_STRIDE') == '4':  # older builds: 4 longs per op
     cyc4 = np.concatenate([cyc4.ravel()[:4 * n].reshape(n, 4), np.zeros((n, 8), np.int64)], 1)
 cyc = cyc4[:, 0]
-names = {0: 'F', 1: 'G', 2: 'R0', 3: 'REP', 4: 'R1', 5: 'SPC', 6: 'NOP'}
+names = {0: 'F', 1: 'G', 2: 'R0', 3: 'REP', 4: 'R1', 5: 'SPC', 6: 'NOP', 7: 'FM', 8: 'GM'}
 tot = cyc.sum()
 print(f'{cfg}: {n} device ops, {tot} cycles for one frame (CTA 0, warps sharing the SM)')
 agg = collections.defaultdict(lambda: [0, 0])
