@@ -102,6 +102,9 @@ typedef struct pb_options {
                                  0 auto (on; the generic kernel runs if NVRTC is unavailable), -1 off
                                  (generic kernel), 1 on (PB_ECUDA if it cannot be built), 3 = on with leaf
                                  Combine-chain targets read at run time (fewer variants) */
+    int32_t frames_per_warp;  /* specialised lane kernel, list sizes <= 16: this many frames share one warp
+                                 (lane = frame slot x path slot; at most 32 / pow2(L)); 0 / 1 = one frame per
+                                 warp through the interpreted kernel */
 } pb_options;
 
 /* Build a decoder for (code, schedule, list size) on a CUDA device.

@@ -214,6 +214,7 @@ struct JitCode {
     int N, n, k, L, has_crc;
     uint32_t crc_const;
     int n_ops, final_op;
+    int G;  // frames per warp
 };
 }  // namespace lk
 

@@ -21,7 +21,8 @@ struct Spec {
     std::vector<lk::LOp> prog;
     int final_op = -1;
     int policy = 1;  // pb_options.specialize (> 0)
-    int fpc = 16;    // frames (warps) per CTA the kernel is compiled for: __launch_bounds__(32 * fpc, 1)
+    int G = 1;       // frames per warp (list sizes <= 16): lane = frame slot * 32/G + path slot
+    int fpc = 16;    // warps per CTA the kernel is compiled for: __launch_bounds__(32 * fpc, 1)
 };
 
 // policy bits beyond 1 (= everything compile-time)

@@ -52,9 +52,17 @@
 #ifdef PB_JIT
 #define LK_LAY(P) (::pb::lk::kLay)
 #define LK_C(P, f) (::pb::lk::kJit.f)
+// frames per warp (list sizes <= 16: a warp's 32 lanes = G frames x 32/G path
+// slots; lane = frame slot * 32/G + path slot).  The warp's 32 row slots, the
+// row-index bytes, the hard-word columns and the survivor tables are indexed
+// by lane as before; selection, the survivor scan and the final pick work on
+// the lanes of one frame (segment masks); each frame has its own channel,
+// the G channels interleaved quad by quad.
+#define LK_G (::pb::lk::kJit.G)
 #else
 #define LK_LAY(P) ((P).lay)
 #define LK_C(P, f) ((P).f)
+#define LK_G 1  // the generic kernel: one frame per warp
 #endif
 
 namespace pb {
@@ -134,7 +142,17 @@ struct Fr {
         if (marks) marks[k] = clock64();
 #endif
     }
-    __device__ __forceinline__ T *channel() const { return reinterpret_cast<T *>(sm + LK_LAY(P).ch_off); }
+    // frames per warp, path slots per frame, channel quad stride (elements)
+    static constexpr int G = LK_G, LP = 32 / LK_G, CQ = 4 * LK_G;
+    __device__ __forceinline__ int base() const { return G == 1 ? 0 : lane & ~(LP - 1); }  // frame's first lane
+    __device__ __forceinline__ int slot() const { return G == 1 ? lane : lane & (LP - 1); }  // path slot in its frame
+    __device__ __forceinline__ unsigned seg() const {  // the lanes of this lane's frame
+        return G == 1 ? FULL_MASK : ((1u << LP) - 1u) << base();
+    }
+    // this lane's frame's channel: quad x at channel() + x * CQ
+    __device__ __forceinline__ T *channel() const {
+        return reinterpret_cast<T *>(sm + LK_LAY(P).ch_off) + (G == 1 ? 0 : 4 * (lane / LP));
+    }
     // hard-decision words of leaves wider than 32 (global scratch): word w of
     // lane q's path at [w * 32 + q]
     __device__ __forceinline__ uint32_t *hard_words() const {
@@ -175,6 +193,13 @@ struct RowLd {  // a stored row (quad stride 128: 32 interleaved rows) or the ch
     __device__ __forceinline__ void quad(int x, float (&v)[4]) const { V4<T>::ld(p + x * qs, v); }
     __device__ __forceinline__ float get(int i) const { return Elem<T>::ld(p + (i >> 2) * qs + (i & 3)); }
 };
+// channel addressing: quad x of a frame's channel at ch + x * CQ (CQ = 4 with
+// one frame per warp; the frames of a warp interleave quad by quad)
+constexpr int CQ = 4 * LK_G;
+template <typename T>
+__device__ __forceinline__ const T *che(const T *ch, int i) {
+    return ch + (i >> 2) * CQ + (i & 3);
+}
 // stage n-1: f or g of the channel halves (g with the path's left-half bits,
 // beta slot n-1)
 template <typename T, int MODE = -1>  // MODE >= 0: g known at compile time (MODE & 1)
@@ -186,8 +211,8 @@ struct V1Ld {
     __device__ __forceinline__ bool gm() const { return MODE >= 0 ? (MODE & 1) != 0 : g_; }
     __device__ __forceinline__ void quad(int x, float (&v)[4]) const {
         float a[4], b[4];
-        V4<T>::ld(ch + 4 * x, a);
-        V4<T>::ld(ch + 4 * x + half, b);
+        V4<T>::ld(ch + CQ * x, a);
+        V4<T>::ld(ch + CQ * (x + (half >> 2)), b);
         if (gm()) {
             const unsigned bits = b1[x >> 3] >> ((x & 7) * 4);
 #pragma unroll
@@ -198,7 +223,7 @@ struct V1Ld {
         }
     }
     __device__ __forceinline__ float get(int i) const {
-        const float a = Elem<T>::ld(ch + i), b = Elem<T>::ld(ch + i + half);
+        const float a = Elem<T>::ld(che(ch, i)), b = Elem<T>::ld(che(ch, i + half));
         return gm() ? g_op<T>(a, b, (b1[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
     }
     // beta words of the 8-quad block starting at quad x (x % 8 == 0), loaded
@@ -209,8 +234,8 @@ struct V1Ld {
     __device__ __forceinline__ Words words(int x) const { return Words{gm() ? b1[x >> 3] : 0u}; }
     __device__ __forceinline__ void quadw(int x, float (&v)[4], const Words &w) const {
         float a[4], b[4];
-        V4<T>::ld(ch + 4 * x, a);
-        V4<T>::ld(ch + 4 * x + half, b);
+        V4<T>::ld(ch + CQ * x, a);
+        V4<T>::ld(ch + CQ * (x + (half >> 2)), b);
         if (gm()) {
             const unsigned bits = w.w1 >> ((x & 7) * 4);
 #pragma unroll
@@ -234,10 +259,10 @@ struct V2Ld {
     __device__ __forceinline__ bool m2() const { return MODE >= 0 ? (MODE & 2) != 0 : g2_; }
     __device__ __forceinline__ void quad(int x, float (&v)[4]) const {
         float c0[4], c1[4], c2[4], c3[4];
-        V4<T>::ld(ch + 4 * x, c0);
-        V4<T>::ld(ch + 4 * x + q, c1);
-        V4<T>::ld(ch + 4 * x + 2 * q, c2);
-        V4<T>::ld(ch + 4 * x + 3 * q, c3);
+        V4<T>::ld(ch + CQ * x, c0);
+        V4<T>::ld(ch + CQ * (x + (q >> 2)), c1);
+        V4<T>::ld(ch + CQ * (x + (q >> 1)), c2);
+        V4<T>::ld(ch + CQ * (x + 3 * (q >> 2)), c3);
         float u0[4], u1[4];
         if (m1()) {
             const unsigned bl = b1[x >> 3] >> ((x & 7) * 4);
@@ -265,7 +290,7 @@ struct V2Ld {
         }
     }
     __device__ __forceinline__ float v1(int i) const {
-        const float a = Elem<T>::ld(ch + i), b = Elem<T>::ld(ch + i + 2 * q);
+        const float a = Elem<T>::ld(che(ch, i)), b = Elem<T>::ld(che(ch, i + 2 * q));
         return m1() ? g_op<T>(a, b, (b1[i >> 5] >> (i & 31)) & 1u) : f_op(a, b);
     }
     __device__ __forceinline__ float get(int i) const {
@@ -280,10 +305,10 @@ struct V2Ld {
     }
     __device__ __forceinline__ void quadw(int x, float (&v)[4], const Words &w) const {
         float c0[4], c1[4], c2[4], c3[4];
-        V4<T>::ld(ch + 4 * x, c0);
-        V4<T>::ld(ch + 4 * x + q, c1);
-        V4<T>::ld(ch + 4 * x + 2 * q, c2);
-        V4<T>::ld(ch + 4 * x + 3 * q, c3);
+        V4<T>::ld(ch + CQ * x, c0);
+        V4<T>::ld(ch + CQ * (x + (q >> 2)), c1);
+        V4<T>::ld(ch + CQ * (x + (q >> 1)), c2);
+        V4<T>::ld(ch + CQ * (x + 3 * (q >> 2)), c3);
         const int sh = (x & 7) * 4;
         float u0[4], u1[4];
         if (m1()) {
@@ -388,7 +413,7 @@ __device__ __forceinline__ LeafLd<T> leaf_src(const Fr<T> &F, const OP &o, int t
     const int mode = (o.flags() >> LF_FUSE_SHIFT) & 3;
     const int ps = mode ? t + 1 : t;
     const uint32_t *bw = mode == 2 ? F.beta_row(t, get8(F.ib, t)) : nullptr;
-    if (o.src() == S_CH) return LeafLd<T>{F.channel(), 4, mode, 1 << t, bw};
+    if (o.src() == S_CH) return LeafLd<T>{F.channel(), CQ, mode, 1 << t, bw};
     return LeafLd<T>{F.a_row(ps, get8(ia, ps)), 128, mode, 1 << t, bw};
 }
 
@@ -469,7 +494,7 @@ __device__ __forceinline__ void fg_body_v(const S &src, T *dst, const uint32_t *
 template <typename T, bool IS_G, int SRC, int DST, class OP>
 __device__ __forceinline__ void fg_op(Fr<T> &F, const OP &o) {
     const int s = o.stage(), h = 1 << (s - 1);
-    if (F.lane < o.pin()) {
+    if (F.slot() < o.pin()) {
         T *dst = F.template a_row_t<DST>(s - 1, F.lane);
         const uint32_t *bw = IS_G ? F.beta_row(s - 1, get8(F.ib, s - 1)) : nullptr;
         if (SRC == S_V2) {
@@ -495,7 +520,7 @@ __device__ __forceinline__ void fg_op(Fr<T> &F, const OP &o) {
             else
                 fg_body_v<T, IS_G, 4>(V1Ld<T, 0>{v.ch, v.b1, v.half, false}, dst, bw, h);
         } else if (SRC == S_CH) {
-            fg_body<T, IS_G, 4>(RowLd<T>{F.channel(), 4}, dst, bw, h);
+            fg_body<T, IS_G, 4>(RowLd<T>{F.channel(), CQ}, dst, bw, h);
         } else {
             const RowLd<T> src{F.template a_row_t<SRC>(s, get8(F.ia, s)), 128};
             fg_body<T, IS_G, SRC == S_GL ? 8 : 4>(src, dst, bw, h);
@@ -554,7 +579,7 @@ __device__ __forceinline__ void fgm_body(const S &src, T *d1, T *d2, T *d3, cons
 template <typename T, bool IS_G, int SRC, int D, int GLM, class OP>
 __device__ __forceinline__ void fgm_op(Fr<T> &F, const OP &o) {
     const int s = o.stage(), h = 1 << (s - 1);
-    if (F.lane < o.pin()) {
+    if (F.slot() < o.pin()) {
         T *d1 = F.template a_row_t<(GLM & 1) ? S_GL : S_SM>(s - 1, F.lane);
         T *d2 = F.template a_row_t<(GLM & 2) ? S_GL : S_SM>(s - 2, F.lane);
         T *d3 = D == 2 ? F.template a_row_t<(GLM & 4) ? S_GL : S_SM>(s - 3, F.lane) : nullptr;
@@ -574,7 +599,7 @@ __device__ __forceinline__ void fgm_op(Fr<T> &F, const OP &o) {
             else
                 fgm_body<T, IS_G, D>(V1Ld<T, 0>{v.ch, v.b1, v.half, false}, d1, d2, d3, bw, h);
         } else if (SRC == S_CH) {
-            fgm_body<T, IS_G, D>(RowLd<T>{F.channel(), 4}, d1, d2, d3, bw, h);
+            fgm_body<T, IS_G, D>(RowLd<T>{F.channel(), CQ}, d1, d2, d3, bw, h);
         } else {
             fgm_body<T, IS_G, D>(RowLd<T>{F.template a_row_t<SRC>(s, get8(F.ia, s)), 128}, d1, d2, d3, bw, h);
         }
@@ -929,8 +954,32 @@ __device__ __forceinline__ int hi27(long long k) { return (int)(k >> 32) & ~31; 
 // names both lanes (no ballots): 2 independent REDUX per iteration.  Every
 // candidate whose prefix is > Th survives; among those == Th the `need`
 // best by full key survive, ties to the earlier (source, cand).
+// 64-bit max / min and the 4-bit exclusive scan over the lanes of one frame
+__device__ __forceinline__ long long seg_max_ll(long long v, unsigned seg) {
+    const int hi = (int)(v >> 32);
+    const int mh = __reduce_max_sync(seg, hi);
+    const unsigned ml = __reduce_max_sync(seg, hi == mh ? (unsigned)v : 0u);
+    return ((long long)mh << 32) | ml;
+}
+__device__ __forceinline__ long long seg_min_ll(long long v, unsigned seg) {
+    const int hi = (int)(v >> 32);
+    const int mh = __reduce_min_sync(seg, hi);
+    const unsigned ml = __reduce_min_sync(seg, hi == mh ? (unsigned)v : 0xffffffffu);
+    return ((long long)mh << 32) | ml;
+}
+__device__ __forceinline__ int seg_excl_scan4(int v, int lane, unsigned seg) {
+    const unsigned below = ((1u << lane) - 1u) & seg;
+    int r = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) r += __popc(__ballot_sync(FULL_MASK, (v >> b) & 1) & below) << b;
+    return r;
+}
+
+// (lane = the warp lane: it tags the keys; slot = the path slot within the
+// frame; seg = the frame's lanes: every reduction runs over them only)
 template <int C>
-__device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool valid, int L, int lane) {
+__device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool valid, int L, int lane, int slot,
+                                                unsigned seg) {
     int srt[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) srt[c] = (valid ? hi27(key[c]) : INT_MIN) | lane;
@@ -951,13 +1000,13 @@ __device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool 
         cs(2, 4); cs(3, 5);
         cs(1, 2); cs(3, 4); cs(5, 6);
     }
-    int kept = lane < L ? ((srt[0] & ~31) | lane) : INT_MAX;
+    int kept = slot < L ? ((srt[0] & ~31) | lane) : INT_MAX;
 #pragma unroll
     for (int c = 0; c < C; ++c) srt[c] = c + 1 < C ? srt[c + 1 < C ? c + 1 : c] : (INT_MIN | lane);
     int worst;
     for (;;) {
-        const int best = __reduce_max_sync(FULL_MASK, srt[0]);
-        worst = __reduce_min_sync(FULL_MASK, kept);
+        const int best = __reduce_max_sync(seg, srt[0]);
+        worst = __reduce_min_sync(seg, kept);
         if ((best & ~31) <= (worst & ~31)) break;
         if (lane == (best & 31)) {
 #pragma unroll
@@ -978,8 +1027,8 @@ __device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool 
             bmask |= 1u << c;
         }
     }
-    const int need = L - (int)__reduce_add_sync(FULL_MASK, (unsigned)gt);
-    const int eqt = (int)__reduce_add_sync(FULL_MASK, (unsigned)__popc(bmask));
+    const int need = L - (int)__reduce_add_sync(seg, (unsigned)gt);
+    const int eqt = (int)__reduce_add_sync(seg, (unsigned)__popc(bmask));
     if (eqt <= need) return mask | bmask;  // the usual case: no surplus at the threshold
     // surplus at Th: full keys decide, then (source, cand)
     long long bmax = LLONG_MIN, bmin = LLONG_MAX;
@@ -989,9 +1038,9 @@ __device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool 
             bmax = max(bmax, key[c]);
             bmin = min(bmin, key[c]);
         }
-    if (warp_max_ll(bmax) == warp_min_ll(bmin)) {
+    if (seg_max_ll(bmax, seg) == seg_min_ll(bmin, seg)) {
         // all tied exactly (int8 mode): the earliest `need` in (source, cand) order
-        int r = excl_scan4(__popc(bmask), lane);
+        int r = seg_excl_scan4(__popc(bmask), lane, seg);
 #pragma unroll
         for (int c = 0; c < C; ++c)
             if ((bmask >> c) & 1u) {
@@ -1010,8 +1059,8 @@ __device__ __forceinline__ unsigned select_mask(const long long (&key)[8], bool 
                 mine = key[c];
                 mc = c;
             }
-        const long long best = warp_max_ll(mine);
-        const int from = __ffs(__ballot_sync(FULL_MASK, mc >= 0 && mine == best)) - 1;
+        const long long best = seg_max_ll(mine, seg);
+        const int from = __ffs(__ballot_sync(seg, mc >= 0 && mine == best) & seg) - 1;
         if (lane == from) {
             mask |= 1u << mc;
             bmask &= ~(1u << mc);
@@ -1157,7 +1206,7 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const OP &o) {
     const int t = o.stage();
     int kind = o.kind();
     if (kind == K_R1 && t == 0) kind = K_REP;  // listdec.py:347
-    const bool valid = F.lane < o.pin();
+    const bool valid = F.slot() < o.pin();
     long long key[8];
     if (valid) leaf_phase_a(F, o, kind, key);
     __syncwarp();
@@ -1178,17 +1227,17 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const OP &o) {
     if (!(o.flags() & LF_SELECT)) {
         mask = valid ? (1u << C) - 1u : 0u;
     } else if (C == 2) {
-        mask = select_mask<2>(key, valid, LK_C(P, L), F.lane);
+        mask = select_mask<2>(key, valid, LK_C(P, L), F.lane, F.slot(), F.seg());
     } else if (C == 4) {
-        mask = select_mask<4>(key, valid, LK_C(P, L), F.lane);
+        mask = select_mask<4>(key, valid, LK_C(P, L), F.lane, F.slot(), F.seg());
     } else {
-        mask = select_mask<8>(key, valid, LK_C(P, L), F.lane);
+        mask = select_mask<8>(key, valid, LK_C(P, L), F.lane, F.slot(), F.seg());
     }
     F.mark(1);
     // survivors in (source, cand) order: this lane's go to slots off ..
     uint8_t *asg = F.sm + LK_LAY(P).asg_off;
     double *met = reinterpret_cast<double *>(F.sm + LK_LAY(P).met_off);
-    int k = excl_scan4(__popc(mask), F.lane);
+    int k = F.base() + seg_excl_scan4(__popc(mask), F.lane, F.seg());
     while (mask) {
         const int c = __ffs(mask) - 1;
         mask &= mask - 1;
@@ -1197,7 +1246,7 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const OP &o) {
         ++k;
     }
     __syncwarp();
-    const bool live = F.lane < o.pout();
+    const bool live = F.slot() < o.pout();
     int p = F.lane, c = 0;
     double pmn = F.pm;
     if (live) {
@@ -1276,11 +1325,12 @@ __device__ __forceinline__ uint32_t syndrome(const LParams &P, const uint32_t *x
 // listdec.py:289-308: among CRC-passing survivors the strictly greater
 // metric wins, earliest survivor on ties; with none passing, the best metric
 // overall -- survivors visited by (metric desc, index asc), first pass wins.
+// The whole warp works on the frame whose survivors are lanes b0 .. b0 + np - 1.
 template <typename T>
-__device__ __forceinline__ void finalize(Fr<T> &F, long long f, int np) {
+__device__ __forceinline__ void finalize(Fr<T> &F, long long f, int np, int b0) {
     const LParams &P = F.P;
     const int lane = F.lane;
-    const bool live = lane < np;
+    const bool live = lane >= b0 && lane < b0 + np;
     const double pmk = live ? F.pm : -INFINITY;
     uint32_t *u = reinterpret_cast<uint32_t *>(F.sm + LK_LAY(P).root_off);
     const int rw = LK_C(P, N) >= 32 ? LK_C(P, N) >> 5 : 1;
@@ -1289,11 +1339,11 @@ __device__ __forceinline__ void finalize(Fr<T> &F, long long f, int np) {
             uint32_t *dst = P.path_cw + ((size_t)f * LK_C(P, L) + kk) * rw;
             if (LK_C(P, N) < 32 && lane == 0) dst[0] = 0u;
             __syncwarp();
-            build_root(F, kk, dst);
+            build_root(F, b0 + kk, dst);
             const uint32_t syn = syndrome(P, dst, lane);
             if (lane == 0) P.path_crc[(size_t)f * LK_C(P, L) + kk] = LK_C(P, has_crc) && syn == LK_C(P, crc_const);
         }
-        if (live) P.path_pm[(size_t)f * LK_C(P, L) + lane] = pmk;
+        if (live) P.path_pm[(size_t)f * LK_C(P, L) + lane - b0] = pmk;
         __syncwarp();
     }
     unsigned tried = 0u;
@@ -1357,10 +1407,11 @@ __device__ __forceinline__ void finalize(Fr<T> &F, long long f, int np) {
 
 template <typename T>
 __device__ __forceinline__ void load_channel_lane(const LParams &P, T *ch, long long f, int lane) {
+    // ch: the frame's channel, quad x at ch + x * CQ (element i at che(ch, i))
     const int N = LK_C(P, N);
     if (P.in_type == PB_IN_I8) {
         const int8_t *src = reinterpret_cast<const int8_t *>(P.llr) + (size_t)f * N;
-        for (int i = lane; i < N; i += 32) ch[i] = (T)src[i];
+        for (int i = lane; i < N; i += 32) ch[(i >> 2) * CQ + (i & 3)] = (T)src[i];
         return;
     }
     const float *src = reinterpret_cast<const float *>(P.llr) + (size_t)f * N;
@@ -1369,10 +1420,10 @@ __device__ __forceinline__ void load_channel_lane(const LParams &P, T *ch, long 
         for (int i = lane; i < (N >> 2); i += 32) {
             const float4 v = __ldcs(s4 + i);  // read once: evict-first
             float q[4] = {ingest<T>(v.x), ingest<T>(v.y), ingest<T>(v.z), ingest<T>(v.w)};
-            V4<T>::st(ch + 4 * i, q);
+            V4<T>::st(ch + CQ * i, q);
         }
     } else {
-        for (int i = lane; i < N; i += 32) Elem<T>::st(ch + i, ingest<T>(src[i]));
+        for (int i = lane; i < N; i += 32) Elem<T>::st(ch + (i >> 2) * CQ + (i & 3), ingest<T>(src[i]));
     }
 }
 
@@ -1465,26 +1516,32 @@ __device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
 template <typename T>
 __device__ __forceinline__ void lane_body(const LParams &P) {
     extern __shared__ __align__(16) unsigned char lk_smem[];
+    constexpr int G = LK_G, LP = 32 / LK_G;  // frames per warp, path slots per frame
     const int grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long slot = (long long)blockIdx.x * P.fpc + grp;
     unsigned char *gs = P.gscratch ? P.gscratch + (size_t)slot * LK_LAY(P).gbytes : nullptr;
     unsigned char *sm = lk_smem + (size_t)grp * LK_LAY(P).smem_bytes;
-    const long long stride = (long long)gridDim.x * P.fpc;
+    const long long per_cta = (long long)P.fpc * G, stride = (long long)gridDim.x * per_cta;
     const long long batch = P.batch_dev ? (long long)*P.batch_dev : P.batch;
     // (measured and dropped: a second frame group per CTA started half a
     // program late, and CTAs started at staggered ops: +2 % / -2 % device
     // rate, both costing a throwaway half frame per launch)
-    for (long long f0 = (long long)blockIdx.x * P.fpc; f0 < batch; f0 += stride) {
-        // tail: idle slots decode the last frame again and write nothing
-        const long long fi = f0 + grp < batch ? f0 + grp : batch - 1;
-        const long long f = P.frame_map ? (long long)P.frame_map[fi] : fi;
-        const bool own = f0 + grp < batch;
+    for (long long f0 = (long long)blockIdx.x * per_cta; f0 < batch; f0 += stride) {
         Fr<T> F(P, sm, gs);
-        load_channel_lane<T>(P, F.channel(), f, lane);
+        // tail: idle frame slots decode the last frame again and write nothing
+        auto frame_of = [&](int g) {
+            const long long fi = f0 + grp * G + g < batch ? f0 + grp * G + g : batch - 1;
+            return P.frame_map ? (long long)P.frame_map[fi] : fi;
+        };
+#pragma unroll 1
+        for (int g = 0; g < G; ++g)
+            load_channel_lane<T>(P, reinterpret_cast<T *>(sm + LK_LAY(P).ch_off) + 4 * g, frame_of(g), lane);
         __syncwarp();
         int np = 1;
         run_ops(F, np);
-        if (own) finalize(F, f, np);
+#pragma unroll 1
+        for (int g = 0; g < G; ++g)
+            if (f0 + grp * G + g < batch) finalize(F, frame_of(g), np, g * LP);
         if (P.fpc > 1) __syncthreads();
     }
 }

@@ -143,7 +143,8 @@ struct pb_handle {
     // lane-per-path list kernel (lane_kernel.cuh), L in 17..32
     bool lane = false;
     pb::lk::LParams *lp = nullptr;  // host copy of the launch parameters (IO fields per call)
-    int lane_fpc = 0, lane_grid = 0;
+    int lane_fpc = 0, lane_grid = 0;  // frames per CTA, CTAs
+    int lane_fpw = 1;                 // frames per warp (specialised kernel, list sizes <= 16)
     size_t lane_smem = 0;           // per CTA
     unsigned char *d_lane_scratch = nullptr;
     pb::jit::Kernel *jk = nullptr;  // the lane kernel specialised for this code (jit.cu), or null: generic
@@ -168,7 +169,7 @@ bool is_device_ptr(const void *p) {
 
 // options of the handle being created (pb_options, zero = default)
 struct Opts {
-    int kernel = 0, warps = 0, fps = 0, sync_every = 0, recompute = 0, chunk = 0, grid_sms = 0, l1_list = 0, fuse = 0, specialize = 0;
+    int kernel = 0, warps = 0, fps = 0, sync_every = 0, recompute = 0, chunk = 0, grid_sms = 0, l1_list = 0, fuse = 0, specialize = 0, fpw = 0;
 };
 Opts read_opts(const pb_options *o) {
     Opts r;
@@ -184,6 +185,7 @@ Opts read_opts(const pb_options *o) {
     // fields added after the first version: present when the caller's struct is long enough
     if (o->size == 0 || o->size >= (int)(offsetof(pb_options, fuse) + sizeof(int32_t))) r.fuse = o->fuse;
     if (o->size == 0 || o->size >= (int)(offsetof(pb_options, specialize) + sizeof(int32_t))) r.specialize = o->specialize;
+    if (o->size == 0 || o->size >= (int)(offsetof(pb_options, frames_per_warp) + sizeof(int32_t))) r.fpw = o->frames_per_warp;
     return r;
 }
 // sync_every (ops, power of two) -> the kernels' barrier mask; dflt = mask
@@ -264,7 +266,7 @@ struct LanePlan {
 
 // Pure host part: storage layout and the lowered program (no device).
 static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_ops, const std::vector<pb::DOp> &dprog,
-                       const Opts &opt, LanePlan &out, std::string &why) {
+                       const Opts &opt, LanePlan &out, std::string &why, int G = 1) {
     using namespace pb::lk;
     (void)L;
     const int es = mode == PB_MODE_F32 ? 4 : 1;
@@ -296,7 +298,7 @@ static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_op
     const int budget = smem_cap / target_fps / 16 * 16;
     int off = 0, goff = 0;
     lay.ch_off = 0;
-    off = align_up(N * es, 16);
+    off = align_up(G * N * es, 16);  // the warp's G frames' channels, interleaved quad by quad
     lay.asg_off = off;
     off = align_up(off + 32, 8);
     lay.met_off = off;
@@ -447,8 +449,21 @@ static bool make_jit_spec(int N, int n, int k, int L, int mode, int has_crc, uin
     // auto: fused leaves + dead-stage discards.  The multi-level F / G (bits 2, 8, 16; only this build
     // implements it) measured neutral to slower at c3 L=32 (4.48 vs 4.32-4.48 Gbit/s): off by default
     if (opt.fuse == 0) jo.fuse = 1 | 4;
-    if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, jo, pl, why)) return false;
-    const int fps = std::max(1, std::min(32, opt.fps ? opt.fps : 16));
+    // frames per warp (pb_options.frames_per_warp): 32 / pow2(L) frames share a warp's lanes
+    int Lp = 1;
+    while (Lp < L) Lp <<= 1;
+    int G = opt.fpw > 1 ? std::min(opt.fpw, 32 / Lp) : 1;
+    while (G & (G - 1)) G &= G - 1;  // a power of two
+    if (G > 1) {
+        // warps per CTA: the G channels, the fixed tables, beta slots 0..5 and alpha stages 0..4 stay in
+        // shared memory; the rest of each warp's share goes to the next alpha stages
+        const int es = mode == PB_MODE_F32 ? 4 : 1;
+        const int need = G * N * es + 1024 + 6 * 132 + 32 * (4 + 4 + 4 + 8 + 16) * es;
+        jo.fps = std::max(1, std::min(opt.fps ? opt.fps : 16, kLaneSmemCap / need));
+    }
+    if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, jo, pl, why, G)) return false;
+    sp.G = G;
+    const int fps = std::max(1, std::min(32, jo.fps ? jo.fps : 16));
     sp.N = N, sp.n = n, sp.k = k, sp.L = L, sp.mode = mode;
     sp.has_crc = has_crc, sp.crc_const = crc_const;
     sp.lay = pl.lay, sp.prog = pl.prog, sp.final_op = pl.final_op;
@@ -482,6 +497,7 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
                 pl = jp;
                 fpc = sp.fpc;
                 bps = 1;
+                h->lane_fpw = sp.G;
                 char jb[512];
                 snprintf(jb, sizeof jb, "\"specialised\": {\"variants\": %d, \"registers\": %d, \"cache_hit\": %s, "
                          "\"compile_s\": %.1f}", nvar, pb::jit::registers(h->jk), hit ? "true" : "false", secs);
@@ -499,7 +515,11 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
             return false;
         }
     }
-    // ---- ... or the generic kernel (compiled for 16 frames per CTA)
+    // ---- ... or the generic kernel (compiled for 16 frames per CTA, one frame per warp)
+    if (!h->jk && L <= 16 && opt.kernel != 2) {
+        why = "list size <= 16 without the specialised kernel: " + jit_err;
+        return false;
+    }
     if (!h->jk) {
         Opts go = opt;
         go.fps = std::min(16, opt.fps ? opt.fps : 16);
@@ -542,11 +562,11 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     std::copy(pl.prog.begin(), pl.prog.end(), lp->prog);
     if (h->jk) std::copy(vid.begin(), vid.end(), lp->vid);
     h->lp = lp;
-    h->lane_fpc = fpc;
+    h->lane_fpc = fpc * h->lane_fpw;  // frames per CTA
     h->lane_grid = h->sms * bps;
     h->lane_smem = (size_t)fpc * lay.smem_bytes;
     if (lay.gbytes) {
-        cudaError_t e = cudaMalloc(&h->d_lane_scratch, (size_t)h->lane_grid * fpc * lay.gbytes);
+        cudaError_t e = cudaMalloc(&h->d_lane_scratch, (size_t)h->lane_grid * fpc * lay.gbytes);  // per warp
         if (e != cudaSuccess) {
             cudaGetLastError();
             delete lp;
@@ -1062,7 +1082,7 @@ int pb_create_ex(const pb_code *code, const pb_op *ops, int n_ops, int list_size
     std::string lane_why = "list size <= 16";
     if (opt.kernel == 1) {
         lane_why = "interpreted kernel requested";
-    } else if ((L > 16 || opt.kernel == 2) && h->warps == 1) {
+    } else if ((L > 16 || opt.kernel == 2 || (opt.fpw > 1 && opt.specialize >= 0)) && h->warps == 1) {
         plan_lane(h, ops, n_ops, h->prog, opt, lane_why);
     } else if (h->warps != 1) {
         lane_why = "several warps per frame requested";
@@ -1095,9 +1115,10 @@ int pb_create_ex(const pb_code *code, const pb_op *ops, int n_ops, int list_size
         if (h->lane)
             snprintf(lb, sizeof lb,
                      ", \"lane_kernel\": {\"ops\": %d, \"smem_per_frame\": %d, \"global_scratch_per_frame\": %d, "
-                     "\"frames_per_cta\": %d, \"grid\": %d, \"alpha_global_mask\": %u, \"beta_global_mask\": %u, ",
-                     h->lp->n_ops, h->lp->lay.smem_bytes, h->lp->lay.gbytes, h->lane_fpc, h->lane_grid, h->lp->lay.a_gl,
-                     h->lp->lay.b_gl);
+                     "\"frames_per_cta\": %d, \"frames_per_warp\": %d, \"grid\": %d, \"alpha_global_mask\": %u, "
+                     "\"beta_global_mask\": %u, ",
+                     h->lp->n_ops, h->lp->lay.smem_bytes, h->lp->lay.gbytes, h->lane_fpc, h->lane_fpw, h->lane_grid,
+                     h->lp->lay.a_gl, h->lp->lay.b_gl);
         else
             snprintf(lb, sizeof lb, ", \"lane_kernel\": null, \"lane_kernel_why\": \"%s\"}", lane_why.c_str());
         h->plan_json.pop_back();
@@ -1273,7 +1294,8 @@ int scratch_acquire(pb_handle *h, cudaStream_t st) {
 cudaError_t lane_launch(pb_handle *h, const pb::lk::LParams *lp, int grid, cudaStream_t st) {
     if (!h->jk) return pb_lane_launch(lp, h->mode, grid, h->lane_smem, st);
     // a batch smaller than one CTA's frame slots runs only the warps it needs (as lane_launch_t)
-    const int warps = grid == 1 && lp->batch < lp->fpc && !lp->batch_dev ? (int)lp->batch : lp->fpc;
+    const long long need = (lp->batch + h->lane_fpw - 1) / h->lane_fpw;
+    const int warps = grid == 1 && need < lp->fpc && !lp->batch_dev ? (int)need : lp->fpc;
     std::string err;
     const cudaError_t e = pb::jit::launch(h->jk, lp, grid, 32 * warps, h->lane_smem, st, err);
     if (e != cudaSuccess) g_err = err;
