@@ -103,8 +103,9 @@ typedef struct pb_options {
                                  (generic kernel), 1 on (PB_ECUDA if it cannot be built), 3 = on with leaf
                                  Combine-chain targets read at run time (fewer variants) */
     int32_t frames_per_warp;  /* specialised lane kernel, list sizes <= 16: this many frames share one warp
-                                 (lane = frame slot x path slot; at most 32 / pow2(L)); 0 / 1 = one frame per
-                                 warp through the interpreted kernel */
+                                 (lane = frame slot x path slot; at most 32 / pow2(L)); 0 auto (32 / pow2(L),
+                                 halved until three warps fit an SM), 1 = one frame per warp (the interpreted
+                                 kernel for L <= 16) */
 } pb_options;
 
 /* Build a decoder for (code, schedule, list size) on a CUDA device.

@@ -452,15 +452,26 @@ static bool make_jit_spec(int N, int n, int k, int L, int mode, int has_crc, uin
     // frames per warp (pb_options.frames_per_warp): 32 / pow2(L) frames share a warp's lanes
     int Lp = 1;
     while (Lp < L) Lp <<= 1;
+    // shared memory a warp needs at least: its G channels, the fixed tables, beta slots 0..5 and alpha
+    // stages 0..4 (the rest of its share goes to the next alpha stages)
+    const int es0 = mode == PB_MODE_F32 ? 4 : 1;
+    auto need = [&](int g) { return g * N * es0 + 1024 + 6 * 132 + 32 * (4 + 4 + 4 + 8 + 16) * es0; };
     int G = opt.fpw > 1 ? std::min(opt.fpw, 32 / Lp) : 1;
-    while (G & (G - 1)) G &= G - 1;  // a power of two
-    if (G > 1) {
-        // warps per CTA: the G channels, the fixed tables, beta slots 0..5 and alpha stages 0..4 stay in
-        // shared memory; the rest of each warp's share goes to the next alpha stages
-        const int es = mode == PB_MODE_F32 ? 4 : 1;
-        const int need = G * N * es + 1024 + 6 * 132 + 32 * (4 + 4 + 4 + 8 + 16) * es;
-        jo.fps = std::max(1, std::min(opt.fps ? opt.fps : 16, kLaneSmemCap / need));
+    if (opt.fpw == 0 && L <= 16) {
+        // auto: every lane a path slot, but at least three warps per SM (measured, Gbit/s: c3 L=2 16 frames
+        // per warp = 1 warp per SM 5.3, 8 = 3 warps 8.9; c3 L=8 4 frames 8.9, 2 frames 8.2; c2 L=8 4 frames
+        // 13.6, 2 frames 9.7; c1 L=4 8 frames 7.1, 4 frames 6.9)
+        G = 32 / Lp;
+        while (G > 1 && kLaneSmemCap / need(G) < 3) G >>= 1;
+        // long codes: the channels leave room for too few frames (c5 N=8192 L=16: 6 frames per SM,
+        // 2.7 Gbit/s against the interpreted kernel's 3.4): stay with the interpreted kernel
+        if (G * std::min(16, kLaneSmemCap / need(G)) < 16) {
+            why = "too few resident frames per SM for the lane kernel at this block length";
+            return false;
+        }
     }
+    while (G & (G - 1)) G &= G - 1;  // a power of two
+    if (G > 1) jo.fps = std::max(1, std::min(opt.fps ? opt.fps : 16, kLaneSmemCap / need(G)));
     if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, jo, pl, why, G)) return false;
     sp.G = G;
     const int fps = std::max(1, std::min(32, jo.fps ? jo.fps : 16));
@@ -1082,7 +1093,8 @@ int pb_create_ex(const pb_code *code, const pb_op *ops, int n_ops, int list_size
     std::string lane_why = "list size <= 16";
     if (opt.kernel == 1) {
         lane_why = "interpreted kernel requested";
-    } else if ((L > 16 || opt.kernel == 2 || (opt.fpw > 1 && opt.specialize >= 0)) && h->warps == 1) {
+    } else if ((L > 16 || opt.kernel == 2 || (opt.fpw != 1 && opt.fpw >= 0 && opt.specialize >= 0 && L > 1)) &&
+               h->warps == 1 && opt.warps <= 1) {
         plan_lane(h, ops, n_ops, h->prog, opt, lane_why);
     } else if (h->warps != 1) {
         lane_why = "several warps per frame requested";

@@ -72,3 +72,58 @@ def test_specialised_small_codes_compile_on_the_fly(cfg):
     got = dec.decode_batch(feed)
     ref = oracle.decode_batch(sch, L, feed.astype(np.float32), int8=(mode == "int8"), threads=4)
     assert _same(got, ref)
+
+
+MULTI = [  # (N, k incl. payload, crc, L, mode, frames per warp: 0 = auto)
+    (2048, 1691, "crc32", 8, "f32", 0), (2048, 1691, "crc32", 2, "f32", 0), (2048, 1691, "crc32", 2, "f32", 16),
+    (1024, 504, "crc8d5", 4, "f32", 0), (1024, 828, "crc32", 8, "int8", 4), (2048, 1691, "crc32", 16, "f32", 2),
+    (512, 300, "crc16", 5, "f32", 0), (256, 100, "none", 3, "int8", 0), (64, 30, "crc8", 7, "f32", 0),
+    (8192, 6112, "crc32", 16, "f32", 2), (4096, 2000, "crc16", 12, "f32", 2),
+]
+
+
+@pytest.mark.parametrize("cfg", MULTI, ids=str)
+def test_frames_sharing_a_warp_match_oracle_and_interpreted_kernel(cfg):
+    """List sizes <= 16: 32 / pow2(L) frames share one warp of the specialised
+    lane kernel (lane = frame slot x path slot).  Bit-exact with the oracle
+    and the interpreted kernel on channel frames plus integer LLRs (metric and
+    reliability ties land in the segment-masked selection), ragged batches
+    and single frames included."""
+    N, k, crc, L, mode, fpw = cfg
+    crcs = {"none": None, "crc8": pb.CRC8, "crc16": pb.CRC16, "crc32": pb.CRC32,
+            "crc8d5": pb.CrcConfig(width=8, polynomial=0xD5)}
+    spec = pb.CodeSpec.from_design_ebn0(N, k, crcs[crc], 3.0)
+    sch = pb.build_schedule(spec)
+    B = 403 if N <= 2048 else 70
+    rng = np.random.default_rng(N + 17 * L)
+    llr = np.concatenate([pb.generate_frames(spec, 2.5, seed=L, start=0, count=B).llrs,
+                          rng.integers(-5, 6, size=(B // 2, N)).astype(np.float32)])
+    feed = llr if mode == "f32" else pb.quantize_int8(llr)
+    dec = pb.ListDecoder(sch, L, mode=mode, options={"specialize": 1, "frames_per_warp": fpw})
+    plan = json.loads(dec.plan)["lane_kernel"]
+    assert plan["specialised"] and plan["frames_per_warp"] >= 2
+    got = dec.decode_batch(feed)
+    twin = pb.ListDecoder(sch, L, mode=mode, options={"kernel": "interpreted"}).decode_batch(feed)
+    assert _same(got, twin)
+    n_or = min(len(feed), 120)
+    pick = np.r_[0:n_or // 2, len(feed) - n_or // 2:len(feed)]
+    ref = oracle.decode_batch(sch, L, feed[pick].astype(np.float32), int8=(mode == "int8"), threads=4)
+    for f in FIELDS:
+        assert np.array_equal(getattr(got, f)[pick], getattr(ref, f)), f
+    assert _same(dec.decode_batch(feed[:1]), got, 1)
+    assert _same(dec.decode_batch(feed[:plan["frames_per_warp"] + 1]), got, plan["frames_per_warp"] + 1)
+
+
+def test_frames_sharing_a_warp_paths_and_adaptive():
+    spec = pb.CodeSpec.from_design_ebn0(1024, 828, pb.CRC32, 4.0)
+    sch = pb.build_schedule(spec)
+    fb = pb.generate_frames(spec, 3.0, seed=8, start=0, count=90)
+    a = pb.ListDecoder(sch, 8, options={"specialize": 1})
+    b = pb.ListDecoder(sch, 8, options={"kernel": "interpreted"})
+    assert json.loads(a.plan)["lane_kernel"]["frames_per_warp"] == 4
+    for x, y in zip(a.decode_paths_batch(fb.llrs[:9]), b.decode_paths_batch(fb.llrs[:9])):
+        assert np.array_equal(x, y)
+    ra = pb.AdaptiveDecoder(sch, 8, options={"specialize": 1}).decode_batch(fb.llrs)
+    rb = pb.AdaptiveDecoder(sch, 8, options={"kernel": "interpreted"}).decode_batch(fb.llrs)
+    for f in FIELDS + ("invoked_list",):
+        assert np.array_equal(getattr(ra, f), getattr(rb, f))
