@@ -422,13 +422,18 @@ def main():
         peak = sms * 128 * sm_mhz * 1e6 / 1e9
         hbm_bytes = B * (spec.N * 4 + spec.k + 13)
         hbm_gbs = hbm_bytes / (kernel_ms * 1e-3) / 1e9
-        traffic = None
+        # measured DRAM traffic of the decode kernel: dram__bytes_read + dram__bytes_write of one
+        # `ncu --set full` capture of this config (profiles/ncu_<config>.json, tools/ncu_summary.py),
+        # per frame, times the frames of one launch
+        traffic = traffic_frames = None
         prof = os.path.join(REPO, "profiles", f"ncu_{args.config}.json")
         if os.path.exists(prof):
             try:
                 with open(prof) as fh:
-                    traffic = json.load(fh).get("dram_bytes_per_launch_per_frame")
-                    traffic = None if traffic is None else traffic * B
+                    pj = json.load(fh)
+                traffic = pj.get("dram_bytes_per_launch_per_frame")
+                traffic_frames = pj.get("frames")
+                traffic = None if traffic is None else traffic * B
             except Exception:
                 traffic = None
         line = {
@@ -451,7 +456,12 @@ def main():
                          "work_per_frame_lane_ops": W,
                          "peak_note": f"{sms} SMs x 128 lanes x {sm_mhz:.0f} MHz "
                                       f"(sm_max_mhz, {peak_kind}); SURVEY 8(d) ALU-issue roofline",
-                         "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / float(peaks.get("hbm_gbs", 6650.0))},
+                         "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / float(peaks.get("hbm_gbs", 6650.0)),
+                         # the same from the measured DRAM bytes (global alpha scratch included)
+                         "dram_gbs_measured": None if traffic is None else traffic / (kernel_ms * 1e-3) / 1e9,
+                         "dram_frac_measured": None if traffic is None else
+                         traffic / (kernel_ms * 1e-3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)),
+                         "traffic_capture_frames": traffic_frames},
             "clocks": clocks.summary(),
             "latency": latency,
             "options": opts,
