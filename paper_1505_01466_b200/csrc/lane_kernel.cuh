@@ -491,9 +491,61 @@ __device__ __forceinline__ void fg_body_v(const S &src, T *dst, const uint32_t *
 }
 
 // F / G of stage s into the path's own row of stage s-1 (listdec.py:317-326)
+// F / G while a frame still has a single path (the ops before its first
+// fork): the frame's lanes split the row's quads instead of one lane walking
+// the whole row (specialised build: the path count is a constant there).
+template <typename T, bool IS_G, class S>
+__device__ __forceinline__ void fg_single_body(const S &src, T *dst, const uint32_t *bw, int nq, int x0, int step) {
+    for (int x = x0; x < nq; x += step) {
+        float a[4], b[4], o[4];
+        src.quad(x, a);
+        src.quad(x + nq, b);
+        const unsigned bits = IS_G ? bw[x >> 3] >> ((x & 7) * 4) : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op_bits<T>(a[j], b[j], bits, j) : f_op(a[j], b[j]);
+        V4<T>::st(dst + x * 128, o);
+    }
+}
+template <typename T, bool IS_G, int SRC, int DST, class OP>
+__device__ __forceinline__ void fg_single(Fr<T> &F, const OP &o) {
+    const int s = o.stage(), nq = 1 << (s - 3), n = LK_C(F.P, n);
+    const int b0 = F.base();  // the lane of the frame's only path
+    uint32_t ia0[4], ib0[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        ia0[j] = __shfl_sync(FULL_MASK, F.ia[j], b0);
+        ib0[j] = __shfl_sync(FULL_MASK, F.ib[j], b0);
+    }
+    T *dst = F.template a_row_t<DST>(s - 1, b0);
+    const uint32_t *bw = IS_G ? F.beta_row(s - 1, get8(ib0, s - 1)) : nullptr;
+    const int x0 = F.slot(), step = Fr<T>::LP;
+    if (SRC == S_V2) {
+        const V2Ld<T> v{F.channel(), F.beta_row(n - 1, get8(ib0, n - 1)), F.beta_row(n - 2, get8(ib0, n - 2)),
+                        LK_C(F.P, N) >> 2, (o.flags() & LF_V1G) != 0, (o.flags() & LF_V2G) != 0};
+        fg_single_body<T, IS_G>(v, dst, bw, nq, x0, step);
+    } else if (SRC == S_V1) {
+        const V1Ld<T> v{F.channel(), F.beta_row(n - 1, get8(ib0, n - 1)), LK_C(F.P, N) >> 1,
+                        (o.flags() & LF_V1G) != 0};
+        fg_single_body<T, IS_G>(v, dst, bw, nq, x0, step);
+    } else if (SRC == S_CH) {
+        fg_single_body<T, IS_G>(RowLd<T>{F.channel(), CQ}, dst, bw, nq, x0, step);
+    } else {
+        fg_single_body<T, IS_G>(RowLd<T>{F.template a_row_t<SRC>(s, get8(ia0, s)), 128}, dst, bw, nq, x0, step);
+    }
+    __syncwarp();
+    if (SRC == S_GL && (o.flags() & LF_LAST)) F.discard_stage(s);
+    set8(F.ia, s - 1, F.lane);
+}
+
 template <typename T, bool IS_G, int SRC, int DST, class OP>
 __device__ __forceinline__ void fg_op(Fr<T> &F, const OP &o) {
     const int s = o.stage(), h = 1 << (s - 1);
+#ifdef PB_JIT
+    if (o.pin() == 1 && h >= 4) {
+        fg_single<T, IS_G, SRC, DST>(F, o);
+        return;
+    }
+#endif
     if (F.slot() < o.pin()) {
         T *dst = F.template a_row_t<DST>(s - 1, F.lane);
         const uint32_t *bw = IS_G ? F.beta_row(s - 1, get8(F.ib, s - 1)) : nullptr;
