@@ -99,9 +99,10 @@ typedef struct pb_options {
     int32_t specialize;       /* lane kernel compiled per code (NVRTC, cubin cached next to the library): every
                                  distinct op of the schedule becomes one instantiation with stage, placements,
                                  offsets and path counts as constants -- the paper's unrolled decoder.
-                                 0 auto (on; the generic kernel runs if NVRTC is unavailable), -1 off
-                                 (generic kernel), 1 on (PB_ECUDA if it cannot be built), 3 = on with leaf
-                                 Combine-chain targets read at run time (fewer variants) */
+                                 0 auto (on; the generic kernels run if NVRTC is unavailable), -1 off
+                                 (generic kernels), 1 on (PB_ECUDA if it cannot be built); larger values are
+                                 explicit policy bits for experiments (csrc/jit.h: 1 | 2 leaf chain targets at
+                                 run time, | 4 level-by-level chains, | 8 / 16 pipelined wide-leaf scans) */
     int32_t frames_per_warp;  /* specialised lane kernel, list sizes <= 16: this many frames share one warp
                                  (lane = frame slot x path slot; at most 32 / pow2(L)); 0 auto (32 / pow2(L),
                                  halved until three warps fit an SM), 1 = one frame per warp (the interpreted
