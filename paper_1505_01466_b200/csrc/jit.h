@@ -33,6 +33,7 @@ enum : int {
                            // c3 L=32 4.49 -> 4.62 Gbit/s)
     POL_SCAN_PIPE2 = 8,    // wide-leaf scans software-pipelined over blocks of 2 quads
     POL_SCAN_PIPE4 = 16,   // ... of 4 quads
+    POL_FG_U16 = 32,       // 16 (instead of 8) quad pairs in flight in F / G over global-scratch stages
 };
 
 // The generated translation unit and, per op, the variant id the kernel
@@ -41,9 +42,10 @@ std::string generate(const Spec &sp, std::vector<uint16_t> &vid, int *n_variants
 
 struct Kernel;  // a loaded module + function (shared between handles of the same code)
 
-// Compile (or fetch from the cubin cache) and load.  device-free when
+// Compile (or fetch from the cubin cache) and load into the current context of `device`.  device-free when
 // load == false (prebuild: fills the cache only).  nullptr + err on failure.
-Kernel *acquire(const std::string &source, bool load, std::string &err, bool *cache_hit, double *compile_s);
+Kernel *acquire(const std::string &source, bool load, int device, std::string &err, bool *cache_hit,
+                double *compile_s);
 void release(Kernel *k);
 cudaError_t launch(Kernel *k, const lk::LParams *p, int grid, int threads, size_t smem, cudaStream_t st,
                    std::string &err);

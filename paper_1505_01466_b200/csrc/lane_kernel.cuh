@@ -27,6 +27,10 @@
 #define PB_LANE_V2SPEC 1
 #endif
 // a survivor's chain rows of at least this many words use the unrolled form
+// quad pairs in flight per lane in an F / G over a global-scratch stage
+#ifndef PB_FG_U_GL
+#define PB_FG_U_GL 8
+#endif
 // specialised build: quads per block of the pipelined wide-leaf scan (0 = off)
 #ifndef PB_SCAN_PIPE
 #define PB_SCAN_PIPE 0
@@ -439,12 +443,13 @@ __device__ __forceinline__ void fg_body(const S &src, T *dst, const uint32_t *bw
             src.quad(x0 + u, a[u]);
             src.quad(x0 + u + nq, b[u]);
         }
-        unsigned wd = 0u;
-        if (IS_G) wd = bw[x0 >> 3];  // U <= 8 quads of one 32-bit word (x0 multiple of U)
+        unsigned wd[(U + 7) / 8];  // 8 quads per 32-bit beta word (x0 is a multiple of U)
+#pragma unroll
+        for (int w = 0; w < (U + 7) / 8; ++w) wd[w] = IS_G ? bw[(x0 >> 3) + w] : 0u;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             float o[4];
-            const unsigned bits = IS_G ? wd >> (((x0 + u) & 7) * 4) : 0u;
+            const unsigned bits = IS_G ? wd[u >> 3] >> (((x0 + u) & 7) * 4) : 0u;
 #pragma unroll
             for (int j = 0; j < 4; ++j) o[j] = IS_G ? g_op_bits<T>(a[u][j], b[u][j], bits, j) : f_op(a[u][j], b[u][j]);
             V4<T>::st(dst + (x0 + u) * 128, o);
@@ -575,7 +580,7 @@ __device__ __forceinline__ void fg_op(Fr<T> &F, const OP &o) {
             fg_body<T, IS_G, 4>(RowLd<T>{F.channel(), CQ}, dst, bw, h);
         } else {
             const RowLd<T> src{F.template a_row_t<SRC>(s, get8(F.ia, s)), 128};
-            fg_body<T, IS_G, SRC == S_GL ? 8 : 4>(src, dst, bw, h);
+            fg_body<T, IS_G, SRC == S_GL ? PB_FG_U_GL : 4>(src, dst, bw, h);
         }
     }
     if (SRC == S_GL && (o.flags() & LF_LAST)) {

@@ -503,7 +503,7 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
             const std::string src = pb::jit::generate(sp, vid, &nvar);
             bool hit = false;
             double secs = 0.0;
-            h->jk = pb::jit::acquire(src, true, jit_err, &hit, &secs);
+            h->jk = pb::jit::acquire(src, true, h->device, jit_err, &hit, &secs);
             if (h->jk && pb::jit::occupancy(h->jk, 32 * sp.fpc, (size_t)sp.fpc * jp.lay.smem_bytes) >= 1) {
                 pl = jp;
                 fpc = sp.fpc;
@@ -1205,7 +1205,7 @@ int pb_jit_prebuild(const pb_code *code, const pb_op *ops, int n_ops, int list_s
     std::string err;
     bool hit = false;
     double secs = 0.0;
-    if (!pb::jit::acquire(src, false, err, &hit, &secs)) return fail(PB_ECUDA, err);
+    if (!pb::jit::acquire(src, false, 0, err, &hit, &secs)) return fail(PB_ECUDA, err);
     if (cache_hit) *cache_hit = hit;
     if (compile_s) *compile_s = secs;
     return PB_OK;
@@ -1539,10 +1539,10 @@ int decode_impl(pb_handle *h, const void *llr, int in_type, int64_t batch, uint8
     // kernels overlap across the two streams, hiding each wave's tail
     // (adaptive decoding: 6 waves, so each chunk's list pass over its few
     // CRC failures amortises its launch and its grid-wide occupancy)
-    const long long chunk = std::max<long long>(
-        1, h->chunk_frames > 0 ? (long long)h->chunk_frames
-                               : (long long)std::max(2048, (adaptive ? 6 : 1) * (h->lane ? h->lane_grid * h->lane_fpc
-                                                                                       : h->grid * h->fpc)));
+    // whole waves of the persistent grid (a partial last wave idles most of the SMs), at least 2048 frames
+    const long long wave = h->lane ? (long long)h->lane_grid * h->lane_fpc : (long long)h->grid * h->fpc;
+    const long long waves = std::max<long long>(adaptive ? 6 : 1, (2048 + wave - 1) / std::max<long long>(1, wave));
+    const long long chunk = std::max<long long>(1, h->chunk_frames > 0 ? (long long)h->chunk_frames : waves * wave);
     if (!dev_in && batch > chunk)
         return decode_pipelined(h, h->base, llr, in_type, in_es, batch, chunk, info_out, crc_ok, pm_out, paths_used,
                                 invoked, adaptive, st);
