@@ -33,6 +33,7 @@ enum : int {
                            // c3 L=32 4.49 -> 4.62 Gbit/s)
     POL_SCAN_PIPE2 = 8,    // wide-leaf scans software-pipelined over blocks of 2 quads
     POL_SCAN_PIPE4 = 16,   // ... of 4 quads
+    POL_ASG_LOOP = 64,     // survivor hand-over as a loop over set bits (keys in local memory)
     POL_FG_U16 = 32,       // 16 (instead of 8) quad pairs in flight in F / G over global-scratch stages
 };
 

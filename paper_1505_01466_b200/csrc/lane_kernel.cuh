@@ -27,6 +27,11 @@
 #define PB_LANE_V2SPEC 1
 #endif
 // a survivor's chain rows of at least this many words use the unrolled form
+// survivor hand-over by a loop over the set bits (run-time key index: the keys
+// live in local memory) instead of the unrolled predicated form
+#ifndef PB_ASG_LOOP
+#define PB_ASG_LOOP 0
+#endif
 // quad pairs in flight per lane in an F / G over a global-scratch stage
 #ifndef PB_FG_U_GL
 #define PB_FG_U_GL 8
@@ -1299,13 +1304,23 @@ __device__ __forceinline__ void leaf_op(Fr<T> &F, const OP &o) {
     uint8_t *asg = F.sm + LK_LAY(P).asg_off;
     double *met = reinterpret_cast<double *>(F.sm + LK_LAY(P).met_off);
     int k = F.base() + seg_excl_scan4(__popc(mask), F.lane, F.seg(), FULL_MASK);
-    while (mask) {
-        const int c = __ffs(mask) - 1;
-        mask &= mask - 1;
+#if PB_ASG_LOOP
+    for (unsigned mk = mask; mk; mk &= mk - 1) {
+        const int c = __ffs(mk) - 1;
         asg[k] = (uint8_t)((F.lane << 3) | c);
         met[k] = unkey(key[c]);
         ++k;
     }
+#else
+    // (static indices: a run-time key[c] would put the keys in local memory)
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        if (c < C && ((mask >> c) & 1u)) {
+            const int kk = k + __popc(mask & ((1u << c) - 1u));  // no chain through k
+            asg[kk] = (uint8_t)((F.lane << 3) | c);
+            met[kk] = unkey(key[c]);
+        }
+#endif
     __syncwarp();
     const bool live = F.slot() < o.pout();
     int p = F.lane, c = 0;

@@ -481,6 +481,10 @@ static bool make_jit_spec(int N, int n, int k, int L, int mode, int has_crc, uin
     // auto / 1: everything compile-time, unrolled chains, wide-leaf scans pipelined over 2-quad blocks
     // (c3 L=32: 4.61 -> 4.65 Gbit/s; 4-quad blocks 4.62); other values: explicit policy bits (jit.h)
     sp.policy = opt.specialize <= 1 ? (pb::jit::POL_FULL | pb::jit::POL_SCAN_PIPE2) : opt.specialize;
+    // survivor hand-over: unrolled with static key indices (c3 L=32 4.67 -> 4.96, int8 5.11 -> 5.67, c2 L=8
+    // 13.9 -> 15.3 Gbit/s: no local-memory round trip), except at L = 2 where the loop over the set bits
+    // measured faster (c3 L=2 8.9 against 7.5)
+    if (opt.specialize <= 1 && L <= 2) sp.policy |= pb::jit::POL_ASG_LOOP;
     sp.fpc = std::max(1, std::min(fps, kLaneSmemCap / std::max(16, pl.lay.smem_bytes)));
     return true;
 }
