@@ -94,15 +94,16 @@ typedef struct pb_options {
     int32_t l1_list_kernel;   /* 1: list size 1 through the list kernel instead of the single-path pass */
     int32_t fuse;             /* lane kernel op fusion: 0 auto (everything measured faster), -1 none, else a
                                  bit set: 1 = a leaf reads f / g of its parent's row (its own row is never
-                                 stored), 2 = an F is computed by the op producing its input row, 4 = a
-                                 global-scratch stage is discarded from the L2 after its last read */
+                                 stored), 4 = a global-scratch stage is discarded from the L2 after its last
+                                 read */
     int32_t specialize;       /* lane kernel compiled per code (NVRTC, cubin cached next to the library): every
                                  distinct op of the schedule becomes one instantiation with stage, placements,
                                  offsets and path counts as constants -- the paper's unrolled decoder.
                                  0 auto (on; the generic kernels run if NVRTC is unavailable), -1 off
                                  (generic kernels), 1 on (PB_ECUDA if it cannot be built); larger values are
                                  explicit policy bits for experiments (csrc/jit.h: 1 | 2 leaf chain targets at
-                                 run time, | 4 level-by-level chains, | 8 / 16 pipelined wide-leaf scans) */
+                                 run time, | 4 level-by-level chains, | 8 pipelined wide-leaf scans, | 64
+                                 survivor hand-over as a loop) */
     int32_t frames_per_warp;  /* specialised lane kernel, list sizes <= 16: this many frames share one warp
                                  (lane = frame slot x path slot; at most 32 / pow2(L)); 0 auto (32 / pow2(L),
                                  halved until three warps fit an SM), 1 = one frame per warp (the interpreted

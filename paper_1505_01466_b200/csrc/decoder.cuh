@@ -142,10 +142,7 @@ struct Params {
 // recomputed from it instead of stored.
 namespace lk {
 constexpr int kMaxOps = 2048;  // the op program travels in the kernel parameters (16 KB)
-enum : uint8_t { K_F = 0, K_G = 1, K_R0 = 2, K_REP = 3, K_R1 = 4, K_SPC = 5, K_NOP = 6,
-                 // specialised build only: F / G of stage s and the ncand (1 or 2) F ops below it as one
-                 // op; aux bit l = stage s-1-l in global scratch
-                 K_FM = 7, K_GM = 8 };
+enum : uint8_t { K_F = 0, K_G = 1, K_R0 = 2, K_REP = 3, K_R1 = 4, K_SPC = 5, K_NOP = 6 };
 // where an op's input stage lives: a stored row in shared memory / global
 // scratch, recomputed stage n-1 (f / g of the channel halves), recomputed
 // stage n-2, or the channel itself (a root leaf)

@@ -32,10 +32,6 @@
 #ifndef PB_ASG_LOOP
 #define PB_ASG_LOOP 0
 #endif
-// quad pairs in flight per lane in an F / G over a global-scratch stage
-#ifndef PB_FG_U_GL
-#define PB_FG_U_GL 8
-#endif
 // specialised build: quads per block of the pipelined wide-leaf scan (0 = off)
 #ifndef PB_SCAN_PIPE
 #define PB_SCAN_PIPE 0
@@ -585,7 +581,7 @@ __device__ __forceinline__ void fg_op(Fr<T> &F, const OP &o) {
             fg_body<T, IS_G, 4>(RowLd<T>{F.channel(), CQ}, dst, bw, h);
         } else {
             const RowLd<T> src{F.template a_row_t<SRC>(s, get8(F.ia, s)), 128};
-            fg_body<T, IS_G, SRC == S_GL ? PB_FG_U_GL : 4>(src, dst, bw, h);
+            fg_body<T, IS_G, SRC == S_GL ? 8 : 4>(src, dst, bw, h);
         }
     }
     if (SRC == S_GL && (o.flags() & LF_LAST)) {
@@ -593,86 +589,6 @@ __device__ __forceinline__ void fg_op(Fr<T> &F, const OP &o) {
         F.discard_stage(s);
     }
     set8(F.ia, s - 1, F.lane);
-}
-
-// F / G of stage s followed by the D F ops below it, as one op (the chain
-// "G_s F_{s-1} F_{s-2}" of a left descent, listdec.py:317-326 applied D + 1
-// times): each block of 2^D source quad pairs yields 2^D quads of stage s-1,
-// 2^(D-1) of stage s-2, ... -- every stage is stored (its G reads it later)
-// but none is read back: the F ops' row loads disappear.  Quad x of stage
-// s-1-l pairs quads x and x + (nq >> (l+1)) of stage s-l.
-template <typename T, bool IS_G, int D, class S>
-__device__ __forceinline__ void fgm_body(const S &src, T *d1, T *d2, T *d3, const uint32_t *bw, int h) {
-    constexpr int R = 1 << D;
-    const int nq = h >> 2, step = nq >> D;  // step >= 1 (runtime.cu merges only then)
-    for (int x = 0; x < step; ++x) {
-        float a[R][4], b[R][4];
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            src.quad(x + j * step, a[j]);
-            src.quad(x + j * step + nq, b[j]);
-        }
-        float o[R][4];
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            const int y = x + j * step;
-            const unsigned bits = IS_G ? bw[y >> 3] >> ((y & 7) * 4) : 0u;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) o[j][e] = IS_G ? g_op_bits<T>(a[j][e], b[j][e], bits, e) : f_op(a[j][e], b[j][e]);
-            V4<T>::st(d1 + y * 128, o[j]);
-        }
-        float p[R / 2][4];
-#pragma unroll
-        for (int j = 0; j < R / 2; ++j) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) p[j][e] = f_op(o[j][e], o[j + R / 2][e]);
-            V4<T>::st(d2 + (x + j * step) * 128, p[j]);
-        }
-        if (D == 2) {
-            float q[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) q[e] = f_op(p[0][e], p[D == 2 ? 1 : 0][e]);
-            V4<T>::st(d3 + x * 128, q);
-        }
-    }
-}
-
-// GLM: bit l set = stage s-1-l lives in global scratch
-template <typename T, bool IS_G, int SRC, int D, int GLM, class OP>
-__device__ __forceinline__ void fgm_op(Fr<T> &F, const OP &o) {
-    const int s = o.stage(), h = 1 << (s - 1);
-    if (F.slot() < o.pin()) {
-        T *d1 = F.template a_row_t<(GLM & 1) ? S_GL : S_SM>(s - 1, F.lane);
-        T *d2 = F.template a_row_t<(GLM & 2) ? S_GL : S_SM>(s - 2, F.lane);
-        T *d3 = D == 2 ? F.template a_row_t<(GLM & 4) ? S_GL : S_SM>(s - 3, F.lane) : nullptr;
-        const uint32_t *bw = IS_G ? F.beta_row(s - 1, get8(F.ib, s - 1)) : nullptr;
-        if (SRC == S_V2) {
-            const V2Ld<T> v = make_v2(F, o.flags());
-            switch ((v.g1_ ? 1 : 0) | (v.g2_ ? 2 : 0)) {
-                case 0: fgm_body<T, IS_G, D>(V2Ld<T, 0>{v.ch, v.b1, v.b2, v.q, false, false}, d1, d2, d3, bw, h); break;
-                case 1: fgm_body<T, IS_G, D>(V2Ld<T, 1>{v.ch, v.b1, v.b2, v.q, true, false}, d1, d2, d3, bw, h); break;
-                case 2: fgm_body<T, IS_G, D>(V2Ld<T, 2>{v.ch, v.b1, v.b2, v.q, false, true}, d1, d2, d3, bw, h); break;
-                default: fgm_body<T, IS_G, D>(V2Ld<T, 3>{v.ch, v.b1, v.b2, v.q, true, true}, d1, d2, d3, bw, h); break;
-            }
-        } else if (SRC == S_V1) {
-            const V1Ld<T> v = make_v1(F, o.flags());
-            if (v.g_)
-                fgm_body<T, IS_G, D>(V1Ld<T, 1>{v.ch, v.b1, v.half, true}, d1, d2, d3, bw, h);
-            else
-                fgm_body<T, IS_G, D>(V1Ld<T, 0>{v.ch, v.b1, v.half, false}, d1, d2, d3, bw, h);
-        } else if (SRC == S_CH) {
-            fgm_body<T, IS_G, D>(RowLd<T>{F.channel(), CQ}, d1, d2, d3, bw, h);
-        } else {
-            fgm_body<T, IS_G, D>(RowLd<T>{F.template a_row_t<SRC>(s, get8(F.ia, s)), 128}, d1, d2, d3, bw, h);
-        }
-    }
-    if (SRC == S_GL && (o.flags() & LF_LAST)) {
-        __syncwarp();
-        F.discard_stage(s);
-    }
-    set8(F.ia, s - 1, F.lane);
-    set8(F.ia, s - 2, F.lane);
-    if (D == 2) set8(F.ia, s - 3, F.lane);
 }
 
 // ------------------------------------------------------------- leaves
@@ -764,7 +680,7 @@ __device__ __forceinline__ int leaf_scan_lane(const S &src, int m, TopK<K> &tk, 
         // software pipeline over blocks of QB quads: the loads of block b + 1
         // are issued before block b is scanned (the rows of wide leaves live
         // in global scratch: an L2 round trip per block otherwise)
-        constexpr int QB = PB_SCAN_PIPE, EB = 4 * QB, BPW = 32 / EB;  // blocks per 32-bit hard word
+        constexpr int QB = PB_SCAN_PIPE, EB = 4 * QB, BPW = 32 / EB;  // blocks per 32-bit hard word (4-quad blocks: 4.62 against 4.65 Gbit/s)
         typename S::Raw buf[2][QB];
         const int nb = m / EB;
         auto ld = [&](int b, typename S::Raw(&r)[QB]) {
@@ -1512,9 +1428,6 @@ __device__ __forceinline__ void exec_op(Fr<T> &F, const Op<K, S, PI, PO, NC, SR,
         if constexpr (K <= K_G) {
             static_assert(SR >= 0 && AX >= 0, "a compile-time F / G needs compile-time placements");
             fg_op<T, K == K_G, SR, AX == S_GL ? S_GL : S_SM>(F, o);
-        } else if constexpr (K == K_FM || K == K_GM) {
-            static_assert(SR >= 0 && AX >= 0 && (NC == 1 || NC == 2), "a multi-level F / G is compile-time only");
-            fgm_op<T, K == K_GM, SR, NC, AX>(F, o);
         } else if constexpr (K != K_NOP) {
             leaf_op(F, o);
             np = o.pout();

@@ -384,21 +384,6 @@ static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_op
             l.src = src_of(s);
             l.aux = ((lay.a_gl >> (s - 1)) & 1u) ? S_GL : S_SM;
             l.flags = flags | ((fuse & 4) && op.kind == PB_OP_G && l.src == S_GL ? LF_LAST : 0);
-            // the F ops right below it (a left descent) join it (specialised build only)
-            if ((fuse & 2) && !out_virtual && ((fuse & 8) || (l.src != S_V1 && l.src != S_V2))) {
-                int D = 0;
-                while (D < ((fuse & 16) ? 2 : 1) && i + 1 + D < n_ops && ops[i + 1 + D].kind == PB_OP_F && ops[i + 1 + D].stage == s - 1 - D &&
-                       !leaf_fusable(i + 1 + D) && (1 << (s - 1)) >= (4 << (D + 1)))
-                    ++D;
-                if (D) {
-                    l.kind = op.kind == PB_OP_F ? K_FM : K_GM;
-                    l.ncand = (uint8_t)D;
-                    l.aux = 0;
-                    for (int q = 0; q <= D; ++q) l.aux |= ((lay.a_gl >> (s - 1 - q)) & 1u) << q;
-                    i += D;
-                    di += D;
-                }
-            }
             prog.push_back(l);
             continue;
         }
@@ -446,9 +431,6 @@ static bool make_jit_spec(int N, int n, int k, int L, int mode, int has_crc, uin
                           int n_ops, const std::vector<pb::DOp> &dprog, const Opts &opt, pb::jit::Spec &sp,
                           LanePlan &pl, std::string &why) {
     Opts jo = opt;
-    // auto: fused leaves + dead-stage discards.  The multi-level F / G (bits 2, 8, 16; only this build
-    // implements it) measured neutral to slower at c3 L=32 (4.48 vs 4.32-4.48 Gbit/s): off by default
-    if (opt.fuse == 0) jo.fuse = 1 | 4;
     // frames per warp (pb_options.frames_per_warp): 32 / pow2(L) frames share a warp's lanes
     int Lp = 1;
     while (Lp < L) Lp <<= 1;
@@ -538,8 +520,6 @@ static bool plan_lane(pb_handle *h, const pb_op *ops, int n_ops, const std::vect
     if (!h->jk) {
         Opts go = opt;
         go.fps = std::min(16, opt.fps ? opt.fps : 16);
-        if (go.fuse > 0) go.fuse &= ~2;  // multi-level F / G: specialised build only
-        if (go.fuse == 0 && opt.fuse > 0) go.fuse = -1;
         if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, go, pl, why)) return false;
         fpc = std::min(go.fps, kLaneSmemCap / std::max(16, pl.lay.smem_bytes));
         while (fpc >= 1) {
