@@ -81,9 +81,11 @@ struct Elem<int8_t> {
 
 // min-sum F: sign(a) sign(b) min(|a|,|b|); a zero product comes out as a
 // signed zero, numerically equal to the reference's 0 (kernels.py:39-48)
+// (one instruction: FMNMX.XORSIGN |a|, |b|)
 __device__ __forceinline__ float f_op(float a, float b) {
-    const unsigned s = (__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u;
-    return __uint_as_float(__float_as_uint(fminf(fabsf(a), fabsf(b))) | s);
+    float d;
+    asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
 }
 
 // G: b + (1 - 2 beta) a -- one correctly rounded add (kernels.py:51-56);

@@ -102,14 +102,13 @@ __device__ __forceinline__ void set8(uint32_t (&w)[4], int s, int v) {
         if (j == i) w[i] = (w[i] & m) | vv;
 }
 
-// min-sum F with the sign from a product: FMNMX and LOP3 on the ALU pipe,
-// FMUL on the FMA pipe (f_op is three ALU-pipe instructions; the two pipes
-// each take a warp instruction every other cycle).  sign(a*b) = sign(a) ^
-// sign(b) for all finite a, b (LLRs are clamped), zero products included.
+// min-sum F in one instruction: min.xorsign.abs (FMNMX.XORSIGN |a|, |b|) returns
+// min(|a|, |b|) with the XOR of the two signs -- kernels.py:39-48 exactly, zero
+// inputs included (a signed zero, numerically the reference's 0).
 __device__ __forceinline__ float f_op(float a, float b) {
-    const float m = fminf(fabsf(a), fabsf(b));
-    const float s = __fmul_rn(a, b);
-    return __uint_as_float(__float_as_uint(m) | (__float_as_uint(s) & 0x80000000u));
+    float d;
+    asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
 }
 
 // the inverse of okey (an involution on the bit pattern)
