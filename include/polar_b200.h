@@ -108,6 +108,9 @@ typedef struct pb_options {
                                  (lane = frame slot x path slot; at most 32 / pow2(L)); 0 auto (32 / pow2(L),
                                  halved until three warps fit an SM), 1 = one frame per warp (the interpreted
                                  kernel for L <= 16) */
+    int32_t channel_global;   /* specialised lane kernel: 1 = the channel LLRs live in global scratch (read
+                                 through L1 / L2) instead of shared memory, which then holds more warps and
+                                 alpha stages; -1 = shared memory; 0 auto (global for list sizes <= 16) */
 } pb_options;
 
 /* Build a decoder for (code, schedule, list size) on a CUDA device.

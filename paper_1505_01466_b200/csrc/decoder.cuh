@@ -166,7 +166,7 @@ struct __align__(8) LOp {
 static_assert(sizeof(LOp) == 8, "LOp is one 8-byte load");
 
 struct LLayout {
-    int ch_off;               // channel, N elements of T (shared memory)
+    int ch_off;               // channel(s), N elements of T per frame (shared memory, or global: ch_gl)
     int a_off[kMaxLog];       // stored alpha stage s: quad-interleaved rows, 32 rows
     uint32_t a_gl;            // bit s: stage s in global scratch
     int b_off[kMaxLog];       // beta slot s: 32 rows of b_stride[s] words
@@ -178,6 +178,8 @@ struct LLayout {
     int hard_off;             // global: uint32 [hard_words][32] hard decisions of leaves wider than 32
     int smem_bytes;           // per frame (16-byte multiple)
     int gbytes;               // per frame global scratch (256-byte multiple)
+    int ch_gl;                // 1: the channel lives in global scratch (ch_off is an offset there): list sizes
+                              // <= 16, where the frames sharing a warp would otherwise fill shared memory
 };
 
 struct LParams {

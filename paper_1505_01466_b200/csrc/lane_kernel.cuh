@@ -155,7 +155,7 @@ struct Fr {
     }
     // this lane's frame's channel: quad x at channel() + x * CQ
     __device__ __forceinline__ T *channel() const {
-        return reinterpret_cast<T *>(sm + LK_LAY(P).ch_off) + (G == 1 ? 0 : 4 * (lane / LP));
+        return reinterpret_cast<T *>((LK_LAY(P).ch_gl ? gs : sm) + LK_LAY(P).ch_off) + (G == 1 ? 0 : 4 * (lane / LP));
     }
     // hard-decision words of leaves wider than 32 (global scratch): word w of
     // lane q's path at [w * 32 + q]
@@ -1523,7 +1523,8 @@ __device__ __forceinline__ void lane_body(const LParams &P) {
         };
 #pragma unroll 1
         for (int g = 0; g < G; ++g)
-            load_channel_lane<T>(P, reinterpret_cast<T *>(sm + LK_LAY(P).ch_off) + 4 * g, frame_of(g), lane);
+            load_channel_lane<T>(P, reinterpret_cast<T *>((LK_LAY(P).ch_gl ? gs : sm) + LK_LAY(P).ch_off) + 4 * g,
+                                 frame_of(g), lane);
         __syncwarp();
         int np = 1;
         run_ops(F, np);

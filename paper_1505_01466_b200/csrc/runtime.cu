@@ -169,7 +169,7 @@ bool is_device_ptr(const void *p) {
 
 // options of the handle being created (pb_options, zero = default)
 struct Opts {
-    int kernel = 0, warps = 0, fps = 0, sync_every = 0, recompute = 0, chunk = 0, grid_sms = 0, l1_list = 0, fuse = 0, specialize = 0, fpw = 0;
+    int kernel = 0, warps = 0, fps = 0, sync_every = 0, recompute = 0, chunk = 0, grid_sms = 0, l1_list = 0, fuse = 0, specialize = 0, fpw = 0, chg = 0;
 };
 Opts read_opts(const pb_options *o) {
     Opts r;
@@ -186,6 +186,7 @@ Opts read_opts(const pb_options *o) {
     if (o->size == 0 || o->size >= (int)(offsetof(pb_options, fuse) + sizeof(int32_t))) r.fuse = o->fuse;
     if (o->size == 0 || o->size >= (int)(offsetof(pb_options, specialize) + sizeof(int32_t))) r.specialize = o->specialize;
     if (o->size == 0 || o->size >= (int)(offsetof(pb_options, frames_per_warp) + sizeof(int32_t))) r.fpw = o->frames_per_warp;
+    if (o->size == 0 || o->size >= (int)(offsetof(pb_options, channel_global) + sizeof(int32_t))) r.chg = o->channel_global;
     return r;
 }
 // sync_every (ops, power of two) -> the kernels' barrier mask; dflt = mask
@@ -266,7 +267,7 @@ struct LanePlan {
 
 // Pure host part: storage layout and the lowered program (no device).
 static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_ops, const std::vector<pb::DOp> &dprog,
-                       const Opts &opt, LanePlan &out, std::string &why, int G = 1) {
+                       const Opts &opt, LanePlan &out, std::string &why, int G = 1, bool chg = false) {
     using namespace pb::lk;
     (void)L;
     const int es = mode == PB_MODE_F32 ? 4 : 1;
@@ -298,7 +299,11 @@ static bool lane_lower(int N, int n, int L, int mode, const pb_op *ops, int n_op
     const int budget = smem_cap / target_fps / 16 * 16;
     int off = 0, goff = 0;
     lay.ch_off = 0;
-    off = align_up(G * N * es, 16);  // the warp's G frames' channels, interleaved quad by quad
+    lay.ch_gl = chg ? 1 : 0;
+    if (chg)
+        goff = align_up(G * N * es, 256);  // the channels in global scratch (first region)
+    else
+        off = align_up(G * N * es, 16);  // the warp's G frames' channels, interleaved quad by quad
     lay.asg_off = off;
     off = align_up(off + 32, 8);
     lay.met_off = off;
@@ -437,7 +442,11 @@ static bool make_jit_spec(int N, int n, int k, int L, int mode, int has_crc, uin
     // shared memory a warp needs at least: its G channels, the fixed tables, beta slots 0..5 and alpha
     // stages 0..4 (the rest of its share goes to the next alpha stages)
     const int es0 = mode == PB_MODE_F32 ? 4 : 1;
-    auto need = [&](int g) { return g * N * es0 + 1024 + 6 * 132 + 32 * (4 + 4 + 4 + 8 + 16) * es0; };
+    // channels in global scratch (pb_options.channel_global; auto: list sizes <= 16, where the channels of
+    // the frames sharing a warp would fill shared memory -- c3 L=2 9.1 -> 27.6, c3 L=8 9.5 -> 14.5, c1 L=4
+    // 7.5 -> 12.4, c2 L=8 15.5 -> 17.2, c5 L=16 3.5 (interpreted) -> 5.9 Gbit/s; neutral at L=32)
+    const bool chg = opt.chg > 0 || (opt.chg == 0 && L <= 16);
+    auto need = [&](int g) { return (chg ? 0 : g * N * es0) + 1024 + 6 * 132 + 32 * (4 + 4 + 4 + 8 + 16) * es0; };
     int G = opt.fpw > 1 ? std::min(opt.fpw, 32 / Lp) : 1;
     if (opt.fpw == 0 && L <= 16) {
         // auto: every lane a path slot, but at least three warps per SM (measured, Gbit/s: c3 L=2 16 frames
@@ -454,7 +463,7 @@ static bool make_jit_spec(int N, int n, int k, int L, int mode, int has_crc, uin
     }
     while (G & (G - 1)) G &= G - 1;  // a power of two
     if (G > 1) jo.fps = std::max(1, std::min(opt.fps ? opt.fps : 16, kLaneSmemCap / need(G)));
-    if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, jo, pl, why, G)) return false;
+    if (!lane_lower(N, n, L, mode, ops, n_ops, dprog, jo, pl, why, G, chg)) return false;
     sp.G = G;
     const int fps = std::max(1, std::min(32, jo.fps ? jo.fps : 16));
     sp.N = N, sp.n = n, sp.k = k, sp.L = L, sp.mode = mode;

@@ -103,6 +103,11 @@ def test_frames_sharing_a_warp_match_oracle_and_interpreted_kernel(cfg):
     plan = json.loads(dec.plan)["lane_kernel"]
     assert plan["specialised"] and plan["frames_per_warp"] >= 2
     got = dec.decode_batch(feed)
+    # the channels in shared memory instead of global scratch (the default for L <= 16)
+    if N <= 2048:
+        alt = pb.ListDecoder(sch, L, mode=mode, options={"specialize": 1, "frames_per_warp": fpw or 2,
+                                                         "channel_global": -1})
+        assert _same(alt.decode_batch(feed), got)
     twin = pb.ListDecoder(sch, L, mode=mode, options={"kernel": "interpreted"}).decode_batch(feed)
     assert _same(got, twin)
     n_or = min(len(feed), 120)

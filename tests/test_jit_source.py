@@ -41,10 +41,12 @@ def test_small_list_sizes_share_a_warp():
     assert int(m.group(1)) == 8                             # 32 / 4 frames per warp
     src2, _ = pb.specialised_source(sch, 4, options={"frames_per_warp": 2})
     assert int(re.search(r"kJit = \{[^}]*, (\d+)\}", src2).group(1)) == 2
-    # a long code keeps too few frames resident: the lane kernel is not planned
+    # with the channels in shared memory a long code keeps too few frames resident: the lane kernel is
+    # not planned; with them in global scratch (the default for L <= 16) it is
     big = _code(8192, 6112, pb.CRC32, 3.0)
     with pytest.raises(ValueError, match="too few resident frames"):
-        pb.specialised_source(big, 16)
+        pb.specialised_source(big, 16, options={"channel_global": -1})
+    assert int(re.search(r"kJit = \{[^}]*, (\d+)\}", pb.specialised_source(big, 16)[0]).group(1)) == 2
 
 
 def test_invalid_requests_are_rejected():
