@@ -1,23 +1,26 @@
 // lane_kernel.cuh -- lane-per-path Fast-SSC list-CRC decode kernel (sm_100a).
 //
-// One warp decodes one frame; lane q owns path slot q (L <= 32).  Compared
-// with the interpreted multi-shape kernel (decode_kernel.cuh) this one is
-// built for the L > 16 north-star shape around three choices:
+// A warp decodes one frame (L > 16: lane q owns path slot q) or 32/pow2(L)
+// frames (L <= 16: lane = frame slot x path slot; the specialised build).
+// The default list kernel; instantiated generically by lane_inst.cu (every op
+// field read at run time) and per code by the translation unit jit.cu
+// generates (PB_JIT: fields, layout and code constants folded in).  Built
+// around:
 //   * per-path state in registers: metric (f64), the row index of every
 //     alpha stage / beta slot (8-bit fields), the leaf data a survivor needs
 //     from its source (hard word, least reliable positions, parity) --
 //     survivors gather it from the source lane with shuffles
 //     (listdec.py:397-434 lazy copy == inheriting the source's row indices);
-//   * the channel in shared memory and the two top stages n-1, n-2 never
-//     stored: every read recomputes them from the channel (all lanes read
-//     the same channel quad, a broadcast) and the path's beta bits, which
-//     halves the per-frame global scratch (c3 L=32: 144 KB -> 70 KB) so the
-//     resident frames' scratch about fits the L2;
-//   * survivor selection on the high 32 bits of the order-preserving metric
-//     keys (one REDUX per max / min), with an exact 64-bit resolution of the
-//     candidates tied at the threshold (listdec.py:63-100 exactly).
-// Code size is kept small (one code path per op kind and source placement)
-// so the SM's warps hit in the instruction cache.
+//   * the channel in shared memory (global scratch for L <= 16) and the two
+//     top stages n-1, n-2 never stored: every read recomputes them from the
+//     channel and the path's beta bits, which halves the per-frame global
+//     scratch (c3 L=32: 144 KB -> 70 KB);
+//   * leaves that read f / g of their parent's row (the F / G before a leaf
+//     is folded into its reads), dead global stages discarded from the L2;
+//   * survivor selection on the high 27 bits of the order-preserving metric
+//     keys with the lane in the low 5 (one REDUX per max / min), and an exact
+//     64-bit resolution of the candidates tied at the threshold
+//     (listdec.py:63-100 exactly); per frame when frames share a warp.
 #pragma once
 #include "decode_kernel.cuh"
 
@@ -26,7 +29,9 @@
 #ifndef PB_LANE_V2SPEC
 #define PB_LANE_V2SPEC 1
 #endif
-// a survivor's chain rows of at least this many words use the unrolled form
+#ifndef PB_SPLIT_SYNC
+#define PB_SPLIT_SYNC 0
+#endif
 // survivor hand-over by a loop over the set bits (run-time key index: the keys
 // live in local memory) instead of the unrolled predicated form
 #ifndef PB_ASG_LOOP
@@ -36,6 +41,8 @@
 #ifndef PB_SCAN_PIPE
 #define PB_SCAN_PIPE 0
 #endif
+// a survivor's chain rows of at least this many words use the unrolled form
+// (all slot-word loads independent); the specialised build sets 2
 #ifndef PB_CHAIN_CLOSED_MIN
 #define PB_CHAIN_CLOSED_MIN 1000000
 #endif
@@ -1490,10 +1497,17 @@ __device__ __forceinline__ void run_ops(Fr<T> &F, int &np) {
 #else
         exec_op<T>(F, Op<>{o}, np);
 #endif
-        if (P.sync_mask >= 0 && (oi & P.sync_mask) == 0)
-            __syncthreads();  // regroup the CTA's frames (shared instruction fetch)
-        else
+        if (P.sync_mask >= 0 && (oi & P.sync_mask) == 0) {
+#if PB_SPLIT_SYNC
+            // two groups of warps regroup separately (their memory phases drift apart)
+            if (blockDim.x == 512)
+                asm volatile("bar.sync %0, 256;" ::"r"(1 + (int)(threadIdx.x >> 8)) : "memory");
+            else
+#endif
+                __syncthreads();  // regroup the CTA's frames (shared instruction fetch)
+        } else {
             __syncwarp();
+        }
     }
 #if PB_PROFILE
     if (prof) P.op_cycles[LK_C(P, n_ops)] = clock64();

@@ -11,9 +11,11 @@
 //     codeword at the end of the frame
 //   * plans the per-frame storage (shared memory vs global scratch per alpha
 //     stage) for the interpreted kernel and the lane-per-path kernel
-//     (plan_lane), sizes the persistent grids, stages host buffers, orders
-//     launches that share a handle's scratch, times launches.  Every knob is
-//     an explicit pb_options field (no environment reads).
+//     (lane_lower / plan_lane: frames per warp, channel placement, fused
+//     leaves, last readers), has jit.cu compile the lane kernel for the code
+//     (make_jit_spec), sizes the persistent grids, stages host buffers,
+//     orders launches that share a handle's scratch, times launches.  Every
+//     knob is an explicit pb_options field (no environment reads).
 #include <cuda_runtime.h>
 
 #include <algorithm>
