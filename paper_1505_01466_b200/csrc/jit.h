@@ -32,7 +32,6 @@ enum : int {
     POL_CHAIN_LEVELS = 4,  // Combine chains level by level (default: the unrolled form, all loads independent:
                            // c3 L=32 4.49 -> 4.62 Gbit/s)
     POL_SCAN_PIPE2 = 8,    // wide-leaf scans software-pipelined over blocks of 2 quads (default)
-    POL_SPLIT_SYNC = 128,  // the CTA's two halves regroup separately
     POL_ASG_LOOP = 64,     // survivor hand-over as a loop over set bits (keys in local memory; default at L <= 2)
 };
 
