@@ -132,3 +132,21 @@ def test_frames_sharing_a_warp_paths_and_adaptive():
     rb = pb.AdaptiveDecoder(sch, 8, options={"kernel": "interpreted"}).decode_batch(fb.llrs)
     for f in FIELDS + ("invoked_list",):
         assert np.array_equal(getattr(ra, f), getattr(rb, f))
+
+
+def test_damaged_cached_cubin_is_recompiled(tmp_path, monkeypatch):
+    """A cubin in the cache that does not load is replaced by a fresh compilation."""
+    import os
+    monkeypatch.setenv("PB_JIT_CACHE", str(tmp_path))
+    spec = pb.CodeSpec.from_design_ebn0(64, 30, pb.CRC8, 2.0)
+    sch = pb.build_schedule(spec)
+    pb.prebuild_specialised(sch, 18)
+    (name,) = [f for f in os.listdir(tmp_path) if f.endswith(".cubin")]
+    good = os.path.getsize(tmp_path / name)
+    with open(tmp_path / name, "wb") as fh:
+        fh.write(b"not a cubin" * 100)
+    llr = pb.generate_frames(spec, 2.0, seed=4, start=0, count=50).llrs
+    dec = pb.ListDecoder(sch, 18, options={"specialize": 1})
+    assert json.loads(dec.plan)["lane_kernel"]["specialised"]
+    assert _same(dec.decode_batch(llr), oracle.decode_batch(sch, 18, llr, threads=2))
+    assert os.path.getsize(tmp_path / name) > good // 2   # rewritten
