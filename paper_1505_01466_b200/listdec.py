@@ -246,7 +246,9 @@ class ListDecoder:
         ``frames_per_sm``, ``sync_every``, ``recompute_stages``,
         ``chunk_frames``, ``grid_sms``, ``l1_list_kernel``, ``fuse``,
         ``specialize`` (the lane kernel compiled per code with NVRTC: 0 auto /
-        -1 off / 1 required); omitted = the measured defaults, merged over
+        -1 off / 1 required), ``frames_per_warp`` (list sizes <= 16: frames
+        sharing a warp, 0 auto), ``channel_global`` (channel LLRs in global
+        scratch, 0 auto); omitted = the measured defaults, merged over
         ``set_default_options``.  Nothing is read from the environment.
     """
 
