@@ -72,3 +72,26 @@ def test_no_gpu_is_a_loud_runtime_error():
     sch = pb.build_schedule(pb.CodeSpec.construct(16, 8, None))
     with pytest.raises(RuntimeError):
         pb.ListDecoder(sch, 4)
+
+
+def test_options_struct_is_forward_compatible():
+    """pb_options.size: a caller built against an older header (a shorter
+    struct) gets the defaults for the fields added since, whatever lies behind
+    its struct in memory."""
+    spec = pb.CodeSpec.from_design_ebn0(256, 100, pb.CRC16, 2.0)
+    sch = pb.build_schedule(spec)
+    default_src, _ = pb.specialised_source(sch, 24)
+    lib = _native.lib()
+    code, ops, n, _keep = pb.listdec._marshal_code(sch)
+    old = _native.PbOptions()
+    old.size = _native.PbOptions.l1_list_kernel.offset + 4      # the round-1 layout
+    old.fuse, old.specialize, old.frames_per_warp, old.channel_global = -1, 3, 7, 1   # "garbage" past its end
+    need = ctypes.c_int64()
+    assert lib.pb_jit_source(ctypes.byref(code), ops, n, 24, 0, ctypes.byref(old), None, 0,
+                             ctypes.byref(need), None) == _native.PB_OK
+    buf = ctypes.create_string_buffer(need.value)
+    assert lib.pb_jit_source(ctypes.byref(code), ops, n, 24, 0, ctypes.byref(old), buf, need.value,
+                             None, None) == _native.PB_OK
+    assert buf.value.decode() == default_src
+    # the same fields are honoured when the struct is long enough
+    assert pb.specialised_source(sch, 24, options={"fuse": -1})[0] != default_src
