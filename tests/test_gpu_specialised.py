@@ -150,3 +150,20 @@ def test_damaged_cached_cubin_is_recompiled(tmp_path, monkeypatch):
     assert json.loads(dec.plan)["lane_kernel"]["specialised"]
     assert _same(dec.decode_batch(llr), oracle.decode_batch(sch, 18, llr, threads=2))
     assert os.path.getsize(tmp_path / name) > good // 2   # rewritten
+
+
+def test_bench_configurations_run_prebuilt_specialised_kernels():
+    """What bench.py measures: the automatic choice (specialize = 0) compiles
+    nothing on the GPU box -- build() put the cubins next to the library --
+    and picks frames per warp / channel placement by list size."""
+    want = {32: (1, False), 8: (4, True), 2: (16, True)}
+    spec = pb.CodeSpec.from_design_ebn0(2048, 1691, pb.CRC32, 4.0)
+    sch = pb.build_schedule(spec)
+    for L, (fpw, chg) in want.items():
+        dec = pb.ListDecoder(sch, L, options={"specialize": 0})
+        lane = json.loads(dec.plan)["lane_kernel"]
+        assert lane and lane["specialised"], (L, json.loads(dec.plan).get("lane_kernel_why"))
+        assert lane["specialised"]["cache_hit"], f"L={L}: the prebuilt cubin was not found"
+        assert lane["frames_per_warp"] == fpw
+        # channels in global scratch: the warp's shared-memory block holds no 8 KB channel
+        assert (lane["smem_per_frame"] < 12000) == chg
